@@ -1,0 +1,185 @@
+/*
+ * paces_b200.h -- C ABI of the B200-native paces adapt-evolve-truncate timestep.
+ *
+ * This is the drop-in boundary.  The reference (arxiv 2603.07341, "paces") has no FFI layer: its
+ * operator API is the set of inline C++ free functions in namespace paces that run()/step() and the
+ * reference tests call.  Every entry point below names the reference function it replaces
+ * (file:line relative to /root/reference/proj/include/paces/).  include/paces_b200.hpp re-creates the
+ * reference's C++ signatures on top of this header; paper_2603_07341_b200/ binds it with ctypes.
+ *
+ * Conventions
+ *   - Every function returns 0 on success.  Nonzero: PB200_ERR_PACES means the reference would have
+ *     thrown paces::Error (common.hpp:21-24) and pb200_last_error() holds the same text (tests grep
+ *     "memory cap", "reduce dt", ...); PB200_ERR_CUDA is a CUDA runtime failure; PB200_ERR_ARG is a
+ *     misuse of this ABI (null pointer, call out of order).
+ *   - Layouts are the reference's: keys are row-major rows x Omega uint32 words, lexicographically
+ *     sorted, no duplicates (basis_codec.hpp:206-238); coefficients are interleaved (re, im) doubles
+ *     (std::complex<double>); CSR is int64 row_ptr[n+1] / int32 col[nnz] ascending per row /
+ *     double val[nnz] (subspace.hpp:25-32).  All pointers are HOST pointers owned by the caller; the
+ *     context owns every device allocation; no allocation crosses the ABI.
+ *   - A context drives one GPU on one stream and is not re-entrant; independent contexts may run
+ *     concurrently.  There is no CPU fallback: pb200_ctx_create fails when no sm_100
+ *     device is visible.
+ */
+#ifndef PACES_B200_H
+#define PACES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB200_OK 0
+#define PB200_ERR_PACES 1
+#define PB200_ERR_CUDA 2
+#define PB200_ERR_ARG 3
+
+typedef struct pb200_ctx pb200_ctx;
+
+/* RunConfig (engine.hpp:34-64) flattened; identical field meaning. */
+typedef struct pb200_run_cfg {
+    int32_t init_kind;  /* InitialStateSpec::Kind: 0 localized, 1 optical, 2 explicit list (engine.hpp:25-32) */
+    int64_t init_site;  /* localized: lattice site, -1 = centre (engine.hpp:173-178) */
+    int32_t m_init;
+    int32_t m;
+    uint64_t q_nom;
+    double dt;
+    double rtol;
+    int32_t max_order;
+    int32_t substeps;
+    double t_max;
+    uint64_t seed;
+    uint64_t cadence;
+    uint64_t n_entries;        /* explicit list: n_entries occupation vectors of layout-site length */
+    const uint32_t* entry_occ; /* n_entries x layout_sites */
+    const double* entry_amp;   /* n_entries x (re, im) */
+} pb200_run_cfg;
+
+/* DiagnosticsRecord (engine.hpp:67-77). */
+typedef struct pb200_diag {
+    uint64_t step;
+    double t;
+    double norm_pre;
+    double norm_post;
+    double discarded_weight;
+    double delta_norm_expmv;
+    double energy;
+    uint64_t q_true;
+    int32_t taylor_order;
+    int32_t pad_;
+} pb200_diag;
+
+/* Device-time breakdown of the resident step (CUDA events on the context's stream), cumulative
+ * since pb200_run_begin; the phases are those of SURVEY 3.5. */
+typedef struct pb200_phase_times {
+    double select_ms, grow_ms, assemble_ms, remap_ms, expectation_ms, expmv_ms, total_ms;
+    uint64_t spmv_nnz;      /* sum over Taylor orders of nnz(H_eff) */
+    uint64_t taylor_orders; /* number of fused Taylor-order launches */
+    uint64_t kernel_launches;
+    uint64_t steps;
+} pb200_phase_times;
+
+/* ---- context ------------------------------------------------------------------------------- */
+int pb200_ctx_create(int device, pb200_ctx** out);
+void pb200_ctx_destroy(pb200_ctx* ctx);
+/* Message of the last failing call on ctx (ctx == NULL: of the last failing pb200_ctx_create). */
+const char* pb200_last_error(const pb200_ctx* ctx);
+const char* pb200_version(void);
+/* Optional externally owned CUDA stream (cudaStream_t as void*); default: a stream the ctx creates. */
+int pb200_ctx_set_stream(pb200_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context has launched so far. */
+uint64_t pb200_kernel_launches(const pb200_ctx* ctx);
+/* common.hpp:76-81 (host-side splitmix64; the per-step tie-break seed of engine.hpp:275). */
+uint64_t pb200_mix_seed(uint64_t x);
+
+/* ---- model: build_model (lattice_models.hpp:140-189) ---------------------------------------------
+ * kind: 0 tight_binding, 1 holstein.  eps/hop/omega/g hold 0, 1 or n values (broadcast rule of
+ * lattice_models.hpp:129-136; hop is per bond in LatticeGeometry::bonds() order, :54-65).  The
+ * spin-lattice kind is rejected exactly as initialize() rejects it (engine.hpp:238-239). */
+int pb200_model_set(pb200_ctx* ctx, int kind, int ndim, const uint32_t* extents, const double* eps,
+                    int n_eps, const double* hop, int n_hop, const double* omega, int n_omega,
+                    const double* g, int n_g, uint32_t d_pho);
+int pb200_model_info(const pb200_ctx* ctx, uint32_t* layout_sites, uint32_t* words_per_row,
+                     uint32_t* lattice_sites, uint32_t* n_terms, uint32_t* total_bits);
+/* pack_state / unpack_state (basis_codec.hpp:131-172), host-side. */
+int pb200_pack(const pb200_ctx* ctx, const uint32_t* occ, uint32_t* words);
+int pb200_unpack(const pb200_ctx* ctx, const uint32_t* words, uint32_t* occ);
+/* apply_terms (lattice_models.hpp:212-267) for n_keys keys on the device: per key up to `cap`
+ * (neighbour key, amplitude) pairs in the reference's emission order, count[i] of them. */
+int pb200_apply_terms(pb200_ctx* ctx, const uint32_t* keys, uint64_t n_keys, uint32_t* out_keys,
+                      double* out_amps, int cap, int* count);
+
+/* ---- stand-alone operators: host buffers in, host buffers out ---------------------------------
+ * Each uploads its inputs, runs the same kernels as the resident step and downloads the result. */
+
+/* grow_subspace (subspace.hpp:195-249) incl. assemble_effective_hamiltonian (:142-187).  The grown
+ * space stays resident as the context's current space; read it with pb200_space_info/_get. */
+int pb200_grow(pb200_ctx* ctx, const uint32_t* seeds, uint64_t rows, int order, uint64_t* q_true,
+               uint64_t* nnz);
+int pb200_space_info(const pb200_ctx* ctx, uint64_t* q_true, uint64_t* nnz, uint64_t* q_nom);
+int pb200_space_get(pb200_ctx* ctx, uint32_t* words, int64_t* row_ptr, int32_t* col, double* val);
+
+/* truncate_select (engine.hpp:107-156): out_words has room for min(rows, q_nom) rows. */
+int pb200_truncate_select(pb200_ctx* ctx, const uint32_t* words, const double* coeff, uint64_t rows,
+                          uint64_t q_nom, uint64_t seed, uint32_t* out_words, uint64_t* kept);
+/* remap_state (subspace.hpp:281-305). */
+int pb200_remap(pb200_ctx* ctx, const uint32_t* src_words, const double* src_coeff,
+                uint64_t src_rows, const uint32_t* dst_words, uint64_t dst_rows, double* out_coeff,
+                double* discarded);
+/* csr_matvec (subspace.hpp:35-43), csr_expectation (:46-55), expmv (propagator.hpp:52-92). */
+int pb200_csr_matvec(pb200_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                     const double* val, const double* x, double* y);
+int pb200_csr_expectation(pb200_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                          const double* val, const double* x, double* out);
+int pb200_expmv(pb200_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                const double* val, double* c, double dt, double rtol, int max_order, int substeps,
+                int* order_used, double* last_term_norm);
+/* state_norm (subspace.hpp:91-95), exciton_density (observables.hpp:26-37), dipole_amplitude
+ * (observables.hpp:99-112), phonon_numbers (observables.hpp:84-95). */
+int pb200_state_norm(pb200_ctx* ctx, const double* coeff, uint64_t rows, double* out);
+int pb200_exciton_density(pb200_ctx* ctx, const uint32_t* words, const double* coeff, uint64_t rows,
+                          double* p);
+int pb200_dipole_amplitude(pb200_ctx* ctx, const uint32_t* words, const double* coeff,
+                           uint64_t rows, double* amp);
+int pb200_phonon_numbers(pb200_ctx* ctx, const uint32_t* words, const double* coeff, uint64_t rows,
+                         double* n_out);
+
+/* ---- device-resident trajectory: initialize / step / run (engine.hpp:235-291, 318-375) ----------
+ * pb200_run_begin = initialize(): seed state, grow to m_init, remap.  pb200_run_step advances one
+ * timestep exactly as run() does: step 1 evolves on the m_init space (engine.hpp:335-352), steps >= 2
+ * are step() (engine.hpp:268-291).  State and space stay in HBM between steps; a failing step leaves
+ * the last good state current (engine.hpp:263-267) and reports the reference's message. */
+int pb200_run_begin(pb200_ctx* ctx, const pb200_run_cfg* cfg);
+int pb200_run_step(pb200_ctx* ctx, pb200_diag* out);
+int pb200_run_info(const pb200_ctx* ctx, uint64_t* rows, uint64_t* nnz, double* t,
+                   uint64_t* steps_done);
+/* Canonical-order download: keys ascending, coefficients aligned (checkpoint order, io.hpp:77-99). */
+int pb200_run_state(pb200_ctx* ctx, uint32_t* words, double* coeff);
+int pb200_run_csr(pb200_ctx* ctx, int64_t* row_ptr, int32_t* col, double* val);
+/* Replace the resident state/space by a host-supplied pair (checkpoint resume; also how bench.py
+ * feeds a synthetic subspace): the space is re-grown from `words` with order 0?  No -- the table is
+ * taken as is and H_eff is assembled over it (grow_subspace with m = 0, subspace.hpp:209 skipped). */
+int pb200_run_load_state(pb200_ctx* ctx, const pb200_run_cfg* cfg, const uint32_t* words,
+                         const double* coeff, uint64_t rows, double t, uint64_t steps_done);
+/* detail::observe (engine.hpp:299-311): ObservablesRow of the resident state; density has
+ * lattice_sites entries, amp is (re, im). */
+int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar,
+                      double* amp, double* density);
+int pb200_run_times(const pb200_ctx* ctx, pb200_phase_times* out);
+int pb200_run_reset_times(pb200_ctx* ctx);
+
+/* ---- measurement helpers (bench.py) -----------------------------------------------------------
+ * Runs `orders` fused Taylor-order launches (SpMV + scale + axpy + two norms, propagator.hpp:68-77)
+ * on the resident space with the stop rule disabled, timing them with CUDA events on the context's
+ * stream; the resident state is restored afterwards.  flush_l2 != 0 overwrites a buffer larger than
+ * L2 between launches (outside the timed intervals). */
+int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush_l2, double dt, double* ms_per_order,
+                       uint64_t* nnz, uint64_t* rows);
+/* Same for the plain SpMV y = H x (subspace.hpp:35-43). */
+int pb200_bench_spmv(pb200_ctx* ctx, int reps, int flush_l2, double* ms_per_spmv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

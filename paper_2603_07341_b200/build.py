@@ -1,0 +1,54 @@
+"""Builds libpaces_b200.so (hand-written sm_100a CUDA + the C ABI of include/paces_b200.h) with nvcc.
+
+The library is built IN-TREE (paper_2603_07341_b200/libpaces_b200.so) so it travels to the GPU box with the
+repo snapshot.  nvcc cross-compiles without a GPU.  -fmad=false: the reference binary contains no FMA
+(proj/CMakeLists.txt:6-8) and bit-exact amplitudes need the same (the kernels also use explicit
+__dmul_rn/__dadd_rn).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libpaces_b200.so")
+SOURCES = ["paces_b200.cu"]
+DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "kernels.cuh", "keys.cuh", "primitives.cuh",
+        "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
+              "-Xcompiler", "-fPIC,-O2", "-shared"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.exists(os.path.join(CSRC, d)) and os.path.getmtime(os.path.join(CSRC, d)) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    if verbose:
+        cmd += ["-Xptxas", "-v"]
+    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libpaces_b200.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

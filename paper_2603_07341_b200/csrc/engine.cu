@@ -1,0 +1,645 @@
+// engine.cu -- implementation of the device-resident paces step (see engine.cuh, kernels.cuh).
+#include "engine.cuh"
+
+namespace pb {
+
+#define PB_DISPATCH_W(Wv, ...)                                  \
+    switch (Wv) {                                               \
+        case 1: { constexpr int W = 1; __VA_ARGS__; } break;    \
+        case 2: { constexpr int W = 2; __VA_ARGS__; } break;    \
+        case 3: { constexpr int W = 3; __VA_ARGS__; } break;    \
+        case 4: { constexpr int W = 4; __VA_ARGS__; } break;    \
+        case 5: { constexpr int W = 5; __VA_ARGS__; } break;    \
+        case 6: { constexpr int W = 6; __VA_ARGS__; } break;    \
+        case 7: { constexpr int W = 7; __VA_ARGS__; } break;    \
+        case 8: { constexpr int W = 8; __VA_ARGS__; } break;    \
+        case 9: { constexpr int W = 9; __VA_ARGS__; } break;    \
+        case 10: { constexpr int W = 10; __VA_ARGS__; } break;  \
+        case 11: { constexpr int W = 11; __VA_ARGS__; } break;  \
+        case 12: { constexpr int W = 12; __VA_ARGS__; } break;  \
+        case 13: { constexpr int W = 13; __VA_ARGS__; } break;  \
+        case 14: { constexpr int W = 14; __VA_ARGS__; } break;  \
+        case 15: { constexpr int W = 15; __VA_ARGS__; } break;  \
+        case 16: { constexpr int W = 16; __VA_ARGS__; } break;  \
+        default: throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build"); \
+    }
+
+// ------------------------------------------------------------------------------------------------
+Engine::Engine(int dev) : device(dev) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw CudaFail(std::string("no CUDA device visible (") + cudaGetErrorString(e) +
+                       "); paces_b200 has no CPU fallback");
+    if (dev < 0 || dev >= count) throw ArgError("device index out of range");
+    PB_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop{};
+    PB_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+        throw CudaFail(std::string("device ") + prop.name + " is sm_" + std::to_string(prop.major) +
+                       std::to_string(prop.minor) + "; this library is built for sm_100a (B200) only");
+    sm_count = prop.multiProcessorCount;
+    PB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    PB_CUDA(cudaMallocHost(&pinned, 4096));
+    for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
+    ctl.ensure(sizeof(Ctl));
+    PB_CUDA(cudaMemsetAsync(ctl.p, 0, sizeof(Ctl), stream));
+    partials.ensure(sizeof(double) * 4 * size_t(sm_count) * 8);
+    hist.ensure(256 * sizeof(uint32_t));
+    PB_CUDA(cudaMemsetAsync(hist.p, 0, 256 * sizeof(uint32_t), stream));
+    sync();
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& x : ev)
+        if (x) cudaEventDestroy(x);
+    if (pinned) cudaFreeHost(pinned);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void Engine::exclusive_scan(uint32_t* data, uint64_t n) {
+    if (n == 0) return;
+    const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    scan_tiles.ensure(ntiles * sizeof(uint32_t));
+    scan_tile_sums_kernel<<<unsigned(ntiles), NT, 0, stream>>>(data, n, scan_tiles.as<uint32_t>());
+    check_launch();
+    scan_spine_kernel<<<1, 1024, 0, stream>>>(scan_tiles.as<uint32_t>(), uint32_t(ntiles));
+    check_launch();
+    scan_apply_kernel<<<unsigned(ntiles), NT, 0, stream>>>(data, n, scan_tiles.as<uint32_t>(), data);
+    check_launch();
+}
+
+// ------------------------------------------------------------------------------------------------
+void Engine::set_model(const HostModel& m) {
+    hm = m;
+    const size_t L = m.L;
+    std::vector<int> nbs(L * MAX_NB, -1);
+    std::vector<double> nba(L * MAX_NB, 0.0);
+    std::vector<int> deg(L, 0);
+    std::vector<std::vector<std::pair<uint32_t, double>>> adj(L);
+    for (size_t b = 0; b < m.bonds.size(); ++b) {
+        if (m.hop[b] == 0.0) continue;  // zero parameters produce no term (lattice_models.hpp:163)
+        adj[m.bonds[b].first].push_back({m.bonds[b].second, m.hop[b]});
+        adj[m.bonds[b].second].push_back({m.bonds[b].first, m.hop[b]});
+    }
+    int max_deg = 0;
+    for (size_t s = 0; s < L; ++s) {
+        std::sort(adj[s].begin(), adj[s].end());
+        if (adj[s].size() > size_t(MAX_NB)) throw PacesError("lattice site with more than 6 bonds");
+        for (size_t d = 0; d < adj[s].size(); ++d) {
+            nbs[s * MAX_NB + d] = int(adj[s][d].first);
+            nba[s * MAX_NB + d] = adj[s][d].second;
+        }
+        max_deg = std::max(max_deg, int(adj[s].size()));
+    }
+    std::vector<double> om = m.omega, gg = m.g;
+    if (om.empty()) om.assign(L, 0.0);
+    if (gg.empty()) gg.assign(L, 0.0);
+    d_eps.ensure(L * 8);
+    d_omega.ensure(L * 8);
+    d_g.ensure(L * 8);
+    d_nbs.ensure(L * MAX_NB * 4);
+    d_nba.ensure(L * MAX_NB * 8);
+    PB_CUDA(cudaMemcpyAsync(d_eps.p, m.eps.data(), L * 8, cudaMemcpyHostToDevice, stream));
+    PB_CUDA(cudaMemcpyAsync(d_omega.p, om.data(), L * 8, cudaMemcpyHostToDevice, stream));
+    PB_CUDA(cudaMemcpyAsync(d_g.p, gg.data(), L * 8, cudaMemcpyHostToDevice, stream));
+    PB_CUDA(cudaMemcpyAsync(d_nbs.p, nbs.data(), L * MAX_NB * 4, cudaMemcpyHostToDevice, stream));
+    PB_CUDA(cudaMemcpyAsync(d_nba.p, nba.data(), L * MAX_NB * 8, cudaMemcpyHostToDevice, stream));
+    sync();
+    md.kind = m.kind;
+    md.L = int(L);
+    md.nph = (m.kind == 1) ? int(L) : 0;
+    md.b0 = m.b0;
+    md.bp = m.bp;
+    md.W = int(m.W);
+    md.d_pho = m.d_pho;
+    md.max_deg = max_deg;
+    md.eps = d_eps.as<double>();
+    md.omega = d_omega.as<double>();
+    md.g = d_g.as<double>();
+    md.nb_site = d_nbs.as<int>();
+    md.nb_amp = d_nba.as<double>();
+    row_width = max_deg + (m.kind == 1 ? 2 : 0) + 1;
+    has_model = true;
+    has_state = false;
+    has_cfg = false;
+    space[0].n = space[1].n = 0;
+    space[0].has_h = space[1].has_h = false;
+    if (m.W > 16) throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build");
+}
+
+// ------------------------------------------------------------------------------------------------
+// grow_subspace (subspace.hpp:195-249)
+// ------------------------------------------------------------------------------------------------
+void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
+    require_model();
+    if (ns == 0) throw PacesError("grow_subspace: empty seed set");
+    if (order < 0) throw PacesError("grow_subspace: neighbor order must be >= 0");
+    const int W = md.W;
+    const int nmoves = md.max_deg + (md.kind == 1 ? 2 : 0);  // off-diagonal moves per key
+    const int count_emitted = memory_cap_bytes() != 0;  // transcript sizes only matter for the cap check
+
+    out.words.ensure(size_t(ns) * W * 4);
+    PB_CUDA(cudaMemcpyAsync(out.words.p, d_seeds, size_t(ns) * W * 4, cudaMemcpyDeviceToDevice, stream));
+    uint32_t n = ns;
+    uint32_t nf = ns;
+    bool identity_frontier = true;
+    int fcur = 0;
+    uint64_t emitted_total = 0;
+    Ctl* c = dctl();
+
+    for (int k = 0; k < order && nf > 0; ++k) {
+        const uint64_t cand_cap64 = uint64_t(nf) * uint64_t(nmoves);
+        if (cand_cap64 == 0) {
+            nf = 0;
+            break;
+        }
+        if (cand_cap64 > 0xfffffff0ull) throw PacesError("subspace growth: candidate count exceeds 32-bit indexing");
+        const uint32_t cand_cap = uint32_t(cand_cap64);
+        cand_keys.ensure(size_t(cand_cap) * W * 4);
+        cand_gap.ensure(size_t(cand_cap) * 4);
+        gap.ensure((size_t(n) + 2) * 4);
+        PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
+        PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
+        const uint32_t* fr = identity_frontier ? nullptr : frontier[fcur].as<uint32_t>();
+        PB_DISPATCH_W(W, expand_level_kernel<W><<<grid_for(nf), NT, 0, stream>>>(
+                             md, out.words.as<uint32_t>(), n, fr, nf, cand_keys.as<uint32_t>(),
+                             cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow, count_emitted));
+        check_launch();
+        GrowCounters gc = read_back<GrowCounters>(&c->grow);
+        if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
+        emitted_total += gc.emitted;
+        const uint32_t nc = gc.n_cand;
+        if (nc == 0) {
+            nf = 0;
+            // the reference still runs its memory check for this order
+            require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
+            break;
+        }
+        // counting sort by insertion gap: gap[] (counts) -> segment starts; row_len[] is the per-gap cursor
+        // during placement and then the per-gap survivor count
+        exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
+        perm.ensure(size_t(nc) * 4);
+        seg_rank.ensure(size_t(nc) * 4);
+        row_len.ensure((size_t(n) + 2) * 4);
+        PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
+        place_candidates_kernel<<<grid_for(nc), NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc, gap.as<uint32_t>(),
+                                                                  row_len.as<uint32_t>(), perm.as<uint32_t>());
+        check_launch();
+        PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
+        PB_DISPATCH_W(W, segment_dedup_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+                             gap.as<uint32_t>(), seg_rank.as<uint32_t>(), row_len.as<uint32_t>(), &c->grow));
+        check_launch();
+        PB_DISPATCH_W(W, segment_rank_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+                             gap.as<uint32_t>(), seg_rank.as<uint32_t>()));
+        check_launch();
+        // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
+        exclusive_scan(row_len.as<uint32_t>(), uint64_t(n) + 2);
+        const uint32_t n_new = read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
+        const uint64_t n_next64 = uint64_t(n) + n_new;
+        if (n_next64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+        tab_tmp.ensure(size_t(n_next64) * W * 4);
+        frontier[fcur ^ 1].ensure(size_t(n_new) * 4 + 4);
+        PB_DISPATCH_W(W, merge_old_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
+                             out.words.as<uint32_t>(), n, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>()));
+        check_launch();
+        PB_DISPATCH_W(W, merge_new_rows_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
+                             seg_rank.as<uint32_t>(), nc, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>(),
+                             frontier[fcur ^ 1].as<uint32_t>()));
+        check_launch();
+        out.words.swap(tab_tmp);
+        fcur ^= 1;
+        identity_frontier = false;
+        n = uint32_t(n_next64);
+        nf = n_new;
+        require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
+    }
+    out.n = n;
+    out.q_nom = ns;
+    out.order = order;
+    PB_CUDA(cudaEventRecord(ev[2], stream));
+    assemble(out);
+}
+
+// ------------------------------------------------------------------------------------------------
+// assemble_effective_hamiltonian (subspace.hpp:142-187), row-wise
+// ------------------------------------------------------------------------------------------------
+void Engine::assemble(Space& sp) {
+    const int W = md.W;
+    const uint32_t n = sp.n;
+    const int width = row_width;
+    tmp_col.ensure(size_t(n) * width * 4);
+    tmp_val.ensure(size_t(n) * width * 8);
+    sp.row_ptr.ensure((size_t(n) + 1) * 4);
+    PB_DISPATCH_W(W, assemble_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
+                         md, sp.words.as<uint32_t>(), n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
+                         sp.row_ptr.as<uint32_t>()));
+    check_launch();
+    PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
+    exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
+    const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
+    // the reference's assembly buffer check: 2 entries of 16 bytes per transcript element (subspace.hpp:152)
+    require_memory(uint64_t(nnz) * 2 * 16, "matrix assembly buffer");
+    sp.col.ensure(size_t(nnz) * 4 + 4);
+    sp.val.ensure(size_t(nnz) * 8 + 8);
+    assemble_compact_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
+                                                            sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                            sp.val.as<double>());
+    check_launch();
+    sp.nnz = nnz;
+    sp.has_h = true;
+}
+
+// ------------------------------------------------------------------------------------------------
+// truncate_select (engine.hpp:107-156)
+// ------------------------------------------------------------------------------------------------
+uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
+                        double* norm2_out) {
+    require_model();
+    if (q_nom < 1) throw PacesError("truncate_select: q_nom must be >= 1");
+    const int W = md.W;
+    Ctl* c = dctl();
+    weights.ensure(size_t(n) * 8 + 8);
+    PB_CUDA(cudaMemsetAsync(hist.p, 0, 256 * sizeof(uint32_t), stream));
+    flag_keep.ensure((size_t(n) + 1) * 4);
+    const int g = grid_for(n);
+    SelectCtl init{};
+    init.k = q_nom;
+    std::memcpy(pinned, &init, sizeof(init));
+    PB_CUDA(cudaMemcpyAsync(&c->select, pinned, sizeof(SelectCtl), cudaMemcpyHostToDevice, stream));
+    weights_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select);
+    check_launch();
+    SelectCtl sc = read_back<SelectCtl>(&c->select);
+    if (norm2_out) *norm2_out = sc.norm2;
+    if (sc.support == 0) throw PacesError("truncate_select: state has no support");
+
+    uint32_t* keep = flag_keep.as<uint32_t>();
+    if (sc.support <= q_nom) {
+        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
+        check_launch();
+    } else {
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            select_hist_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, shift, &c->select, hist.as<uint32_t>());
+            check_launch();
+            select_pick_kernel<<<1, 32, 0, stream>>>(hist.as<uint32_t>(), &c->select);
+            check_launch();
+        }
+        sc = read_back<SelectCtl>(&c->select);
+        const uint64_t need = q_nom - sc.count_gt;  // 1 <= need <= count_eq
+        if (need >= sc.count_eq) {
+            // every tie is admitted: the shuffle loop of engine.hpp:138-141 does not run
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr);
+            check_launch();
+        } else {
+            // ties in ascending table index -> host -> seeded Fisher-Yates exactly as engine.hpp:137-142
+            flag_tie.ensure((size_t(n) + 1) * 4);
+            pos_a.ensure((size_t(n) + 1) * 4);
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 0, keep,
+                                                      flag_tie.as<uint32_t>());
+            check_launch();
+            PB_CUDA(cudaMemcpyAsync(pos_a.p, flag_tie.p, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
+            exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+            const uint32_t nt = uint32_t(sc.count_eq);
+            idx_tmp.ensure(size_t(nt) * 4 + 4);
+            compact_index_kernel<<<g, NT, 0, stream>>>(flag_tie.as<uint32_t>(), pos_a.as<uint32_t>(), n,
+                                                       idx_tmp.as<uint32_t>());
+            check_launch();
+            std::vector<uint32_t> ties(nt);
+            PB_CUDA(cudaMemcpyAsync(ties.data(), idx_tmp.p, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+            sync();
+            std::mt19937_64 rng(seed);
+            for (size_t i = ties.size(); i > 1 && need < ties.size(); --i) {
+                const size_t j = size_t(rng() % i);
+                std::swap(ties[i - 1], ties[j]);
+            }
+            PB_CUDA(cudaMemcpyAsync(idx_tmp.p, ties.data(), size_t(need) * 4, cudaMemcpyHostToDevice, stream));
+            set_flags_kernel<<<grid_for(need), NT, 0, stream>>>(idx_tmp.as<uint32_t>(), uint32_t(need), keep);
+            check_launch();
+            sync();  // `ties` must outlive the copy
+        }
+    }
+    pos_a.ensure((size_t(n) + 1) * 4);
+    PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
+    exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+    const uint32_t kept = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
+    seeds.ensure(size_t(kept) * W * 4 + 4);
+    PB_DISPATCH_W(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,
+                                                                  seeds.as<uint32_t>()));
+    check_launch();
+    n_seeds = kept;
+    return kept;
+}
+
+// ------------------------------------------------------------------------------------------------
+// remap_state (subspace.hpp:281-305)
+// ------------------------------------------------------------------------------------------------
+double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
+                     uint32_t nd, double2* dst_c) {
+    const int W = md.W;
+    Ctl* c = dctl();
+    PB_CUDA(cudaMemsetAsync(dst_c, 0, size_t(nd) * 16, stream));
+    PB_DISPATCH_W(W, remap_kernel<W><<<grid_for(ns), NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, dst_c,
+                                                                      partials.as<double>(), &c->ticket, c->out));
+    check_launch();
+    return read_back<double>(c->out);
+}
+
+// ------------------------------------------------------------------------------------------------
+void Engine::expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite) {
+    Ctl* c = dctl();
+    expectation_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                          sp.val.as<double>(), x, partials.as<double>(), &c->ticket,
+                                                          c->out);
+    check_launch();
+    struct R {
+        double v[3];
+    };
+    R r = read_back<R>(c->out);
+    if (exp_out) *exp_out = r.v[0];
+    if (norm2_out) *norm2_out = r.v[1];
+    if (check_finite && r.v[2] != 0.0) throw PacesError("expmv: non-finite input coefficient");
+}
+
+void Engine::spmv(const Space& sp, const double2* x, double2* y) {
+    spmv_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                   sp.val.as<double>(), x, y);
+    check_launch();
+}
+
+// ------------------------------------------------------------------------------------------------
+// expmv (propagator.hpp:52-92)
+// ------------------------------------------------------------------------------------------------
+void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
+                   int* order_used, double* last_term_norm, double* last_c_norm) {
+    if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
+    if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
+    if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
+    if (substeps < 1) throw PacesError("propagator: substeps must be >= 1");
+    const uint32_t n = sp.n;
+    Ctl* c = dctl();
+    term[0].ensure(size_t(n) * 16 + 16);
+    term[1].ensure(size_t(n) * 16 + 16);
+    const double dt_sub = dt / substeps;
+    const int g = grid_for(n);
+    TaylorCtl tc{};
+    PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
+    for (int s = 0; s < substeps; ++s) {
+        PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
+        if (s > 0) {
+            // new substep: streak and done restart, order_used keeps its running maximum
+            tc.done = 0;
+            tc.streak = 0;
+            tc.ticket = 0;
+            std::memcpy(pinned, &tc, sizeof(tc));
+            PB_CUDA(cudaMemcpyAsync(&c->taylor, pinned, sizeof(TaylorCtl), cudaMemcpyHostToDevice, stream));
+        }
+        int order = 1;
+        bool converged = false;
+        // launch in batches; the stop rule runs on the device and turns the tail of a batch into no-ops
+        int batch = last_order > 2 ? last_order : 8;
+        while (order <= max_order) {
+            const int end = std::min(max_order, order + batch - 1);
+            for (; order <= end; ++order) {
+                const double b = -dt_sub / double(order);
+                taylor_order_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                          sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
+                                                          term[order & 1].as<double2>(), c_vec, b, order, rtol,
+                                                          partials.as<double>(), &c->taylor, 0);
+                check_launch();
+            }
+            tc = read_back<TaylorCtl>(&c->taylor);
+            if (tc.done) {
+                converged = true;
+                break;
+            }
+            batch = 2;
+        }
+        times.taylor_orders += uint64_t(tc.last_order);
+        if (!converged)
+            throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
+                             "; reduce dt or increase substeps");
+    }
+    last_order = tc.order_used;
+    if (order_used) *order_used = tc.order_used;
+    if (last_term_norm) *last_term_norm = tc.last_term_norm;
+    if (last_c_norm) *last_c_norm = tc.last_c_norm;
+}
+
+void Engine::upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val) {
+    if (n < 0 || n > 0x7fffffffLL) throw ArgError("csr: n out of range");
+    const int64_t nnz = row_ptr[n];
+    if (nnz < 0 || nnz > 0xfffffff0LL) throw ArgError("csr: nnz out of range");
+    std::vector<uint32_t> rp(size_t(n) + 1);
+    for (int64_t i = 0; i <= n; ++i) rp[size_t(i)] = uint32_t(row_ptr[i]);
+    sp.row_ptr.ensure((size_t(n) + 1) * 4);
+    sp.col.ensure(size_t(nnz) * 4 + 4);
+    sp.val.ensure(size_t(nnz) * 8 + 8);
+    PB_CUDA(cudaMemcpyAsync(sp.row_ptr.p, rp.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice, stream));
+    if (nnz) {
+        PB_CUDA(cudaMemcpyAsync(sp.col.p, col, size_t(nnz) * 4, cudaMemcpyHostToDevice, stream));
+        PB_CUDA(cudaMemcpyAsync(sp.val.p, val, size_t(nnz) * 8, cudaMemcpyHostToDevice, stream));
+    }
+    sync();
+    sp.n = uint32_t(n);
+    sp.nnz = uint64_t(nnz);
+    sp.has_h = true;
+}
+
+// ------------------------------------------------------------------------------------------------
+// observables (observables.hpp:26-37, 84-95, 99-112)
+// ------------------------------------------------------------------------------------------------
+void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, double* density, double* amp,
+                     double* phonons) {
+    require_model();
+    const int W = md.W;
+    const int L = md.L;
+    const uint32_t rows_per_block = 4096;
+    const uint32_t nb = (n + rows_per_block - 1) / rows_per_block;
+    aux_vec.ensure((size_t(nb) * L + size_t(L) * 3 + 8) * 8);
+    double* block_part = aux_vec.as<double>();
+    double* d_out = block_part + size_t(nb) * L;     // L doubles
+    double2* d_found = reinterpret_cast<double2*>(d_out + L);  // L double2
+    if (density) {
+        PB_CUDA(cudaMemsetAsync(block_part, 0, size_t(nb) * L * 8, stream));
+        if (nb) {
+            PB_DISPATCH_W(W, density_kernel<W><<<nb, NT, 0, stream>>>(md, words, cvec, n, rows_per_block, block_part));
+            check_launch();
+        }
+        density_finish_kernel<<<(L + 127) / 128, 128, 0, stream>>>(block_part, nb, L, d_out);
+        check_launch();
+        PB_CUDA(cudaMemcpyAsync(density, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+    if (phonons) {
+        if (md.kind != 1) throw PacesError("phonon numbers: not a Holstein model");
+        PB_CUDA(cudaMemsetAsync(block_part, 0, size_t(nb) * L * 8, stream));
+        if (nb) {
+            PB_DISPATCH_W(W, phonon_numbers_kernel<W><<<nb, NT, 0, stream>>>(md, words, cvec, n, rows_per_block,
+                                                                            block_part));
+            check_launch();
+        }
+        density_finish_kernel<<<(L + 127) / 128, 128, 0, stream>>>(block_part, nb, L, d_out);
+        check_launch();
+        PB_CUDA(cudaMemcpyAsync(phonons, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+    if (amp) {
+        PB_DISPATCH_W(W, dipole_kernel<W><<<1, 256, 0, stream>>>(md, words, cvec, n, d_found, d_out));
+        check_launch();
+        PB_CUDA(cudaMemcpyAsync(amp, d_out, 16, cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// initialize (engine.hpp:235-251) and the per-step driver (engine.hpp:268-291, 333-368)
+// ------------------------------------------------------------------------------------------------
+static void validate_cfg(const pb200_run_cfg& c) {
+    if (c.m < 0 || c.m_init < c.m) throw PacesError("run: need m_init >= m >= 0");
+    if (c.q_nom < 1) throw PacesError("run: q_nom must be >= 1");
+    if (c.t_max < 0) throw PacesError("run: t_max must be >= 0");
+    if (c.cadence < 1) throw PacesError("run: cadence must be >= 1");
+    if (!(c.dt > 0)) throw PacesError("propagator: dt must be > 0");
+    if (!(c.rtol > 0) || !(c.rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
+    if (c.max_order < 1) throw PacesError("propagator: max_order must be >= 1");
+    if (c.substeps < 1) throw PacesError("propagator: substeps must be >= 1");
+}
+
+void Engine::run_begin(const pb200_run_cfg& c) {
+    require_model();
+    validate_cfg(c);
+    cfg = c;
+    cfg_occ.clear();
+    cfg_amp.clear();
+    if (c.init_kind == 2 && c.n_entries && c.entry_occ && c.entry_amp) {
+        cfg_occ.assign(c.entry_occ, c.entry_occ + c.n_entries * hm.layout_sites());
+        cfg_amp.assign(c.entry_amp, c.entry_amp + 2 * c.n_entries);
+        cfg.entry_occ = cfg_occ.data();
+        cfg.entry_amp = cfg_amp.data();
+    }
+    has_cfg = true;
+    has_state = false;
+    std::vector<uint32_t> words;
+    std::vector<cplx> amps;
+    build_seed_state(hm, c.init_kind, c.init_site, c.n_entries, c.entry_occ, c.entry_amp, words, amps);
+    const uint32_t ns = uint32_t(amps.size());
+    const int W = md.W;
+    aux_words.ensure(words.size() * 4);
+    aux_coeff.ensure(amps.size() * 16);
+    PB_CUDA(cudaMemcpyAsync(aux_words.p, words.data(), words.size() * 4, cudaMemcpyHostToDevice, stream));
+    PB_CUDA(cudaMemcpyAsync(aux_coeff.p, amps.data(), amps.size() * 16, cudaMemcpyHostToDevice, stream));
+    sync();
+    Space& sp = space[cur];
+    grow(aux_words.as<uint32_t>(), ns, c.m_init, sp);
+    coeff[ccur].ensure(size_t(sp.n) * 16 + 16);
+    const double discarded = remap(aux_words.as<uint32_t>(), aux_coeff.as<double2>(), ns, sp.words.as<uint32_t>(),
+                                   sp.n, coeff[ccur].as<double2>());
+    if (discarded != 0) throw PacesError("initialize: seed keys lost during growth");
+    (void)W;
+    t = 0;
+    steps_done = 0;
+    last_order = 0;
+    has_state = true;
+    times = pb200_phase_times{};
+}
+
+void Engine::run_step(pb200_diag* out) {
+    if (!has_state || !has_cfg) throw ArgError("no resident run: call pb200_run_begin first");
+    const uint64_t s = steps_done + 1;
+    pb200_diag rec{};
+    rec.step = s;
+    const uint64_t launches0 = launches;
+    Space& old = space[cur];
+    double2* c_old = coeff[ccur].as<double2>();
+    PB_CUDA(cudaEventRecord(ev[0], stream));
+    if (s == 1) {
+        // engine.hpp:335-352: the m_init space is the effective space of the first evolution
+        double e = 0, n2 = 0;
+        expectation(old, c_old, &e, &n2, true);
+        PB_CUDA(cudaEventRecord(ev[5], stream));
+        rec.norm_pre = std::sqrt(n2);
+        rec.norm_post = rec.norm_pre;
+        rec.q_true = old.n;
+        rec.energy = e;
+        coeff[ccur ^ 1].ensure(size_t(old.n) * 16 + 16);
+        double2* psi = coeff[ccur ^ 1].as<double2>();
+        PB_CUDA(cudaMemcpyAsync(psi, c_old, size_t(old.n) * 16, cudaMemcpyDeviceToDevice, stream));
+        int order = 0;
+        double ltn = 0, lcn = 0;
+        expmv(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        PB_CUDA(cudaEventRecord(ev[6], stream));
+        sync();
+        rec.taylor_order = order;
+        rec.delta_norm_expmv = lcn - rec.norm_post;
+        ccur ^= 1;
+        float ms = 0;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[5]));
+        times.expectation_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[5], ev[6]));
+        times.expmv_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[6]));
+        times.total_ms += ms;
+        times.spmv_nnz += uint64_t(order) * old.nnz;
+    } else {
+        // engine.hpp:268-291
+        Space& next = space[cur ^ 1];
+        double n2_pre = 0;
+        const uint32_t kept = select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, pb200_mix_seed(cfg.seed + s),
+                                     &n2_pre);
+        rec.norm_pre = std::sqrt(n2_pre);
+        PB_CUDA(cudaEventRecord(ev[1], stream));
+        // grow() = expansion + assembly; split the timer inside via ev[2]
+        grow(seeds.as<uint32_t>(), kept, cfg.m, next);
+        PB_CUDA(cudaEventRecord(ev[3], stream));
+        require_memory(uint64_t(next.n) * 16 * 4, "state vectors");
+        coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
+        double2* psi = coeff[ccur ^ 1].as<double2>();
+        rec.discarded_weight =
+            remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+        PB_CUDA(cudaEventRecord(ev[4], stream));
+        double e = 0, n2 = 0;
+        expectation(next, psi, &e, &n2, true);
+        PB_CUDA(cudaEventRecord(ev[5], stream));
+        rec.norm_post = std::sqrt(n2);
+        rec.q_true = next.n;
+        rec.energy = e;
+        int order = 0;
+        double ltn = 0, lcn = 0;
+        expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        PB_CUDA(cudaEventRecord(ev[6], stream));
+        sync();
+        rec.taylor_order = order;
+        rec.delta_norm_expmv = lcn - rec.norm_post;
+        cur ^= 1;
+        ccur ^= 1;
+        float ms = 0;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        times.select_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+        times.grow_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        times.assemble_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[3], ev[4]));
+        times.remap_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[4], ev[5]));
+        times.expectation_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[5], ev[6]));
+        times.expmv_ms += ms;
+        PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[6]));
+        times.total_ms += ms;
+        times.spmv_nnz += uint64_t(order) * next.nnz;
+    }
+    t = t + cfg.dt;
+    rec.t = t;
+    steps_done = s;
+    times.steps += 1;
+    times.kernel_launches += launches - launches0;
+    if (out) *out = rec;
+}
+
+}  // namespace pb

@@ -1,0 +1,211 @@
+// engine.cuh -- host-side orchestration of the device-resident paces step: context, pooled device
+// buffers, and one method per reference function on the hot path.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/paces_b200.h"
+#include "host_model.hpp"
+#include "kernels.cuh"
+
+namespace pb {
+
+struct CudaFail : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define PB_CUDA(call)                                                                                      \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess)                                                                             \
+            throw pb::CudaFail(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + __FILE__ + ":" + \
+                               std::to_string(__LINE__) + " (" #call ")");                                 \
+    } while (0)
+
+/// PACES_MAX_MEMORY_BYTES (common.hpp:30-49): 0 = unlimited; read on every call.
+inline uint64_t memory_cap_bytes() {
+    const char* env = std::getenv("PACES_MAX_MEMORY_BYTES");
+    if (env == nullptr || *env == '\0') return 0;
+    char* end = nullptr;
+    unsigned long long v = std::strtoull(env, &end, 10);
+    if (end == env) throw PacesError("PACES_MAX_MEMORY_BYTES is not a number: " + std::string(env));
+    return uint64_t(v);
+}
+inline void require_memory(uint64_t bytes, const char* what) {
+    const uint64_t cap = memory_cap_bytes();
+    if (cap != 0 && bytes > cap)
+        throw PacesError(std::string("memory cap exceeded: ") + what + " needs " + std::to_string(bytes) +
+                         " bytes, PACES_MAX_MEMORY_BYTES=" + std::to_string(cap));
+}
+
+/// Grow-only device allocation; steady-state steps never call cudaMalloc.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    /// Contents are NOT preserved when the buffer grows.
+    void ensure(size_t bytes) {
+        if (bytes <= cap) return;
+        size_t want = bytes + bytes / 4 + 256;
+        if (p) cudaFree(p);  // implicit device synchronisation: nothing in flight still uses it
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            want = bytes;
+            e = cudaMalloc(&p, want);
+        }
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw CudaFail(std::string("CUDA error: out of device memory allocating ") + std::to_string(bytes) +
+                           " bytes: " + cudaGetErrorString(e));
+        }
+        cap = want;
+    }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+/// EffectiveSpace (subspace.hpp:76-82) on the device: sorted key table + CSR H_eff.
+struct Space {
+    DevBuf words;  // n x W uint32, canonical order
+    uint32_t n = 0;
+    DevBuf row_ptr;  // uint32[n+1]
+    DevBuf col;      // int32[nnz] ascending per row
+    DevBuf val;      // double[nnz]
+    uint64_t nnz = 0;
+    uint64_t q_nom = 0;
+    int order = 0;
+    bool has_h = false;
+};
+
+struct Engine {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    std::string err;
+    uint64_t launches = 0;
+
+    bool has_model = false;
+    HostModel hm;
+    ModelDev md{};
+    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba;
+    int row_width = 1;  // max entries of an H_eff row for this model
+
+    // resident trajectory
+    Space space[2];
+    int cur = 0;
+    DevBuf coeff[2];
+    int ccur = 0;
+    bool has_state = false;
+    double t = 0;
+    uint64_t steps_done = 0;
+    pb200_run_cfg cfg{};
+    std::vector<uint32_t> cfg_occ;
+    std::vector<double> cfg_amp;
+    bool has_cfg = false;
+    int last_order = 0;
+    pb200_phase_times times{};
+
+    // scratch
+    DevBuf seeds;  // kept keys
+    uint32_t n_seeds = 0;
+    DevBuf tab_tmp, frontier[2], cand_keys, cand_gap, perm, seg_rank, gap, scan_tiles;
+    DevBuf tmp_col, tmp_val, row_len;
+    DevBuf weights, flag_keep, flag_tie, pos_a, idx_tmp, hist;
+    DevBuf term[2], partials, ctl;  // ctl: small device control block
+    DevBuf aux_words, aux_coeff, aux2_words, aux2_coeff, aux_vec;  // staging for the host-buffer operators
+    DevBuf flush;
+    void* pinned = nullptr;  // 4 KiB pinned host scratch for read-backs
+    cudaEvent_t ev[10]{};
+
+    explicit Engine(int dev);
+    ~Engine();
+
+    // ---- helpers
+    int grid_for(uint64_t n) const {
+        uint64_t g = (n + NT - 1) / NT;
+        const uint64_t cap = uint64_t(sm_count) * 8;
+        if (g > cap) g = cap;
+        if (g < 1) g = 1;
+        return int(g);
+    }
+    void sync() { PB_CUDA(cudaStreamSynchronize(stream)); }
+    void check_launch() {
+        ++launches;
+        PB_CUDA(cudaGetLastError());
+    }
+    template <class T>
+    T read_back(const void* dptr) {
+        PB_CUDA(cudaMemcpyAsync(pinned, dptr, sizeof(T), cudaMemcpyDeviceToHost, stream));
+        sync();
+        T v;
+        std::memcpy(&v, pinned, sizeof(T));
+        return v;
+    }
+    void exclusive_scan(uint32_t* data, uint64_t n);  // in place over n elements
+    void require_model() const {
+        if (!has_model) throw ArgError("no model set: call pb200_model_set first");
+    }
+
+    // ---- control block layout (device)
+    struct Ctl {
+        GrowCounters grow;
+        TaylorCtl taylor;
+        SelectCtl select;
+        unsigned ticket;  // generic reduction ticket
+        unsigned pad[3];
+        double out[8];  // generic reduction outputs
+    };
+    Ctl* dctl() const { return ctl.as<Ctl>(); }
+
+    // ---- model
+    void set_model(const HostModel& m);
+
+    // ---- operators on device data
+    void grow(const uint32_t* d_seeds, uint32_t n_seeds_, int order, Space& out);
+    void assemble(Space& sp);
+    /// returns kept count; result in this->seeds
+    uint32_t select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
+                    double* norm2_out);
+    double remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
+                 uint32_t nd, double2* dst_c);
+    /// out: <x|H|x>, |x|^2; throws on non-finite input when check_finite
+    void expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite);
+    void expmv(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps, int* order_used,
+               double* last_term_norm, double* last_c_norm);
+    void spmv(const Space& sp, const double2* x, double2* y);
+    void upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val);
+    void observe(const uint32_t* words, const double2* c, uint32_t n, double* density, double* amp, double* phonons);
+
+    // ---- resident trajectory
+    void run_begin(const pb200_run_cfg& c);
+    void run_step(pb200_diag* out);
+};
+
+}  // namespace pb

@@ -1,0 +1,610 @@
+// kernels.cuh -- the sm_100a kernels of the paces adapt-evolve-truncate step.
+//
+// Invariant shared by all of them: a basis table is ALWAYS held in canonical order (rows strictly
+// ascending in word-lexicographic order), exactly like the reference's PackedBasisTable with
+// sorted == true.  Consequences: (1) CSR column order == neighbour-key order, which fixes the
+// floating-point summation order of every SpMV row to the reference's (SURVEY hard part 1);
+// (2) uploads/downloads are plain copies; (3) neighbour look-ups are binary searches whose upper
+// levels are shared by a warp working on consecutive rows (monotone moves -> monotone answers);
+// (4) the x-gather of the SpMV is nearly coalesced for the same reason.
+//
+// Arithmetic that must match the reference bit for bit uses __dmul_rn/__dadd_rn/__dsqrt_rn so no FMA
+// is ever contracted (the reference is built without -march, i.e. without FMA: proj/CMakeLists.txt:6-8).
+#pragma once
+#include "keys.cuh"
+#include "primitives.cuh"
+
+namespace pb {
+
+// ================================================================================================
+// K1  expansion: candidates of one BFS order
+// ================================================================================================
+struct GrowCounters {
+    uint32_t n_cand;         // candidates not present in the table (with duplicates)
+    uint32_t overflow;       // candidate buffer too small
+    unsigned long long emitted;  // matrix elements emitted (transcript growth, subspace.hpp:117-123)
+    uint32_t n_new;          // unique new keys (after segment dedup)
+    uint32_t max_seg;        // longest gap segment seen (diagnostic)
+};
+
+/// For every frontier row: generate the off-diagonal neighbours (apply_terms,
+/// lattice_models.hpp:212-267; apply_to_rows, subspace.hpp:102-134), look each one up in the sorted
+/// table and append those that are absent, together with their insertion gap.  gap_count[g] counts the
+/// candidates that fall between table rows g-1 and g.
+/// frontier == nullptr means "all rows" (order 0: the seeds are the table).
+template <int W>
+__global__ void __launch_bounds__(NT) expand_level_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+                                                          const uint32_t* __restrict__ frontier, uint32_t nf,
+                                                          uint32_t* __restrict__ cand_keys,
+                                                          uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
+                                                          uint32_t* __restrict__ gap_count, GrowCounters* ctr,
+                                                          int count_emitted) {
+    unsigned long long emitted = 0;
+    for (uint32_t f = blockIdx.x * NT + threadIdx.x; f < nf; f += gridDim.x * NT) {
+        const uint32_t row = frontier ? __ldg(frontier + f) : f;
+        const Key<W> k = load_key<W>(table + size_t(row) * W);
+        const uint32_t e = exciton_site<W>(m, k);
+        if (count_emitted && diagonal_element<W>(m, k, e) != 0.0) ++emitted;
+        for_each_neighbor<W>(m, k, false, [&](int, const Key<W>& kk, double, bool) {
+            ++emitted;
+            uint32_t pos;
+            if (!find_row<W>(table, n, kk, pos)) {
+                const uint32_t slot = append_slot(&ctr->n_cand);
+                if (slot < cand_cap) {
+                    store_key<W>(cand_keys + size_t(slot) * W, kk);
+                    cand_gap[slot] = pos;
+                    atomicAdd(gap_count + pos, 1u);
+                } else {
+                    ctr->overflow = 1;
+                }
+            }
+        });
+    }
+    // transcript size bookkeeping (feeds the reference's memory-cap check, subspace.hpp:215-217)
+    if (count_emitted) {
+        for (int o = 16; o > 0; o >>= 1) emitted += __shfl_xor_sync(0xffffffffu, emitted, o);
+        if ((threadIdx.x & 31) == 0 && emitted) atomicAdd(&ctr->emitted, emitted);
+    }
+}
+
+// ================================================================================================
+// K2  dedup: counting sort by insertion gap, then exact dedup + ranking inside each (tiny) gap segment
+// ================================================================================================
+
+/// perm[seg_start[gap] + k] = candidate id, k = arrival order inside the gap (gap_fill starts at zero).
+__global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap, uint32_t nc,
+                                                              const uint32_t* __restrict__ seg_start,
+                                                              uint32_t* __restrict__ gap_fill,
+                                                              uint32_t* __restrict__ perm) {
+    for (uint32_t c = blockIdx.x * NT + threadIdx.x; c < nc; c += gridDim.x * NT) {
+        const uint32_t g = cand_gap[c];
+        const uint32_t r = atomicAdd(gap_fill + g, 1u);
+        perm[seg_start[g] + r] = c;
+    }
+}
+
+constexpr uint32_t SEG_DUP = 0xffffffffu;
+
+/// One thread per placed slot s.  Inside its gap segment a candidate is a duplicate if an equal key sits
+/// at a smaller slot (which copy survives is irrelevant: they are the same key).  seg_rank[s] = SEG_DUP
+/// for dropped duplicates, 0 otherwise; gap_kept[g] += 1 per survivor.
+template <int W>
+__global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __restrict__ cand_keys,
+                                                           const uint32_t* __restrict__ cand_gap,
+                                                           const uint32_t* __restrict__ perm, uint32_t nc,
+                                                           const uint32_t* __restrict__ seg_start,
+                                                           uint32_t* __restrict__ seg_rank,
+                                                           uint32_t* __restrict__ gap_kept, GrowCounters* ctr) {
+    for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
+        const uint32_t c = perm[s];
+        const uint32_t g = cand_gap[c];
+        const uint32_t s0 = seg_start[g], s1 = seg_start[g + 1];
+        const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
+        bool dup = false;
+        for (uint32_t t = s0; t < s && !dup; ++t)
+            dup = key_equal<W>(load_key<W>(cand_keys + size_t(perm[t]) * W), k);
+        seg_rank[s] = dup ? SEG_DUP : 0u;
+        if (!dup) atomicAdd(gap_kept + g, 1u);
+        if (s == s0 && s1 - s0 > 32) atomicMax(&ctr->max_seg, s1 - s0);
+    }
+}
+
+/// Survivors get rank = number of surviving smaller keys in their segment = canonical position inside
+/// the gap.  Readers only test a slot for SEG_DUP, which a concurrent rank write never produces.
+template <int W>
+__global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __restrict__ cand_keys,
+                                                          const uint32_t* __restrict__ cand_gap,
+                                                          const uint32_t* __restrict__ perm, uint32_t nc,
+                                                          const uint32_t* __restrict__ seg_start,
+                                                          volatile uint32_t* seg_rank) {
+    for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
+        if (seg_rank[s] == SEG_DUP) continue;
+        const uint32_t c = perm[s];
+        const uint32_t g = cand_gap[c];
+        const uint32_t s0 = seg_start[g], s1 = seg_start[g + 1];
+        if (s1 - s0 == 1) continue;  // alone in its gap: rank 0 already stored
+        const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
+        uint32_t rank = 0;
+        for (uint32_t t = s0; t < s1; ++t) {
+            if (t == s || seg_rank[t] == SEG_DUP) continue;
+            if (key_cmp<W>(load_key<W>(cand_keys + size_t(perm[t]) * W), k) < 0) ++rank;
+        }
+        seg_rank[s] = rank;
+    }
+}
+
+/// Writes the merged table: old row i moves to i + (#new keys in gaps <= i); a surviving candidate in
+/// gap g with rank r goes to g + kept_before[g] + r.  Also emits the next frontier (ascending row
+/// indices of the new keys in the merged table).   (sort_unique_rows + diff_rows + merge_rows,
+/// basis_codec.hpp:247-321, in one pass.)
+template <int W>
+__global__ void __launch_bounds__(NT) merge_old_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
+                                                            const uint32_t* __restrict__ kept_before,
+                                                            uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(table + size_t(i) * W);
+        store_key<W>(out + size_t(i + kept_before[i + 1]) * W, k);
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(NT) merge_new_rows_kernel(const uint32_t* __restrict__ cand_keys,
+                                                            const uint32_t* __restrict__ cand_gap,
+                                                            const uint32_t* __restrict__ perm,
+                                                            const uint32_t* __restrict__ seg_rank, uint32_t nc,
+                                                            const uint32_t* __restrict__ kept_before,
+                                                            uint32_t* __restrict__ out,
+                                                            uint32_t* __restrict__ next_frontier) {
+    for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
+        const uint32_t r = seg_rank[s];
+        if (r == SEG_DUP) continue;
+        const uint32_t c = perm[s];
+        const uint32_t g = cand_gap[c];
+        const uint32_t ord = kept_before[g] + r;  // index among all new keys, canonical order
+        const uint32_t pos = g + ord;
+        const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
+        store_key<W>(out + size_t(pos) * W, k);
+        next_frontier[ord] = pos;
+    }
+}
+
+// ================================================================================================
+// K3  row-wise assembly of H_eff
+// ================================================================================================
+constexpr int MAX_ROW = 2 * 3 + 3;  // hops (<= 6) + 2 ladder + diagonal
+
+/// Pass 1: row i of H_eff = {(index(k'), a) : (k', a) in apply_terms(key_i), k' in table}
+/// (replaces assemble_effective_hamiltonian, subspace.hpp:142-187, and the
+/// final-frontier filter, :225-241).  Neighbours are generated in ascending key order, so the found
+/// columns are already ascending.  Results are parked in fixed-width scratch (stride `width`).
+template <int W>
+__global__ void __launch_bounds__(NT) assemble_rows_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+                                                           int width, uint32_t* __restrict__ tmp_col,
+                                                           double* __restrict__ tmp_val,
+                                                           uint32_t* __restrict__ row_len) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(table + size_t(i) * W);
+        int len = 0;
+        uint32_t* tc = tmp_col + size_t(i) * width;
+        double* tv = tmp_val + size_t(i) * width;
+        for_each_neighbor<W>(m, k, true, [&](int, const Key<W>& kk, double amp, bool is_diag) {
+            uint32_t pos = i;
+            bool found = true;
+            if (!is_diag) {
+                // a smaller neighbour lives in [0, i), a larger one in (i, n)
+                const bool below = key_cmp<W>(kk, k) < 0;
+                found = below ? find_row_in<W>(table, 0, i, kk, pos) : find_row_in<W>(table, i + 1, n, kk, pos);
+            }
+            if (found) {
+                tc[len] = pos;
+                tv[len] = amp;
+                ++len;
+            }
+        });
+        row_len[i] = uint32_t(len);
+    }
+}
+
+/// Pass 2: compact the fixed-width scratch into CSR (row_ptr from the scan of row_len).
+__global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int width, const uint32_t* __restrict__ tmp_col,
+                                                              const double* __restrict__ tmp_val,
+                                                              const uint32_t* __restrict__ row_ptr,
+                                                              int32_t* __restrict__ col, double* __restrict__ val) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t b = row_ptr[i], e = row_ptr[i + 1];
+        const uint32_t* tc = tmp_col + size_t(i) * width;
+        const double* tv = tmp_val + size_t(i) * width;
+        for (uint32_t k = b; k < e; ++k) {
+            col[k] = int32_t(tc[k - b]);
+            val[k] = tv[k - b];
+        }
+    }
+}
+
+// ================================================================================================
+// K4  fused Taylor order:  hterm = H term ; term' = (0,-dt/n) hterm ; c += term' ; |term'|^2, |c|^2
+//     (csr_matvec, subspace.hpp:35-43 + propagator.hpp:68-84; arithmetic recipe SURVEY App. C.1)
+// ================================================================================================
+struct TaylorCtl {
+    int done;        // stop rule satisfied: later launches of this substep return immediately
+    int streak;      // consecutive small terms (propagator.hpp:80)
+    int order_used;  // max over substeps (propagator.hpp:78)
+    int last_order;  // order of the most recent launch that did work
+    double last_term_norm;
+    double last_c_norm;
+    unsigned ticket;
+    unsigned pad;
+};
+
+__global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double2* __restrict__ term_in,
+                                                          double2* __restrict__ term_out, double2* __restrict__ c,
+                                                          double b, int order, double rtol,
+                                                          double* __restrict__ partials, TaylorCtl* ctl,
+                                                          int ignore_stop) {
+    __shared__ double smem[NT / 32];
+    if (!ignore_stop && *(volatile int*)&ctl->done) return;
+    double acc[2] = {0.0, 0.0};
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        double ar = 0.0, ai = 0.0;
+        for (uint32_t k = kb; k < ke; ++k) {
+            const double v = __ldg(val + k);
+            const double2 x = __ldg(term_in + __ldg(col + k));
+            ar = __dadd_rn(ar, __dmul_rn(v, x.x));
+            ai = __dadd_rn(ai, __dmul_rn(v, x.y));
+        }
+        // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
+        const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
+        const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
+        double2 cc = c[i];
+        cc.x = __dadd_rn(cc.x, tr);
+        cc.y = __dadd_rn(cc.y, ti);
+        term_out[i] = make_double2(tr, ti);
+        c[i] = cc;
+        acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti)));
+        acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+    }
+    double tot[2];
+    if (grid_sum<2>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+        const double tn = __dsqrt_rn(tot[0]), rn = __dsqrt_rn(tot[1]);
+        if (order > ctl->order_used) ctl->order_used = order;
+        ctl->last_order = order;
+        ctl->last_term_norm = tn;
+        ctl->last_c_norm = rn;
+        const int streak = (tn <= __dmul_rn(rtol, rn)) ? ctl->streak + 1 : 0;
+        ctl->streak = streak;
+        if (streak >= 2) ctl->done = 1;
+        __threadfence();
+    }
+}
+
+/// Plain y = H x (csr_matvec, subspace.hpp:35-43).
+__global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                  const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                  const double2* __restrict__ x, double2* __restrict__ y) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        double ar = 0.0, ai = 0.0;
+        for (uint32_t k = kb; k < ke; ++k) {
+            const double v = __ldg(val + k);
+            const double2 xx = __ldg(x + __ldg(col + k));
+            ar = __dadd_rn(ar, __dmul_rn(v, xx.x));
+            ai = __dadd_rn(ai, __dmul_rn(v, xx.y));
+        }
+        y[i] = make_double2(ar, ai);
+    }
+}
+
+// ================================================================================================
+// K5  <x|H|x> (csr_expectation, subspace.hpp:46-55) fused with |x|^2 and the finiteness check of
+//     expmv (propagator.hpp:55-57).  out[0] = <x|H|x>, out[1] = sum |x|^2, out[2] = #non-finite.
+// ================================================================================================
+__global__ void __launch_bounds__(NT) expectation_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double2* __restrict__ x, double* __restrict__ partials,
+                                                         unsigned* ticket, double* __restrict__ out) {
+    __shared__ double smem[NT / 32];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        double ar = 0.0, ai = 0.0;
+        for (uint32_t k = kb; k < ke; ++k) {
+            const double v = __ldg(val + k);
+            const double2 xx = __ldg(x + __ldg(col + k));
+            ar = __dadd_rn(ar, __dmul_rn(v, xx.x));
+            ai = __dadd_rn(ai, __dmul_rn(v, xx.y));
+        }
+        const double2 xi = __ldg(x + i);
+        // real(conj(x) * row) = xr*rr - (-xi)*ri
+        acc[0] = __dadd_rn(acc[0], __dsub_rn(__dmul_rn(xi.x, ar), __dmul_rn(-xi.y, ai)));
+        acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(xi.x, xi.x), __dmul_rn(xi.y, xi.y)));
+        if (!isfinite(xi.x) || !isfinite(xi.y)) acc[2] = acc[2] + 1.0;
+    }
+    double tot[3];
+    if (grid_sum<3>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) {
+        out[0] = tot[0];
+        out[1] = tot[1];
+        out[2] = tot[2];
+    }
+}
+
+// ================================================================================================
+// K6  truncation: weights, exact q_nom-th largest by radix select on the double's bit pattern,
+//     flags, order-preserving compaction   (truncate_select, engine.hpp:107-156)
+// ================================================================================================
+struct SelectCtl {
+    unsigned long long prefix;    // bit pattern of the cutoff being built, top digits first
+    unsigned long long k;         // rank still wanted inside the current prefix group (1-based from the top)
+    unsigned long long count_gt;  // weights strictly above the cutoff
+    unsigned long long count_eq;  // weights equal to the cutoff
+    unsigned long long support;   // weights > 0
+    unsigned ticket;
+    unsigned pad;
+    double norm2;                 // sum of weights
+};
+
+/// w_i = re^2 + im^2 (std::norm), sum and support count.
+__global__ void __launch_bounds__(NT) weights_kernel(const double2* __restrict__ c, uint32_t n, double* __restrict__ w,
+                                                     double* __restrict__ partials, SelectCtl* ctl) {
+    __shared__ double smem[NT / 32];
+    double acc[2] = {0.0, 0.0};
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const double2 x = c[i];
+        const double ww = __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y));
+        w[i] = ww;
+        acc[0] = __dadd_rn(acc[0], ww);
+        if (ww > 0.0) acc[1] = acc[1] + 1.0;  // exact for counts < 2^53
+    }
+    double tot[2];
+    if (grid_sum<2>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+        ctl->norm2 = tot[0];
+        ctl->support = (unsigned long long)tot[1];
+    }
+}
+
+/// Histogram of the 8-bit digit at `shift` over the weights whose higher bits equal ctl->prefix.
+/// Positive doubles order like their bit patterns, so this is an exact selection.
+__global__ void __launch_bounds__(NT) select_hist_kernel(const double* __restrict__ w, uint32_t n, int shift,
+                                                         const SelectCtl* __restrict__ ctl,
+                                                         uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[256];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long prefix = ctl->prefix;
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const double ww = w[i];
+        if (!(ww > 0.0)) continue;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(ww);
+        if (shift == 56 || (bits >> (shift + 8)) == prefix) atomicAdd(&sh[(bits >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    const uint32_t v = sh[threadIdx.x];
+    if (v) atomicAdd(hist + threadIdx.x, v);
+}
+
+__global__ void select_pick_kernel(uint32_t* __restrict__ hist, SelectCtl* ctl) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned long long k = ctl->k, gt = ctl->count_gt;
+    int d = 255;
+    for (; d > 0; --d) {
+        const unsigned long long h = hist[d];
+        if (k <= h) break;
+        k -= h;
+        gt += h;
+    }
+    ctl->count_eq = hist[d];
+    ctl->prefix = (ctl->prefix << 8) | (unsigned long long)d;
+    ctl->k = k;
+    ctl->count_gt = gt;
+    for (int i = 0; i < 256; ++i) hist[i] = 0;
+}
+
+/// mode 0: keep every supported row (w > 0).  mode 1: keep w > cutoff, and w == cutoff too when
+/// keep_ties; otherwise the ties are flagged separately for the host-side Fisher-Yates draw.
+__global__ void __launch_bounds__(NT) select_flags_kernel(const double* __restrict__ w, uint32_t n, int mode,
+                                                          const SelectCtl* __restrict__ ctl, int keep_ties,
+                                                          uint32_t* __restrict__ keep, uint32_t* __restrict__ tie) {
+    const unsigned long long cut = ctl->prefix;
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const double ww = w[i];
+        uint32_t kf = 0, tf = 0;
+        if (ww > 0.0) {
+            if (mode == 0) {
+                kf = 1;
+            } else {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(ww);
+                if (bits > cut)
+                    kf = 1;
+                else if (bits == cut) {
+                    if (keep_ties)
+                        kf = 1;
+                    else
+                        tf = 1;
+                }
+            }
+        }
+        keep[i] = kf;
+        if (tie) tie[i] = tf;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        keep[n] = 0;
+        if (tie) tie[n] = 0;
+    }
+}
+
+/// idx[pos[i]] = i for flagged i (order preserving).
+__global__ void __launch_bounds__(NT) compact_index_kernel(const uint32_t* __restrict__ flag,
+                                                           const uint32_t* __restrict__ pos, uint32_t n,
+                                                           uint32_t* __restrict__ idx) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT)
+        if (flag[i]) idx[pos[i]] = i;
+}
+
+__global__ void set_flags_kernel(const uint32_t* __restrict__ idx, uint32_t cnt, uint32_t* __restrict__ flag) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) flag[idx[i]] = 1;
+}
+
+/// out[pos[i]] = table[i] for flagged rows: ascending indices of a sorted parent stay sorted
+/// (engine.hpp:146-155).
+template <int W>
+__global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __restrict__ table,
+                                                          const uint32_t* __restrict__ flag,
+                                                          const uint32_t* __restrict__ pos, uint32_t n,
+                                                          uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        if (flag[i]) store_key<W>(out + size_t(pos[i]) * W, load_key<W>(table + size_t(i) * W));
+    }
+}
+
+// ================================================================================================
+// K7  remap (remap_state, subspace.hpp:281-305): look every old key up in the new table; copy the
+//     coefficient when present, otherwise add |c|^2 to the discarded weight.  dst must be zeroed.
+// ================================================================================================
+template <int W>
+__global__ void __launch_bounds__(NT) remap_kernel(const uint32_t* __restrict__ src_table,
+                                                   const double2* __restrict__ src_c, uint32_t ns,
+                                                   const uint32_t* __restrict__ dst_table, uint32_t nd,
+                                                   double2* __restrict__ dst_c, double* __restrict__ partials,
+                                                   unsigned* ticket, double* __restrict__ out) {
+    __shared__ double smem[NT / 32];
+    double acc[1] = {0.0};
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < ns; i += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(src_table + size_t(i) * W);
+        const double2 x = src_c[i];
+        uint32_t pos;
+        if (find_row<W>(dst_table, nd, k, pos))
+            dst_c[pos] = x;
+        else
+            acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+    }
+    double tot[1];
+    if (grid_sum<1>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) out[0] = tot[0];
+}
+
+// ================================================================================================
+// K8  observables: norm^2 + exciton density (observables.hpp:26-37), dipole overlap (:99-112),
+//     phonon numbers (:84-95)
+// ================================================================================================
+
+/// The table is sorted and the exciton register is the most significant field, so the rows of one
+/// site are contiguous: a CTA's chunk touches only a few sites and reduces each with the fixed tree.
+/// block_part[(blockIdx, site)] partial sums are combined in CTA order by density_finish_kernel.
+template <int W>
+__global__ void __launch_bounds__(NT) density_kernel(ModelDev m, const uint32_t* __restrict__ table,
+                                                     const double2* __restrict__ c, uint32_t n,
+                                                     uint32_t rows_per_block, double* __restrict__ block_part) {
+    __shared__ double smem[NT / 32];
+    __shared__ uint32_t s_lo, s_hi;
+    const uint32_t r0 = blockIdx.x * rows_per_block;
+    const uint32_t r1 = min(n, r0 + rows_per_block);
+    if (r0 >= r1) return;
+    if (threadIdx.x == 0) {
+        s_lo = exciton_site<W>(m, load_key<W>(table + size_t(r0) * W));
+        s_hi = exciton_site<W>(m, load_key<W>(table + size_t(r1 - 1) * W));
+    }
+    __syncthreads();
+    const uint32_t lo = s_lo, hi = s_hi;
+    for (uint32_t site = lo; site <= hi; ++site) {
+        double acc = 0.0;
+        for (uint32_t i = r0 + threadIdx.x; i < r1; i += NT) {
+            const uint32_t e = exciton_site<W>(m, load_key<W>(table + size_t(i) * W));
+            if (e == site) {
+                const double2 x = c[i];
+                acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+            }
+        }
+        const double t = block_sum(acc, smem);
+        if (threadIdx.x == 0) block_part[size_t(blockIdx.x) * m.L + site] = t;
+    }
+}
+
+/// density[site] = sum over CTAs in ascending order; one thread per site.  block_part must be zeroed
+/// before density_kernel.
+__global__ void density_finish_kernel(const double* __restrict__ block_part, uint32_t nblocks, int L,
+                                      double* __restrict__ density) {
+    const int site = blockIdx.x * blockDim.x + threadIdx.x;
+    if (site >= L) return;
+    double acc = 0.0;
+    for (uint32_t b = 0; b < nblocks; ++b) acc = __dadd_rn(acc, block_part[size_t(b) * L + site]);
+    density[site] = acc;
+}
+
+/// amp = (1/sqrt(L)) sum_j c[find_row(|j; vacuum>)], summed in ascending j by one thread after the
+/// L look-ups ran in parallel.
+template <int W>
+__global__ void dipole_kernel(ModelDev m, const uint32_t* __restrict__ table, const double2* __restrict__ c,
+                              uint32_t n, double2* __restrict__ found, double* __restrict__ out) {
+    for (int j = threadIdx.x; j < m.L; j += blockDim.x) {
+        Key<W> k;
+#pragma unroll
+        for (int i = 0; i < W; ++i) k.w[i] = 0;
+        set_bits<W>(k, 0, m.b0, uint32_t(j));
+        uint32_t pos;
+        found[j] = find_row<W>(table, n, k, pos) ? c[pos] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ar = 0.0, ai = 0.0;
+        for (int j = 0; j < m.L; ++j) {
+            ar = __dadd_rn(ar, found[j].x);
+            ai = __dadd_rn(ai, found[j].y);
+        }
+        const double s = __dsqrt_rn(double(m.L));
+        out[0] = __ddiv_rn(ar, s);
+        out[1] = __ddiv_rn(ai, s);
+    }
+}
+
+/// n_j = sum_i |c_i|^2 * occ_j(i); per-CTA partials for all L sites, combined by density_finish_kernel.
+template <int W>
+__global__ void __launch_bounds__(NT) phonon_numbers_kernel(ModelDev m, const uint32_t* __restrict__ table,
+                                                            const double2* __restrict__ c, uint32_t n,
+                                                            uint32_t rows_per_block, double* __restrict__ block_part) {
+    __shared__ double smem[NT / 32];
+    const uint32_t r0 = blockIdx.x * rows_per_block;
+    const uint32_t r1 = min(n, r0 + rows_per_block);
+    for (int j = 0; j < m.L; ++j) {
+        double acc = 0.0;
+        for (uint32_t i = r0 + threadIdx.x; i < r1; i += NT) {
+            const double2 x = c[i];
+            const double w = __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y));
+            if (w != 0.0) {
+                const uint32_t occ = phonon_occ<W>(m, load_key<W>(table + size_t(i) * W), j);
+                acc = __dadd_rn(acc, __dmul_rn(w, double(occ)));
+            }
+        }
+        const double t = block_sum(acc, smem);
+        if (threadIdx.x == 0) block_part[size_t(blockIdx.x) * m.L + j] = t;
+    }
+}
+
+/// apply_terms for a batch of keys (lattice_models.hpp:212-267), canonical neighbour order.
+template <int W>
+__global__ void apply_terms_kernel(ModelDev m, const uint32_t* __restrict__ keys, uint32_t n, int cap,
+                                   uint32_t* __restrict__ out_keys, double* __restrict__ out_amps,
+                                   int* __restrict__ count) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const Key<W> k = load_key<W>(keys + size_t(i) * W);
+        int len = 0;
+        for_each_neighbor<W>(m, k, true, [&](int, const Key<W>& kk, double amp, bool) {
+            if (len < cap) {
+                store_key<W>(out_keys + (size_t(i) * cap + len) * W, kk);
+                out_amps[size_t(i) * cap + len] = amp;
+            }
+            ++len;
+        });
+        count[i] = len;
+    }
+}
+
+/// L2 flush for benchmarking: streams a buffer larger than L2.
+__global__ void flush_kernel(double* __restrict__ buf, size_t n) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        buf[i] = buf[i] + 1.0;
+}
+
+}  // namespace pb

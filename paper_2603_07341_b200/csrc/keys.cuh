@@ -1,0 +1,242 @@
+// keys.cuh -- packed basis keys on the device: bit fields, lexicographic order, sorted-table search
+// and the closed-form Holstein / tight-binding neighbour generator.
+//
+// Key format (reference basis_codec.hpp:17-26, 90-128): site i gets bit_width(d_i - 1) bits, payloads
+// packed back to back MSB-first into W 32-bit words, site 0 (the exciton register) in the top bits of
+// word 0; a payload that straddles a word boundary keeps its high bits in the earlier word; padding
+// bits are zero.  Word-lexicographic order equals occupation-vector order (basis_codec.hpp:188-194).
+//
+// Everything is templated on W (words per key) so a key lives in registers; runtime word indices are
+// resolved with unrolled selects instead of dynamic indexing (which would spill the key to local memory).
+#pragma once
+#include <cstdint>
+
+namespace pb {
+
+constexpr int MAX_NB = 6;  // 2 * ndim hop partners per site
+
+/// Model constants in device-readable form (closed form of the term list).
+/// Layout: site 0 = exciton register with b0 bits at offset 0; phonon register j has bp bits at
+/// offset b0 + j*bp (HamiltonianTermSet::phonon_slot, lattice_models.hpp:123-124).
+struct ModelDev {
+    int kind;        // 0 tight-binding, 1 holstein
+    int L;           // lattice sites
+    int nph;         // phonon registers (0 for tight binding)
+    int b0;          // bits of the exciton register
+    int bp;          // bits per phonon register
+    int W;           // words per key
+    uint32_t d_pho;  // phonon cutoff dimension
+    int max_deg;     // max hop partners of a site
+    const double* eps;     // [L]   onsite energies (0 where the term is absent)
+    const double* omega;   // [L]   phonon frequencies (0 where absent)
+    const double* g;       // [L]   vibronic couplings (0 where absent)
+    const int* nb_site;    // [L*MAX_NB] hop partners sorted ascending, -1 padded; zero-amplitude bonds removed
+    const double* nb_amp;  // [L*MAX_NB] bond amplitude J
+};
+
+template <int W>
+struct Key {
+    uint32_t w[W];
+};
+
+template <int W>
+__device__ __forceinline__ Key<W> load_key(const uint32_t* __restrict__ p) {
+    Key<W> k;
+#pragma unroll
+    for (int i = 0; i < W; ++i) k.w[i] = __ldg(p + i);
+    return k;
+}
+
+template <int W>
+__device__ __forceinline__ void store_key(uint32_t* __restrict__ p, const Key<W>& k) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) p[i] = k.w[i];
+}
+
+template <int W>
+__device__ __forceinline__ bool key_equal(const Key<W>& a, const Key<W>& b) {
+    bool eq = true;
+#pragma unroll
+    for (int i = 0; i < W; ++i) eq = eq && (a.w[i] == b.w[i]);
+    return eq;
+}
+
+/// -1 / 0 / +1 for a < b / a == b / a > b in word-lexicographic order (row_less, basis_codec.hpp:188-194).
+template <int W>
+__device__ __forceinline__ int key_cmp(const Key<W>& a, const Key<W>& b) {
+    int r = 0;
+#pragma unroll
+    for (int i = W - 1; i >= 0; --i) {
+        if (a.w[i] != b.w[i]) r = (a.w[i] < b.w[i]) ? -1 : 1;
+    }
+    return r;
+}
+
+/// Compares a table row in global memory against a key, reading only as many words as needed.
+template <int W>
+__device__ __forceinline__ int row_cmp(const uint32_t* __restrict__ row, const Key<W>& k) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        const uint32_t v = __ldg(row + i);
+        if (v != k.w[i]) return (v < k.w[i]) ? -1 : 1;
+    }
+    return 0;
+}
+
+/// Binary search in a sorted table (find_row, basis_codec.hpp:334-348).  Returns true and the row
+/// index when present; otherwise false and the insertion point (number of rows < key).
+template <int W>
+__device__ __forceinline__ bool find_row(const uint32_t* __restrict__ table, uint32_t n, const Key<W>& k,
+                                         uint32_t& pos) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        const int c = row_cmp<W>(table + size_t(mid) * W, k);
+        if (c == 0) {
+            pos = mid;
+            return true;
+        }
+        if (c < 0)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    pos = lo;
+    return false;
+}
+
+/// Same search restricted to [lo, hi) (callers that know a bracket).
+template <int W>
+__device__ __forceinline__ bool find_row_in(const uint32_t* __restrict__ table, uint32_t lo, uint32_t hi,
+                                            const Key<W>& k, uint32_t& pos) {
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        const int c = row_cmp<W>(table + size_t(mid) * W, k);
+        if (c == 0) {
+            pos = mid;
+            return true;
+        }
+        if (c < 0)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    pos = lo;
+    return false;
+}
+
+/// b-bit field at bit offset off (get_site, basis_codec.hpp:90-108).  b in [0, 32].
+template <int W>
+__device__ __forceinline__ uint32_t get_bits(const Key<W>& k, int off, int b) {
+    if (b == 0) return 0;
+    const int wi = off >> 5;
+    uint32_t hi = 0, lo = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (i == wi) hi = k.w[i];
+        if (i == wi + 1) lo = k.w[i];
+    }
+    const uint64_t win = (uint64_t(hi) << 32) | lo;
+    const int sh = 64 - (off & 31) - b;
+    const uint64_t mask = (b >= 32) ? 0xffffffffull : ((1ull << b) - 1);
+    return uint32_t((win >> sh) & mask);
+}
+
+/// Overwrites the b-bit field at bit offset off (set_site, basis_codec.hpp:111-128).
+template <int W>
+__device__ __forceinline__ void set_bits(Key<W>& k, int off, int b, uint32_t value) {
+    if (b == 0) return;
+    const int wi = off >> 5;
+    const int sh = 64 - (off & 31) - b;
+    const uint64_t mask = ((b >= 32) ? 0xffffffffull : ((1ull << b) - 1)) << sh;
+    const uint64_t val = (uint64_t(value) << sh) & mask;
+    const uint32_t mhi = uint32_t(mask >> 32), mlo = uint32_t(mask);
+    const uint32_t vhi = uint32_t(val >> 32), vlo = uint32_t(val);
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (i == wi) k.w[i] = (k.w[i] & ~mhi) | vhi;
+        if (i == wi + 1) k.w[i] = (k.w[i] & ~mlo) | vlo;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t exciton_site(const ModelDev& m, const Key<W>& k) {
+    return m.b0 == 0 ? 0u : (k.w[0] >> (32 - m.b0));
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t phonon_occ(const ModelDev& m, const Key<W>& k, int j) {
+    return get_bits<W>(k, m.b0 + j * m.bp, m.bp);
+}
+
+/// Diagonal element: eps[e] first, then omega[j]*n_j for ascending j, separate multiply and add
+/// (apply_terms accumulation order, lattice_models.hpp:228-235 over the term order of :160-171).
+/// Registers with n_j == 0 contribute +0.0 and are skipped; whole zero words are skipped at once.
+template <int W>
+__device__ __forceinline__ double diagonal_element(const ModelDev& m, const Key<W>& k, uint32_t e) {
+    double diag = 0.0;
+    const double ee = __ldg(m.eps + e);
+    if (ee != 0.0) diag = __dadd_rn(diag, ee);
+    if (m.nph > 0 && m.bp > 0) {
+        for (int j = 0; j < m.nph; ++j) {
+            const uint32_t n = phonon_occ<W>(m, k, j);
+            if (n != 0) {
+                const double om = __ldg(m.omega + j);
+                if (om != 0.0) diag = __dadd_rn(diag, __dmul_rn(om, double(n)));
+            }
+        }
+    }
+    return diag;
+}
+
+/// Neighbour generator in CANONICAL (ascending key) order:
+///   hops to partners t < e (ascending t) | lower n_e | diagonal | raise n_e | hops to t > e (ascending t)
+/// A hop rewrites the most significant field, so t < e sorts before every key with site0 = e; the
+/// ladder moves keep site0 and change one later field.  F is called as f(slot, key', amp, is_diag);
+/// slot numbers are stable per (site, move) so a caller can tabulate per-slot results.
+/// Amplitudes follow lattice_models.hpp:236-248: g*sqrt(double(n+1)) (dropped at the cutoff
+/// n+1 == d_pho), g*sqrt(double(n)), bond J; sqrt is the correctly rounded IEEE one.
+template <int W, class F>
+__device__ __forceinline__ void for_each_neighbor(const ModelDev& m, const Key<W>& k, bool with_diag, F&& f) {
+    const uint32_t e = exciton_site<W>(m, k);
+    const int* nbs = m.nb_site + size_t(e) * MAX_NB;
+    const double* nba = m.nb_amp + size_t(e) * MAX_NB;
+    int slot = 0;
+    int d = 0;
+    for (; d < MAX_NB; ++d) {
+        const int t = __ldg(nbs + d);
+        if (t < 0 || uint32_t(t) > e) break;
+        Key<W> kk = k;
+        set_bits<W>(kk, 0, m.b0, uint32_t(t));
+        f(slot++, kk, __ldg(nba + d), false);
+    }
+    uint32_t n = 0;
+    double ge = 0.0;
+    if (m.nph > 0) {
+        n = phonon_occ<W>(m, k, int(e));
+        ge = __ldg(m.g + e);
+    }
+    if (ge != 0.0 && n >= 1) {
+        Key<W> kk = k;
+        set_bits<W>(kk, m.b0 + int(e) * m.bp, m.bp, n - 1);
+        f(slot++, kk, __dmul_rn(ge, __dsqrt_rn(double(n))), false);
+    }
+    if (with_diag) {
+        const double diag = diagonal_element<W>(m, k, e);
+        if (diag != 0.0) f(slot++, k, diag, true);
+    }
+    if (ge != 0.0 && n + 1 < m.d_pho) {
+        Key<W> kk = k;
+        set_bits<W>(kk, m.b0 + int(e) * m.bp, m.bp, n + 1);
+        f(slot++, kk, __dmul_rn(ge, __dsqrt_rn(double(n + 1))), false);
+    }
+    for (; d < MAX_NB; ++d) {
+        const int t = __ldg(nbs + d);
+        if (t < 0) break;
+        Key<W> kk = k;
+        set_bits<W>(kk, 0, m.b0, uint32_t(t));
+        f(slot++, kk, __ldg(nba + d), false);
+    }
+}
+
+}  // namespace pb

@@ -1,0 +1,3 @@
+// paces_b200.cu -- unity translation unit of libpaces_b200.so (kernels are defined once, in headers).
+#include "engine.cu"
+#include "capi.cu"
