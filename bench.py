@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- the paces adapt-evolve-truncate timestep on B200 (metric of BASELINE.json).
+
+  python bench.py --gpus N --steps K --warmup W            # this repo's CUDA path (libpaces_b200.so)
+  python bench.py --impl reference --steps K --warmup W    # the reference's own CPU path (oracle/_ref)
+
+A "step" is one full paces timestep (truncate-select -> grow m=2 -> assemble H_eff -> remap -> <H> ->
+Taylor expmv; reference engine.hpp:268-291) of BASELINE config 2 -- 1D Holstein chain, 16 sites, g = 1,
+d_pho = 16, localized start, m_init = 10, dt = 0.05, rtol = 1e-15 -- at q_nom = 1e6 in the steady state where
+truncation binds (q_true ~ 3.3e6 rows, nnz ~ 1.15e7).  The trajectory is spun up (untimed) from
+the initial state until the support exceeds q_nom; then W warm-up steps, then K timed steps.
+
+value    timesteps/s with state and subspace resident in HBM (whole job: sum over ranks).
+e2e      the same step through the host-buffer operator pb200_step (paces::step with a host SparseState in
+         and out): pinned host state -> H2D -> step -> D2H of the new state, every step.
+roofline the fused Taylor-order kernel (SpMV + scale + axpy + 2 norms): algorithmic bytes 12*nnz + 72*n per
+         launch / its average launch duration inside the timed steps (CUDA events on the launch stream).
+cpu_baseline  the unmodified reference (oracle/_ref, else the oracle port) timed on this box's host cores on
+         the same resident state.
+
+One JSON line on stdout (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+MODEL = dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16)
+RUN = dict(init="localized", site=-1, m_init=10, m=2, dt=0.05, rtol=1e-15, max_order=200, substeps=1, t_max=50.0,
+           seed=7)
+WORKLOAD = "C2: 1D Holstein chain L=16, g=1, J=1, omega=1, d_pho=16 (68-bit keys, 3 words), m=2, dt=0.05"
+SPINUP_MAX = 40
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], set(), None, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self.t = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+
+    def start(self):
+        if self.ok:
+            self.t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=1.0)
+        s = sorted(self.samples)
+        return {"sm_mhz": (s[len(s) // 2] if s else None), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def spin_up(stepper, q_nom):
+    """Steps until truncation binds (support > q_nom, i.e. q_true has saturated) -- untimed."""
+    last = 0
+    for s in range(SPINUP_MAX):
+        d = stepper()
+        if d["q_true"] > 2 * q_nom and abs(d["q_true"] - last) < 0.02 * d["q_true"]:
+            return s + 1
+        last = d["q_true"]
+    return SPINUP_MAX
+
+
+# --------------------------------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation on the host cores
+# --------------------------------------------------------------------------------------------------------------
+def cpu_checker():
+    from oracle import pyoracle
+
+    if os.path.exists(pyoracle.REF_LIB):
+        return pyoracle, pyoracle.load_reference(), "reference"
+    if not os.path.exists(pyoracle.PORT_LIB):
+        import subprocess
+
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"])
+    return pyoracle, pyoracle.load_port(), "port"
+
+
+def cpu_step_from_state(pyoracle, orc, om, w, c, q_nom, seed, step_index):
+    """One reference step() from a given state through the reference's stand-alone functions
+    (same five calls as engine.hpp:268-291)."""
+    kept = om.truncate_select(w, c, q_nom, orc.mix_seed(seed + step_index))
+    tw, rp, col, val = om.grow(kept, RUN["m"])
+    psi, disc = om.remap(w, c, tw)
+    e = pyoracle.csr_expectation(orc, rp, col, val, psi)
+    psi, order, _ = pyoracle.expmv(orc, rp, col, val, psi, dt=RUN["dt"], rtol=RUN["rtol"], max_order=RUN["max_order"],
+                                   substeps=RUN["substeps"])
+    return tw, psi, dict(q_true=len(tw), nnz=int(rp[-1]), taylor_order=order, energy=e, discarded_weight=disc)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pyoracle, orc, kind = cpu_checker()
+    q_nom = args.q_nom_reference or args.q_nom
+    om = orc.model(pyoracle.ModelDef(**MODEL))
+    run = om.run(q_nom=q_nom, **RUN)
+    t_spin = time.perf_counter()
+    spin = spin_up(run.step, q_nom)
+    t_spin = time.perf_counter() - t_spin
+    # bounded sample: cap the timed work so the arm ends within a few minutes on 8-ish host cores
+    t0 = time.perf_counter()
+    run.step()
+    one = time.perf_counter() - t0
+    budget = args.reference_budget_s
+    k_eff = max(1, min(args.steps, int(budget / max(one, 1e-3))))
+    w_eff = 1 + min(max(args.warmup - 1, 0), 1 if one > 1.0 else args.warmup)
+    for _ in range(w_eff - 1):
+        run.step()
+    t0 = time.perf_counter()
+    for _ in range(k_eff):
+        d = run.step()
+    el = time.perf_counter() - t0
+    rows, nnz, _, _ = run.info()
+    value = k_eff / el
+    line = {
+        "impl": "reference", "metric": "timesteps_per_sec", "value": value, "unit": "timesteps/s", "n_gpus": args.gpus,
+        "steps": k_eff, "warmup": w_eff, "ms_per_step": 1e3 * el / k_eff, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128 amplitudes, u32 packed keys)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "q_nom": q_nom, "q_true": rows, "nnz": nnz, "spinup_steps": spin,
+                   "note": "reference CPU path (proj/include/paces, -O3 -fopenmp, no -march) through oracle/_ref; "
+                           "timed steps are capped by --reference-budget-s so the arm ends within minutes",
+                   "requested_steps": args.steps, "requested_warmup": args.warmup},
+        "cpu_baseline": {"value": value, "unit": "timesteps/s", "cores": orc.threads(), "kind": kind,
+                         "sample": f"{k_eff} steady-state timesteps at q_nom={q_nom} (q_true={rows}) after "
+                                   f"{spin} spin-up steps ({t_spin:.1f} s)"},
+        "e2e": {"value": value, "unit": "timesteps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------------------------
+# this repo's arm
+# --------------------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--q-nom", dest="q_nom", type=int, default=1_000_000)
+    ap.add_argument("--q-nom-reference", dest="q_nom_reference", type=int, default=0, help="0 = same as --q-nom")
+    ap.add_argument("--reference-budget-s", dest="reference_budget_s", type=float, default=90.0)
+    ap.add_argument("--cpu-baseline-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device; the B200 path has no CPU fallback (use --impl reference)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2603_07341_b200 as pb
+
+    stream = torch.cuda.Stream()
+    ctx = pb.Context(pb.ModelDef(**MODEL), device=local)
+    ctx.set_stream(stream.cuda_stream)
+    # N > 1: independent replicas, one per rank (weak scaling); each rank draws its own tie-break seed.
+    run_kw = dict(RUN, q_nom=args.q_nom, seed=RUN["seed"] + rank)
+
+    with torch.cuda.stream(stream):
+        run = ctx.run(**run_kw)
+        spin = spin_up(run.step, args.q_nom)
+        for _ in range(args.warmup):
+            run.step()
+
+        def barrier():
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+
+        sampler = ClockSampler(local)
+        run.reset_times()
+        launches0 = ctx.kernel_launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        sampler.start()
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            d = run.step()
+        ev1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        dev_ms = ev0.elapsed_time(ev1)
+        times = run.times()
+        launches = ctx.kernel_launches - launches0
+        # keep the same loop running so NVML (10 ms period) sees the clocks under this load
+        t_probe = time.perf_counter()
+        while time.perf_counter() - t_probe < 1.0:
+            run.step()
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        clocks["window"] = "timed steps + 1 s continuation of the same step loop (NVML, 10 ms period)"
+
+        rows, nnz, t_now, steps_done = run.info()
+        t_ms = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        step_ms = float(t_ms.item()) / args.steps
+        value = world * args.steps / (float(t_ms.item()) * 1e-3)
+
+        # ---- roofline of the dominant kernel (fused Taylor order) inside the timed steps
+        peak, peak_src = measured_peak()
+        orders = max(1, times["taylor_orders"])
+        avg_launch_ms = times["expmv_ms"] / orders
+        bytes_per_launch = 12.0 * (times["spmv_nnz"] / orders) + 72.0 * rows
+        achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+        iso_ms, _, _ = run.bench_taylor(orders=20, flush_l2=True, dt=RUN["dt"])
+        spmv_ms = run.bench_spmv(reps=20, flush_l2=True)
+        roofline = {
+            "kernel": "taylor_order_kernel (y=H_eff x fused with term'=(0,-dt/n) y, c+=term', |term'|^2, |c|^2)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
+            "launches_timed": int(orders),
+            "isolated_l2_flushed": {"ms": iso_ms, "GB/s": (12.0 * nnz + 72.0 * rows) / (iso_ms * 1e-3) / 1e9},
+            "plain_spmv_l2_flushed": {"ms": spmv_ms, "GB/s": (12.0 * nnz + 40.0 * rows) / (spmv_ms * 1e-3) / 1e9,
+                                      "nnz_per_s": nnz / (spmv_ms * 1e-3)},
+            "share_of_step": times["expmv_ms"] / max(times["total_ms"], 1e-9),
+        }
+        spmv_rate = times["spmv_nnz"] / (times["expmv_ms"] * 1e-3) * world
+
+        # ---- e2e: paces::step with a host SparseState in and out, every step (pinned host buffers)
+        e2e = None
+        if not args.no_e2e:
+            W = ctx.words
+            cap = int(rows * 1.25) + 1024
+            hw = [torch.empty(cap * W, dtype=torch.int32).pin_memory() for _ in range(2)]
+            hc = [torch.empty(cap * 2, dtype=torch.float64).pin_memory() for _ in range(2)]
+            nw = [x.numpy().view(np.uint32) for x in hw]
+            nc = [x.numpy().view(np.complex128) for x in hc]
+            w0, c0 = run.state()
+            n0 = len(c0)
+            nw[0][: n0 * W] = w0.ravel()
+            nc[0][:n0] = c0
+            cur, n_cur, t_cur, sidx = 0, n0, t_now, steps_done + 1
+            h2d = d2h = 0
+            kw = {k: v for k, v in run_kw.items() if k not in ("init", "site")}
+
+            def one(cur, n_cur, t_cur, sidx):
+                ow, oc, dd = ctx.step(nw[cur][: n_cur * W], nc[cur][:n_cur], t_cur, sidx, out_words=nw[cur ^ 1],
+                                      out_coeff=nc[cur ^ 1], **kw)
+                return len(oc), dd
+
+            for _ in range(3):
+                n_next, dd = one(cur, n_cur, t_cur, sidx)
+                cur, n_cur, t_cur, sidx = cur ^ 1, n_next, dd["t"], sidx + 1
+            k_e2e = max(5, min(args.steps, 20))
+            barrier()
+            ev0.record(stream)
+            for _ in range(k_e2e):
+                h2d += n_cur * (4 * W + 16)
+                n_next, dd = one(cur, n_cur, t_cur, sidx)
+                d2h += n_next * (4 * W + 16) + 72
+                cur, n_cur, t_cur, sidx = cur ^ 1, n_next, dd["t"], sidx + 1
+            ev1.record(stream)
+            barrier()
+            e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+            e2e = {"value": world * k_e2e / (float(e_ms.item()) * 1e-3), "unit": "timesteps/s",
+                   "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e, "steps": k_e2e,
+                   "api": "pb200_step + pb200_run_state (paces::step on a host SparseState, pinned buffers)"}
+
+    # ---- CPU baseline on the same state (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        pyoracle, orc, kind = cpu_checker()
+        om = orc.model(pyoracle.ModelDef(**MODEL))
+        w, c = run.state()
+        _, _, _, sd = run.info()
+        t0 = time.perf_counter()
+        ww, cc = w, c
+        for i in range(args.cpu_baseline_steps):
+            ww, cc, dcpu = cpu_step_from_state(pyoracle, orc, om, ww, cc, args.q_nom, run_kw["seed"], sd + 1 + i)
+        el = time.perf_counter() - t0
+        # parity gate next to the measurement: the GPU continues from the same state
+        dg = run.step()
+        wg, cg = run.state()
+        w1, c1, d1 = cpu_step_from_state(pyoracle, orc, om, w, c, args.q_nom, run_kw["seed"], sd + 1) \
+            if args.cpu_baseline_steps != 1 else (ww, cc, dcpu)
+        parity = {"table_bit_exact": bool(np.array_equal(wg, w1)), "coeff_bit_exact": cg.tobytes() == c1.tobytes(),
+                  "q_true": [int(dg["q_true"]), int(d1["q_true"])],
+                  "taylor_order": [int(dg["taylor_order"]), int(d1["taylor_order"])]}
+        cpu = {"value": args.cpu_baseline_steps / el, "unit": "timesteps/s", "cores": orc.threads(), "kind": kind,
+               "sample": f"{args.cpu_baseline_steps} timesteps from the GPU's resident steady state "
+                         f"(q_nom={args.q_nom}, q_true={len(c)}), stand-alone reference calls "
+                         "truncate_select/grow_subspace/remap_state/csr_expectation/expmv",
+               "parity_on_sample": parity}
+
+    if rank == 0:
+        line = {
+            "metric": "timesteps_per_sec", "value": value, "unit": "timesteps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128 amplitudes, u32 packed keys)",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "q_nom": args.q_nom, "q_true": rows, "nnz": nnz,
+                       "taylor_order": d["taylor_order"], "spinup_steps": spin,
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+                       "l2": "per-step working set (~150 B/row x q_true ~ 0.5 GB) exceeds the 126 MB L2; no flush"},
+            "spmv_nnz_per_sec": spmv_rate,
+            "wall_ms_per_step": 1e3 * wall / args.steps,
+            "phase_ms_per_step": {k: times[k] / args.steps for k in
+                                  ("select_ms", "grow_ms", "assemble_ms", "remap_ms", "expectation_ms", "expmv_ms",
+                                   "total_ms")},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

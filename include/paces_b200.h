@@ -157,11 +157,18 @@ int pb200_run_info(const pb200_ctx* ctx, uint64_t* rows, uint64_t* nnz, double* 
 /* Canonical-order download: keys ascending, coefficients aligned (checkpoint order, io.hpp:77-99). */
 int pb200_run_state(pb200_ctx* ctx, uint32_t* words, double* coeff);
 int pb200_run_csr(pb200_ctx* ctx, int64_t* row_ptr, int32_t* col, double* val);
-/* Replace the resident state/space by a host-supplied pair (checkpoint resume; also how bench.py
- * feeds a synthetic subspace): the space is re-grown from `words` with order 0?  No -- the table is
- * taken as is and H_eff is assembled over it (grow_subspace with m = 0, subspace.hpp:209 skipped). */
+/* Replaces the resident state/space by a host-supplied pair (checkpoint resume, io.hpp:101-144 read side):
+ * the sorted table is taken as is and H_eff is assembled over it (grow_subspace with m = 0). */
 int pb200_run_load_state(pb200_ctx* ctx, const pb200_run_cfg* cfg, const uint32_t* words,
                          const double* coeff, uint64_t rows, double t, uint64_t steps_done);
+/* step() (engine.hpp:268-291) as a stand-alone operator on HOST buffers: uploads the caller's SparseState
+ * (sorted table + coefficients at time t), runs select -> grow -> remap -> expectation -> expmv for
+ * step_index >= 2 (the index only feeds the tie-break seed, engine.hpp:275) and leaves the new
+ * (state, space) resident; rows_out/nnz_out size the buffers for pb200_run_state / pb200_run_csr, which
+ * download StepOutput.state and StepOutput.space. */
+int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
+               const double* coeff, uint64_t rows, double t, pb200_diag* out, uint64_t* rows_out,
+               uint64_t* nnz_out);
 /* detail::observe (engine.hpp:299-311): ObservablesRow of the resident state; density has
  * lattice_sites entries, amp is (re, im). */
 int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar,

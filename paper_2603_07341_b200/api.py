@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
-    "pb200_run_state", "pb200_run_csr", "pb200_run_load_state", "pb200_run_observe", "pb200_run_times",
+    "pb200_run_state", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_run_observe", "pb200_run_times",
     "pb200_run_reset_times", "pb200_bench_taylor", "pb200_bench_spmv",
 ]
 
@@ -141,6 +141,8 @@ def load_library():
     L.pb200_run_state.argtypes = [vp, u32p, f64p]
     L.pb200_run_csr.argtypes = [vp, i64p, i32p, f64p]
     L.pb200_run_load_state.argtypes = [vp, C.POINTER(RunCfg), u32p, f64p, C.c_uint64, C.c_double, C.c_uint64]
+    L.pb200_step.argtypes = [vp, C.POINTER(RunCfg), C.c_uint64, u32p, f64p, C.c_uint64, C.c_double, C.POINTER(Diag), u64p,
+                             u64p]
     L.pb200_run_observe.argtypes = [vp, f64p, f64p, f64p, f64p, f64p, f64p]
     L.pb200_run_times.argtypes = [vp, C.POINTER(PhaseTimes)]
     L.pb200_run_reset_times.argtypes = [vp]
@@ -215,6 +217,10 @@ class Context:
     def _ck(self, rc):
         if rc != 0:
             raise PacesError(self.lib.pb200_last_error(self.h).decode(), rc)
+
+    def set_stream(self, cuda_stream_handle: int):
+        """Run on an externally owned CUDA stream (e.g. torch.cuda.Stream().cuda_stream)."""
+        self._ck(self.lib.pb200_ctx_set_stream(self.h, C.c_void_p(int(cuda_stream_handle))))
 
     @property
     def kernel_launches(self) -> int:
@@ -348,6 +354,24 @@ class Context:
         p = np.zeros(self.lattice_sites)
         self._ck(self.lib.pb200_phonon_numbers(self.h, _p(w, u32p), _p(cf, f64p), w.shape[0], _p(p, f64p)))
         return p
+
+    def step(self, words, coeff, t, step_index, out_words=None, out_coeff=None, **kw):
+        """paces::step on host buffers (engine.hpp:268-291): (new words, new coeff, DiagnosticsRecord dict).
+
+        out_words/out_coeff: optional preallocated (e.g. pinned) arrays large enough for the result.
+        """
+        w = _u32(words).reshape(-1, self.words)
+        c, cf = _cview(coeff)
+        cfg, keep = make_cfg(self.layout_sites, **kw)
+        d = Diag()
+        rows, nnz = C.c_uint64(), C.c_uint64()
+        self._ck(self.lib.pb200_step(self.h, C.byref(cfg), step_index, _p(w, u32p), _p(cf, f64p), w.shape[0], t,
+                                     C.byref(d), C.byref(rows), C.byref(nnz)))
+        n = rows.value
+        ow = np.zeros((n, self.words), np.uint32) if out_words is None else out_words[: n * self.words].reshape(n, self.words)
+        oc = np.zeros(n, np.complex128) if out_coeff is None else out_coeff[:n]
+        self._ck(self.lib.pb200_run_state(self.h, _p(ow, u32p), _p(oc.view(np.float64), f64p)))
+        return ow, oc, d.as_dict()
 
     # ---- resident trajectory -------------------------------------------------------------------
     def run(self, **kw) -> "Run":

@@ -416,6 +416,44 @@ int pb200_run_load_state(pb200_ctx* ctx, const pb200_run_cfg* cfg, const uint32_
     });
 }
 
+int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
+               const double* coeff, uint64_t rows, double t, pb200_diag* out, uint64_t* rows_out, uint64_t* nnz_out) {
+    return guarded(ctx, [&](Engine& e) {
+        e.require_model();
+        need(cfg && words && coeff, "step: null pointer");
+        need(step_index >= 2, "step: step_index must be >= 2 (step 1 evolves on the initial space, use pb200_run_*)");
+        if (rows == 0) throw PacesError("truncate_select: state has no support");
+        need(rows <= 0x7fffffffull, "too many rows");
+        pb200_run_cfg c = *cfg;
+        c.init_kind = 0;
+        c.n_entries = 0;
+        c.entry_occ = nullptr;
+        c.entry_amp = nullptr;
+        e.cfg = c;
+        e.has_cfg = true;
+        e.has_state = false;
+        // the caller's table must be sorted (engine.hpp:110); checked on the device copy would cost a kernel, the
+        // host pass is a streaming compare of data that is about to cross PCIe anyway
+        if (!host_rows_sorted(words, rows, e.hm.W)) throw PacesError("truncate_select: state table must be sorted");
+        Space& sp = e.space[e.cur];
+        const size_t W = e.hm.W;
+        sp.words.ensure(rows * W * 4 + 4);
+        e.coeff[e.ccur].ensure(rows * 16 + 16);
+        PB_CUDA(cudaMemcpyAsync(sp.words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.stream));
+        PB_CUDA(cudaMemcpyAsync(e.coeff[e.ccur].p, coeff, rows * 16, cudaMemcpyHostToDevice, e.stream));
+        sp.n = uint32_t(rows);
+        sp.nnz = 0;
+        sp.has_h = false;
+        e.t = t;
+        e.steps_done = step_index - 1;
+        e.has_state = true;
+        e.run_step(out);
+        const Space& nsp = e.space[e.cur];
+        if (rows_out) *rows_out = nsp.n;
+        if (nnz_out) *nnz_out = nsp.nnz;
+    });
+}
+
 int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar, double* amp,
                       double* density) {
     return guarded(ctx, [&](Engine& e) {
