@@ -164,8 +164,9 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
         PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
         PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
         const uint32_t* fr = identity_frontier ? nullptr : frontier[fcur].as<uint32_t>();
-        PB_DISPATCH_W(W, expand_level_kernel<W><<<grid_for(nf), NT, 0, stream>>>(
-                             md, out.words.as<uint32_t>(), n, fr, nf, cand_keys.as<uint32_t>(),
+        const uint32_t xchunk = chunk_for(nf);
+        PB_DISPATCH_W(W, expand_level_kernel<W><<<grid_chunked(nf, xchunk), NT, 0, stream>>>(
+                             md, out.words.as<uint32_t>(), n, fr, nf, xchunk, cand_keys.as<uint32_t>(),
                              cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow, count_emitted));
         check_launch();
         GrowCounters gc = read_back<GrowCounters>(&c->grow);
@@ -236,8 +237,9 @@ void Engine::assemble(Space& sp) {
     tmp_col.ensure(size_t(n) * width * 4);
     tmp_val.ensure(size_t(n) * width * 8);
     sp.row_ptr.ensure((size_t(n) + 1) * 4);
-    PB_DISPATCH_W(W, assemble_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
-                         md, sp.words.as<uint32_t>(), n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
+    const uint32_t achunk = chunk_for(n);
+    PB_DISPATCH_W(W, assemble_rows_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
+                         md, sp.words.as<uint32_t>(), n, achunk, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                          sp.row_ptr.as<uint32_t>()));
     check_launch();
     PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
@@ -343,8 +345,10 @@ double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t n
     const int W = md.W;
     Ctl* c = dctl();
     PB_CUDA(cudaMemsetAsync(dst_c, 0, size_t(nd) * 16, stream));
-    PB_DISPATCH_W(W, remap_kernel<W><<<grid_for(ns), NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, dst_c,
-                                                                      partials.as<double>(), &c->ticket, c->out));
+    const uint32_t rchunk = 1;
+    const int rgrid = grid_for(ns);
+    PB_DISPATCH_W(W, remap_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
+                                                               partials.as<double>(), &c->ticket, c->out));
     check_launch();
     return read_back<double>(c->out);
 }

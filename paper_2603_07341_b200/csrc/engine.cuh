@@ -155,6 +155,19 @@ struct Engine {
         if (g < 1) g = 1;
         return int(g);
     }
+    /// Rows per thread for the cursor kernels: long enough to amortise the first full search, short enough
+    /// to keep ~3/4 of the machine's thread slots busy.
+    uint32_t chunk_for(uint64_t n) const {
+        const uint64_t slots = uint64_t(sm_count) * 1536;
+        uint32_t c = 16;
+        while (c > 2 && n / c < slots) c >>= 1;
+        return c;
+    }
+    int grid_chunked(uint64_t n, uint32_t chunk) const {
+        const uint64_t threads = (n + chunk - 1) / chunk;
+        const uint64_t g = (threads + NT - 1) / NT;
+        return int(g < 1 ? 1 : g);
+    }
     void sync() { PB_CUDA(cudaStreamSynchronize(stream)); }
     void check_launch() {
         ++launches;

@@ -31,24 +31,32 @@ struct GrowCounters {
 /// lattice_models.hpp:212-267; apply_to_rows, subspace.hpp:102-134), look each one up in the sorted
 /// table and append those that are absent, together with their insertion gap.  gap_count[g] counts the
 /// candidates that fall between table rows g-1 and g.
+/// Each thread walks `chunk` CONSECUTIVE frontier rows (ascending keys) with one cursor per move, so all
+/// look-ups after the first are short forward gallops (per-thread merge join with the table).
 /// frontier == nullptr means "all rows" (order 0: the seeds are the table).
 template <int W>
 __global__ void __launch_bounds__(NT) expand_level_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
                                                           const uint32_t* __restrict__ frontier, uint32_t nf,
-                                                          uint32_t* __restrict__ cand_keys,
+                                                          uint32_t chunk, uint32_t* __restrict__ cand_keys,
                                                           uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
                                                           uint32_t* __restrict__ gap_count, GrowCounters* ctr,
                                                           int count_emitted) {
     unsigned long long emitted = 0;
-    for (uint32_t f = blockIdx.x * NT + threadIdx.x; f < nf; f += gridDim.x * NT) {
-        const uint32_t row = frontier ? __ldg(frontier + f) : f;
+    // a warp covers 32*chunk consecutive frontier rows; lane l takes rows base + 32 j + l, so every step of
+    // the warp reads 32 consecutive rows (coalesced) while each lane still sees ascending keys
+    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
+    MoveCursors cur;
+    cur.reset(0xffffffffu);
+    for (uint64_t f = wbase; f < min(uint64_t(nf), uint64_t(wbase + 32ull * chunk)); f += 32) {
+        const uint32_t row = frontier ? __ldg(frontier + f) : uint32_t(f);
         const Key<W> k = load_key<W>(table + size_t(row) * W);
         const uint32_t e = exciton_site<W>(m, k);
+        if (e != cur.site) cur.reset(e);
         if (count_emitted && diagonal_element<W>(m, k, e) != 0.0) ++emitted;
-        for_each_neighbor<W>(m, k, false, [&](int, const Key<W>& kk, double, bool) {
+        for_each_neighbor<W>(m, k, false, [&](int move, const Key<W>& kk, double, bool) {
             ++emitted;
             uint32_t pos;
-            if (!find_row<W>(table, n, kk, pos)) {
+            if (!cursor_find<W>(table, n, cur, move, kk, pos)) {
                 const uint32_t slot = append_slot(&ctr->n_cand);
                 if (slot < cand_cap) {
                     store_key<W>(cand_keys + size_t(slot) * W, kk);
@@ -176,25 +184,27 @@ constexpr int MAX_ROW = 2 * 3 + 3;  // hops (<= 6) + 2 ladder + diagonal
 /// Pass 1: row i of H_eff = {(index(k'), a) : (k', a) in apply_terms(key_i), k' in table}
 /// (replaces assemble_effective_hamiltonian, subspace.hpp:142-187, and the
 /// final-frontier filter, :225-241).  Neighbours are generated in ascending key order, so the found
-/// columns are already ascending.  Results are parked in fixed-width scratch (stride `width`).
+/// columns are already ascending.  Each thread walks `chunk` consecutive rows with per-move cursors
+/// (see expand_level_kernel).  Results are parked in fixed-width scratch (stride `width`).
 template <int W>
 __global__ void __launch_bounds__(NT) assemble_rows_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
-                                                           int width, uint32_t* __restrict__ tmp_col,
+                                                           uint32_t chunk, int width, uint32_t* __restrict__ tmp_col,
                                                            double* __restrict__ tmp_val,
                                                            uint32_t* __restrict__ row_len) {
-    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
+    MoveCursors cur;
+    cur.reset(0xffffffffu);
+    for (uint64_t ii = wbase; ii < min(uint64_t(n), uint64_t(wbase + 32ull * chunk)); ii += 32) {
+        const uint32_t i = uint32_t(ii);
         const Key<W> k = load_key<W>(table + size_t(i) * W);
+        const uint32_t e = exciton_site<W>(m, k);
+        if (e != cur.site) cur.reset(e);
         int len = 0;
         uint32_t* tc = tmp_col + size_t(i) * width;
         double* tv = tmp_val + size_t(i) * width;
-        for_each_neighbor<W>(m, k, true, [&](int, const Key<W>& kk, double amp, bool is_diag) {
+        for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
             uint32_t pos = i;
-            bool found = true;
-            if (!is_diag) {
-                // a smaller neighbour lives in [0, i), a larger one in (i, n)
-                const bool below = key_cmp<W>(kk, k) < 0;
-                found = below ? find_row_in<W>(table, 0, i, kk, pos) : find_row_in<W>(table, i + 1, n, kk, pos);
-            }
+            const bool found = is_diag ? true : cursor_find<W>(table, n, cur, move, kk, pos);
             if (found) {
                 tc[len] = pos;
                 tv[len] = amp;
@@ -467,11 +477,12 @@ __global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __rest
 template <int W>
 __global__ void __launch_bounds__(NT) remap_kernel(const uint32_t* __restrict__ src_table,
                                                    const double2* __restrict__ src_c, uint32_t ns,
-                                                   const uint32_t* __restrict__ dst_table, uint32_t nd,
+                                                   const uint32_t* __restrict__ dst_table, uint32_t nd, uint32_t chunk,
                                                    double2* __restrict__ dst_c, double* __restrict__ partials,
                                                    unsigned* ticket, double* __restrict__ out) {
     __shared__ double smem[NT / 32];
     double acc[1] = {0.0};
+    (void)chunk;
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < ns; i += gridDim.x * NT) {
         const Key<W> k = load_key<W>(src_table + size_t(i) * W);
         const double2 x = src_c[i];

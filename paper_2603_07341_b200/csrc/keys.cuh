@@ -189,11 +189,17 @@ __device__ __forceinline__ double diagonal_element(const ModelDev& m, const Key<
     return diag;
 }
 
+constexpr int MOVE_LOWER = MAX_NB;      // stable move ids: 0..MAX_NB-1 = hop to the d-th partner of the site
+constexpr int MOVE_RAISE = MAX_NB + 1;
+constexpr int MOVE_DIAG = MAX_NB + 2;
+constexpr int N_MOVES = MAX_NB + 2;     // off-diagonal moves
+
 /// Neighbour generator in CANONICAL (ascending key) order:
 ///   hops to partners t < e (ascending t) | lower n_e | diagonal | raise n_e | hops to t > e (ascending t)
 /// A hop rewrites the most significant field, so t < e sorts before every key with site0 = e; the
-/// ladder moves keep site0 and change one later field.  F is called as f(slot, key', amp, is_diag);
-/// slot numbers are stable per (site, move) so a caller can tabulate per-slot results.
+/// ladder moves keep site0 and change one later field.  F is called as f(move, key', amp, is_diag) with
+/// the stable move id above.  Every move is strictly order-preserving on keys that share the exciton
+/// site (it adds a fixed multi-word constant), which the cursor searches below rely on.
 /// Amplitudes follow lattice_models.hpp:236-248: g*sqrt(double(n+1)) (dropped at the cutoff
 /// n+1 == d_pho), g*sqrt(double(n)), bond J; sqrt is the correctly rounded IEEE one.
 template <int W, class F>
@@ -201,14 +207,13 @@ __device__ __forceinline__ void for_each_neighbor(const ModelDev& m, const Key<W
     const uint32_t e = exciton_site<W>(m, k);
     const int* nbs = m.nb_site + size_t(e) * MAX_NB;
     const double* nba = m.nb_amp + size_t(e) * MAX_NB;
-    int slot = 0;
     int d = 0;
     for (; d < MAX_NB; ++d) {
         const int t = __ldg(nbs + d);
         if (t < 0 || uint32_t(t) > e) break;
         Key<W> kk = k;
         set_bits<W>(kk, 0, m.b0, uint32_t(t));
-        f(slot++, kk, __ldg(nba + d), false);
+        f(d, kk, __ldg(nba + d), false);
     }
     uint32_t n = 0;
     double ge = 0.0;
@@ -219,24 +224,74 @@ __device__ __forceinline__ void for_each_neighbor(const ModelDev& m, const Key<W
     if (ge != 0.0 && n >= 1) {
         Key<W> kk = k;
         set_bits<W>(kk, m.b0 + int(e) * m.bp, m.bp, n - 1);
-        f(slot++, kk, __dmul_rn(ge, __dsqrt_rn(double(n))), false);
+        f(MOVE_LOWER, kk, __dmul_rn(ge, __dsqrt_rn(double(n))), false);
     }
     if (with_diag) {
         const double diag = diagonal_element<W>(m, k, e);
-        if (diag != 0.0) f(slot++, k, diag, true);
+        if (diag != 0.0) f(MOVE_DIAG, k, diag, true);
     }
     if (ge != 0.0 && n + 1 < m.d_pho) {
         Key<W> kk = k;
         set_bits<W>(kk, m.b0 + int(e) * m.bp, m.bp, n + 1);
-        f(slot++, kk, __dmul_rn(ge, __dsqrt_rn(double(n + 1))), false);
+        f(MOVE_RAISE, kk, __dmul_rn(ge, __dsqrt_rn(double(n + 1))), false);
     }
     for (; d < MAX_NB; ++d) {
         const int t = __ldg(nbs + d);
         if (t < 0) break;
         Key<W> kk = k;
         set_bits<W>(kk, 0, m.b0, uint32_t(t));
-        f(slot++, kk, __ldg(nba + d), false);
+        f(d, kk, __ldg(nba + d), false);
     }
+}
+
+/// Forward search from a cursor: the answer (lower bound of k) is known to be >= start.  Gallops
+/// 1, 2, 4, ... rows ahead, then bisects.  When a thread walks consecutive sorted rows, the targets of
+/// one move are increasing, so the next answer is usually within a few rows of the previous one: a
+/// handful of cache-local probes instead of log2(n) scattered ones (a per-thread merge join).
+template <int W>
+__device__ __forceinline__ bool gallop_find(const uint32_t* __restrict__ table, uint32_t n, uint32_t start,
+                                            const Key<W>& k, uint32_t& pos) {
+    uint32_t lo = start, hi = start, step = 1;
+    while (hi < n) {
+        const int c = row_cmp<W>(table + size_t(hi) * W, k);
+        if (c == 0) {
+            pos = hi;
+            return true;
+        }
+        if (c > 0) break;
+        lo = hi + 1;
+        hi = (n - hi > step) ? hi + step : n;
+        step <<= 1;
+    }
+    return find_row_in<W>(table, lo, hi < n ? hi : n, k, pos);
+}
+
+/// Per-thread cursors, one per move; CUR_NONE = no previous answer (do a full binary search).
+constexpr uint32_t CUR_NONE = 0xffffffffu;
+struct MoveCursors {
+    uint32_t c[N_MOVES];
+    uint32_t site;
+    __device__ __forceinline__ void reset(uint32_t e) {
+#pragma unroll
+        for (int i = 0; i < N_MOVES; ++i) c[i] = CUR_NONE;
+        site = e;
+    }
+};
+
+/// Look-up of the `move` neighbour of a row that a thread visits in ascending order.
+template <int W>
+__device__ __forceinline__ bool cursor_find(const uint32_t* __restrict__ table, uint32_t n, MoveCursors& cur, int move,
+                                            const Key<W>& k, uint32_t& pos) {
+    uint32_t start = 0;
+#pragma unroll
+    for (int i = 0; i < N_MOVES; ++i)
+        if (i == move) start = cur.c[i];
+    const bool found = (start == CUR_NONE) ? find_row<W>(table, n, k, pos) : gallop_find<W>(table, n, start, k, pos);
+    const uint32_t next = found ? pos + 1 : pos;
+#pragma unroll
+    for (int i = 0; i < N_MOVES; ++i)
+        if (i == move) cur.c[i] = next;
+    return found;
 }
 
 }  // namespace pb
