@@ -45,8 +45,8 @@ Engine::Engine(int dev) : device(dev) {
     ctl.ensure(sizeof(Ctl));
     PB_CUDA(cudaMemsetAsync(ctl.p, 0, sizeof(Ctl), stream));
     partials.ensure(sizeof(double) * 4 * size_t(sm_count) * 8);
-    hist.ensure(256 * sizeof(uint32_t));
-    PB_CUDA(cudaMemsetAsync(hist.p, 0, 256 * sizeof(uint32_t), stream));
+    hist.ensure(SEL_BINS * sizeof(uint32_t));
+    PB_CUDA(cudaMemsetAsync(hist.p, 0, SEL_BINS * sizeof(uint32_t), stream));
     sync();
 }
 
@@ -267,7 +267,7 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
     const int W = md.W;
     Ctl* c = dctl();
     weights.ensure(size_t(n) * 8 + 8);
-    PB_CUDA(cudaMemsetAsync(hist.p, 0, 256 * sizeof(uint32_t), stream));
+    PB_CUDA(cudaMemsetAsync(hist.p, 0, SEL_BINS * sizeof(uint32_t), stream));
     flag_keep.ensure((size_t(n) + 1) * 4);
     const int g = grid_for(n);
     SelectCtl init{};
@@ -285,10 +285,13 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
         check_launch();
     } else {
-        for (int shift = 56; shift >= 0; shift -= 8) {
-            select_hist_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, shift, &c->select, hist.as<uint32_t>());
-            check_launch();
-            select_pick_kernel<<<1, 32, 0, stream>>>(hist.as<uint32_t>(), &c->select);
+        // 6 passes over 64 bits: 11-bit digits from the top, the last one 9 bits wide
+        static const int shifts[6] = {53, 42, 31, 20, 9, 0};
+        static const int widths[6] = {11, 11, 11, 11, 11, 9};
+        const int sg = std::min(g, sm_count * 2);
+        for (int p = 0; p < 6; ++p) {
+            select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
+                                                      hist.as<uint32_t>());
             check_launch();
         }
         sc = read_back<SelectCtl>(&c->select);

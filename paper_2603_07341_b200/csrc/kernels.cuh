@@ -376,41 +376,69 @@ __global__ void __launch_bounds__(NT) weights_kernel(const double2* __restrict__
     }
 }
 
-/// Histogram of the 8-bit digit at `shift` over the weights whose higher bits equal ctl->prefix.
-/// Positive doubles order like their bit patterns, so this is an exact selection.
-__global__ void __launch_bounds__(NT) select_hist_kernel(const double* __restrict__ w, uint32_t n, int shift,
-                                                         const SelectCtl* __restrict__ ctl,
-                                                         uint32_t* __restrict__ hist) {
-    __shared__ uint32_t sh[256];
-    sh[threadIdx.x] = 0;
+/// Radix select, one pass: histogram of the `width`-bit digit at `shift` over the weights whose higher
+/// bits equal ctl->prefix (positive doubles order like their bit patterns, so the selection is exact),
+/// then -- in the last CTA to finish -- the pick: walk the bins from the top until the wanted rank k falls
+/// inside one, extend the prefix by that digit, and clear the histogram for the next pass.
+constexpr int SEL_BITS = 11;
+constexpr int SEL_BINS = 1 << SEL_BITS;
+
+__global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restrict__ w, uint32_t n, int shift, int width,
+                                                         SelectCtl* ctl, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[SEL_BINS];
+    __shared__ uint32_t wsum[NT / 32];
+    __shared__ bool is_last;
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) sh[i] = 0;
     __syncthreads();
     const unsigned long long prefix = ctl->prefix;
+    const uint32_t dmask = (1u << width) - 1u;
+    const int hi_shift = shift + width;
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         const double ww = w[i];
         if (!(ww > 0.0)) continue;
         const unsigned long long bits = (unsigned long long)__double_as_longlong(ww);
-        if (shift == 56 || (bits >> (shift + 8)) == prefix) atomicAdd(&sh[(bits >> shift) & 255u], 1u);
+        if (hi_shift >= 64 || (bits >> hi_shift) == prefix) atomicAdd(&sh[uint32_t(bits >> shift) & dmask], 1u);
     }
     __syncthreads();
-    const uint32_t v = sh[threadIdx.x];
-    if (v) atomicAdd(hist + threadIdx.x, v);
-}
-
-__global__ void select_pick_kernel(uint32_t* __restrict__ hist, SelectCtl* ctl) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    unsigned long long k = ctl->k, gt = ctl->count_gt;
-    int d = 255;
-    for (; d > 0; --d) {
-        const unsigned long long h = hist[d];
-        if (k <= h) break;
-        k -= h;
-        gt += h;
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) {
+        const uint32_t v = sh[i];
+        if (v) atomicAdd(hist + i, v);
     }
-    ctl->count_eq = hist[d];
-    ctl->prefix = (ctl->prefix << 8) | (unsigned long long)d;
-    ctl->k = k;
-    ctl->count_gt = gt;
-    for (int i = 0; i < 256; ++i) hist[i] = 0;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // pick: bins in DESCENDING order, thread t owns descending positions [t*PER, (t+1)*PER)
+    constexpr int PER = SEL_BINS / NT;
+    uint32_t loc[PER];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        loc[j] = __ldcg(hist + (SEL_BINS - 1 - (threadIdx.x * PER + j)));
+        s += loc[j];
+    }
+    uint32_t tot;
+    const uint32_t before = block_exclusive_scan_u32(s, wsum, tot);  // weights in higher bins owned by earlier threads
+    const unsigned long long k = ctl->k;
+    if (k > before && k <= (unsigned long long)before + s) {
+        unsigned long long kk = k - before, gt = ctl->count_gt + before;
+        int j = 0;
+        for (; j < PER - 1; ++j) {
+            if (kk <= loc[j]) break;
+            kk -= loc[j];
+            gt += loc[j];
+        }
+        const uint32_t d = SEL_BINS - 1 - (threadIdx.x * PER + j);
+        ctl->count_eq = loc[j];
+        ctl->prefix = (prefix << width) | (unsigned long long)d;
+        ctl->k = kk;
+        ctl->count_gt = gt;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) hist[i] = 0;
+    if (threadIdx.x == 0) ctl->ticket = 0;
 }
 
 /// mode 0: keep every supported row (w > 0).  mode 1: keep w > cutoff, and w == cutoff too when

@@ -83,46 +83,42 @@ __device__ __forceinline__ int row_cmp(const uint32_t* __restrict__ row, const K
     return 0;
 }
 
+/// Branch-free "row < key" with all words loaded up front (independent loads, no early-exit divergence).
+template <int W>
+__device__ __forceinline__ bool row_less_key(const uint32_t* __restrict__ row, const Key<W>& k) {
+    uint32_t v[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] = __ldg(row + i);
+    bool lt = false;
+#pragma unroll
+    for (int i = W - 1; i >= 0; --i) lt = (v[i] < k.w[i]) || (v[i] == k.w[i] && lt);
+    return lt;
+}
+
+/// Lower bound of k in table[lo, hi): uniform trip count (depends only on hi - lo), conditional moves
+/// instead of branches, so a warp never diverges inside the search.
+template <int W>
+__device__ __forceinline__ bool find_row_in(const uint32_t* __restrict__ table, uint32_t lo, uint32_t hi,
+                                            const Key<W>& k, uint32_t& pos) {
+    const uint32_t end = hi;
+    uint32_t len = hi - lo;
+    while (len > 0) {
+        const uint32_t half = len >> 1;
+        const uint32_t mid = lo + half;
+        const bool lt = row_less_key<W>(table + size_t(mid) * W, k);
+        lo = lt ? mid + 1 : lo;
+        len = lt ? len - half - 1 : half;
+    }
+    pos = lo;
+    return lo < end && row_cmp<W>(table + size_t(lo) * W, k) == 0;
+}
+
 /// Binary search in a sorted table (find_row, basis_codec.hpp:334-348).  Returns true and the row
 /// index when present; otherwise false and the insertion point (number of rows < key).
 template <int W>
 __device__ __forceinline__ bool find_row(const uint32_t* __restrict__ table, uint32_t n, const Key<W>& k,
                                          uint32_t& pos) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        const int c = row_cmp<W>(table + size_t(mid) * W, k);
-        if (c == 0) {
-            pos = mid;
-            return true;
-        }
-        if (c < 0)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    pos = lo;
-    return false;
-}
-
-/// Same search restricted to [lo, hi) (callers that know a bracket).
-template <int W>
-__device__ __forceinline__ bool find_row_in(const uint32_t* __restrict__ table, uint32_t lo, uint32_t hi,
-                                            const Key<W>& k, uint32_t& pos) {
-    while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        const int c = row_cmp<W>(table + size_t(mid) * W, k);
-        if (c == 0) {
-            pos = mid;
-            return true;
-        }
-        if (c < 0)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    pos = lo;
-    return false;
+    return find_row_in<W>(table, 0, n, k, pos);
 }
 
 /// b-bit field at bit offset off (get_site, basis_codec.hpp:90-108).  b in [0, 32].
