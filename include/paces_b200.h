@@ -93,6 +93,29 @@ uint64_t pb200_kernel_launches(const pb200_ctx* ctx);
 /* common.hpp:76-81 (host-side splitmix64; the per-step tie-break seed of engine.hpp:275). */
 uint64_t pb200_mix_seed(uint64_t x);
 
+/* ---- multi-GPU: one process (and one context) per GPU; the table is sharded by hash of the phonon part of the
+ * basis key.  The library does not talk to NCCL itself: the host supplies the collectives
+ * (torch.distributed over NCCL in production -- plumbing -- or any other transport) through this table.  Device
+ * variants receive DEVICE pointers on the context's device plus the context's stream; they must be complete or
+ * stream-ordered on that stream when they return.  Host variants are small blocking collectives on host memory.
+ * All ranks call every pb200_* function collectively and in the same order.  Every callback returns 0 on success. */
+typedef struct pb200_comm_ops {
+    void* user;
+    int (*allreduce_f64_host)(void* user, double* buf, uint64_t n);          /* sum, in place */
+    int (*allreduce_u64_host)(void* user, uint64_t* buf, uint64_t n);        /* sum, in place */
+    int (*alltoall_u64_host)(void* user, const uint64_t* send, uint64_t* recv); /* one value per peer */
+    int (*allgather_host)(void* user, const void* send, uint64_t nbytes, void* recv); /* recv: world * nbytes */
+    /* buckets are contiguous and in rank order on both sides; counts are in elements of elem_bytes bytes */
+    int (*alltoallv_dev)(void* user, const void* send, const uint64_t* send_counts, void* recv,
+                         const uint64_t* recv_counts, uint64_t elem_bytes, void* stream);
+    int (*allreduce_f64_dev)(void* user, double* buf, uint64_t n, void* stream);   /* sum, in place */
+    int (*allreduce_u32_dev)(void* user, uint32_t* buf, uint64_t n, void* stream); /* sum, in place */
+} pb200_comm_ops;
+/* Must be called before pb200_model_set; world == 1 (or never calling it) is the single-GPU path. */
+int pb200_ctx_set_comm(pb200_ctx* ctx, int rank, int world, const pb200_comm_ops* ops);
+/* Shard owner of a key (host-side restatement of the device rule), and this context's rank/world. */
+int pb200_owner_of(const pb200_ctx* ctx, const uint32_t* key, uint32_t world, uint32_t* owner);
+
 /* ---- model: build_model (lattice_models.hpp:140-189) ---------------------------------------------
  * kind: 0 tight_binding, 1 holstein.  eps/hop/omega/g hold 0, 1 or n values (broadcast rule of
  * lattice_models.hpp:129-136; hop is per bond in LatticeGeometry::bonds() order, :54-65).  The

@@ -26,7 +26,7 @@ intp = C.POINTER(C.c_int)
 
 EXPORTED_SYMBOLS = [
     "pb200_ctx_create", "pb200_ctx_destroy", "pb200_last_error", "pb200_version", "pb200_ctx_set_stream",
-    "pb200_kernel_launches", "pb200_mix_seed", "pb200_model_set", "pb200_model_info", "pb200_pack", "pb200_unpack",
+    "pb200_kernel_launches", "pb200_mix_seed", "pb200_ctx_set_comm", "pb200_owner_of", "pb200_model_set", "pb200_model_info", "pb200_pack", "pb200_unpack",
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
@@ -116,6 +116,8 @@ def load_library():
     L.pb200_kernel_launches.restype = C.c_uint64
     L.pb200_mix_seed.argtypes = [C.c_uint64]
     L.pb200_mix_seed.restype = C.c_uint64
+    L.pb200_ctx_set_comm.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.pb200_owner_of.argtypes = [vp, u32p, C.c_uint32, u32p]
     L.pb200_model_set.argtypes = [vp, C.c_int, C.c_int, u32p, f64p, C.c_int, f64p, C.c_int, f64p, C.c_int, f64p,
                                   C.c_int, C.c_uint32]
     L.pb200_model_info.argtypes = [vp, u32p, u32p, u32p, u32p, u32p]
@@ -192,7 +194,7 @@ def make_cfg(layout_sites, init="localized", site=-1, entries=None, m_init=6, m=
 class Context:
     """One GPU context + one model.  ``Context(model_def, device=0)``."""
 
-    def __init__(self, model: ModelDef | None = None, device: int = 0):
+    def __init__(self, model: ModelDef | None = None, device: int = 0, comm=None):
         self.lib = load_library()
         h = C.c_void_p()
         rc = self.lib.pb200_ctx_create(int(device), C.byref(h))
@@ -200,8 +202,25 @@ class Context:
             raise PacesError(self.lib.pb200_last_error(None).decode(), rc)
         self.h = h
         self.d = None
+        self.comm = None
+        if comm is not None:
+            self.set_comm(comm)
         if model is not None:
             self.set_model(model)
+
+    def set_comm(self, comm):
+        """Sharded (multi-GPU) mode: `comm` is a paper_2603_07341_b200.dist.TorchComm (or anything exposing
+        rank, world and a pb200_comm_ops struct as .ops).  Call before set_model."""
+        self.comm = comm  # keeps the callbacks alive
+        self._ck(self.lib.pb200_ctx_set_comm(self.h, int(comm.rank), int(comm.world), C.addressof(comm.ops)))
+
+    def owner_of(self, key, world):
+        key = _u32(key)
+        out = C.c_uint32()
+        rc = self.lib.pb200_owner_of(self.h, _p(key, u32p), int(world), C.byref(out))
+        if rc != 0:
+            raise PacesError("owner_of: bad arguments", rc)
+        return out.value
 
     def close(self):
         if getattr(self, "h", None):

@@ -113,6 +113,27 @@ uint64_t pb200_mix_seed(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+int pb200_ctx_set_comm(pb200_ctx* ctx, int rank, int world, const pb200_comm_ops* ops) {
+    return guarded(ctx, [&](Engine& e) {
+        need(world >= 1 && world <= 64 && rank >= 0 && rank < world, "set_comm: bad rank/world (world <= 64)");
+        if (world > 1) {
+            need(ops && ops->allreduce_f64_host && ops->allreduce_u64_host && ops->alltoall_u64_host &&
+                     ops->allgather_host && ops->alltoallv_dev && ops->allreduce_f64_dev && ops->allreduce_u32_dev,
+                 "set_comm: every collective must be supplied when world > 1");
+            e.ops = *ops;
+        }
+        e.rank = rank;
+        e.world = world;
+        e.has_state = false;
+    });
+}
+
+int pb200_owner_of(const pb200_ctx* ctx, const uint32_t* key, uint32_t world, uint32_t* owner) {
+    if (!ctx || !ctx->eng.has_model || !key || !owner || world == 0) return PB200_ERR_ARG;
+    *owner = host_owner(ctx->eng.hm, key, world);
+    return PB200_OK;
+}
+
 // ---- model ---------------------------------------------------------------------------------------
 int pb200_model_set(pb200_ctx* ctx, int kind, int ndim, const uint32_t* extents, const double* eps, int n_eps,
                     const double* hop, int n_hop, const double* omega, int n_omega, const double* g, int n_g,
@@ -384,6 +405,7 @@ int pb200_run_state(pb200_ctx* ctx, uint32_t* words, double* coeff) {
 int pb200_run_csr(pb200_ctx* ctx, int64_t* row_ptr, int32_t* col, double* val) {
     return guarded(ctx, [&](Engine& e) {
         need(e.has_state, "no resident state");
+        // sharded: this is the rank-local CSR block; columns >= local rows index the halo
         download_csr(e, e.space[e.cur], row_ptr, col, val);
     });
 }
@@ -556,7 +578,7 @@ int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush, double dt, double*
             taylor_order_kernel<<<e.grid_for(n), NT, 0, e.stream>>>(
                 n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
                 e.term[(o - 1) & 1].as<double2>(), e.term[o & 1].as<double2>(), e.aux_coeff.as<double2>(),
-                -dt / double(o), o, 1e-15, e.partials.as<double>(), &c->taylor, 1);
+                -dt / double(o), o, 1e-15, e.partials.as<double>(), &c->taylor, 1, nullptr);
             e.check_launch();
             PB_CUDA(cudaEventRecord(e.ev[9], e.stream));
             e.sync();

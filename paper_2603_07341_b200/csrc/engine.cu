@@ -131,6 +131,53 @@ void Engine::set_model(const HostModel& m) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// K2: counting sort of the candidates by insertion gap, exact dedup + rank inside each gap segment, and the
+// scatter that writes the merged sorted table plus the next (sorted) frontier.  Expects gap[] (n+2 counters)
+// filled by the expansion kernel; the new frontier ends up in frontier[fcur] (fcur is flipped).
+// ------------------------------------------------------------------------------------------------
+uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc, int& fcur) {
+    const int W = md.W;
+    Ctl* c = dctl();
+    // counting sort by insertion gap: gap[] (counts) -> segment starts; row_len[] is the per-gap cursor
+    // during placement and then the per-gap survivor count
+    exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
+    perm.ensure(size_t(nc) * 4);
+    seg_rank.ensure(size_t(nc) * 4);
+    row_len.ensure((size_t(n) + 2) * 4);
+    PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
+    place_candidates_kernel<<<grid_for(nc), NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc, gap.as<uint32_t>(),
+                                                              row_len.as<uint32_t>(), perm.as<uint32_t>());
+    check_launch();
+    PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
+    PB_DISPATCH_W(W, segment_dedup_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+                         gap.as<uint32_t>(), seg_rank.as<uint32_t>(), row_len.as<uint32_t>(), &c->grow));
+    check_launch();
+    PB_DISPATCH_W(W, segment_rank_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+                         gap.as<uint32_t>(), seg_rank.as<uint32_t>()));
+    check_launch();
+    // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
+    exclusive_scan(row_len.as<uint32_t>(), uint64_t(n) + 2);
+    const uint32_t n_new = read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
+    const uint64_t n_next64 = uint64_t(n) + n_new;
+    if (n_next64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+    tab_tmp.ensure(size_t(n_next64) * W * 4);
+    frontier[fcur ^ 1].ensure(size_t(n_new) * 4 + 4);
+    PB_DISPATCH_W(W, merge_old_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
+                         out.words.as<uint32_t>(), n, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>()));
+    check_launch();
+    PB_DISPATCH_W(W, merge_new_rows_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
+                         seg_rank.as<uint32_t>(), nc, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>(),
+                         frontier[fcur ^ 1].as<uint32_t>()));
+    check_launch();
+    out.words.swap(tab_tmp);
+    fcur ^= 1;
+    return n_new;
+}
+
+// ------------------------------------------------------------------------------------------------
 // grow_subspace (subspace.hpp:195-249)
 // ------------------------------------------------------------------------------------------------
 void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
@@ -179,44 +226,9 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
             require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
             break;
         }
-        // counting sort by insertion gap: gap[] (counts) -> segment starts; row_len[] is the per-gap cursor
-        // during placement and then the per-gap survivor count
-        exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
-        perm.ensure(size_t(nc) * 4);
-        seg_rank.ensure(size_t(nc) * 4);
-        row_len.ensure((size_t(n) + 2) * 4);
-        PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
-        place_candidates_kernel<<<grid_for(nc), NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc, gap.as<uint32_t>(),
-                                                                  row_len.as<uint32_t>(), perm.as<uint32_t>());
-        check_launch();
-        PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
-        PB_DISPATCH_W(W, segment_dedup_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
-                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
-                             gap.as<uint32_t>(), seg_rank.as<uint32_t>(), row_len.as<uint32_t>(), &c->grow));
-        check_launch();
-        PB_DISPATCH_W(W, segment_rank_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
-                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
-                             gap.as<uint32_t>(), seg_rank.as<uint32_t>()));
-        check_launch();
-        // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
-        exclusive_scan(row_len.as<uint32_t>(), uint64_t(n) + 2);
-        const uint32_t n_new = read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
-        const uint64_t n_next64 = uint64_t(n) + n_new;
-        if (n_next64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
-        tab_tmp.ensure(size_t(n_next64) * W * 4);
-        frontier[fcur ^ 1].ensure(size_t(n_new) * 4 + 4);
-        PB_DISPATCH_W(W, merge_old_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
-                             out.words.as<uint32_t>(), n, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>()));
-        check_launch();
-        PB_DISPATCH_W(W, merge_new_rows_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
-                             cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
-                             seg_rank.as<uint32_t>(), nc, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>(),
-                             frontier[fcur ^ 1].as<uint32_t>()));
-        check_launch();
-        out.words.swap(tab_tmp);
-        fcur ^= 1;
+        const uint32_t n_new = merge_level(out, n, nc, fcur);
         identity_frontier = false;
-        n = uint32_t(n_next64);
+        n += n_new;
         nf = n_new;
         require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
     }
@@ -291,7 +303,7 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         const int sg = std::min(g, sm_count * 2);
         for (int p = 0; p < 6; ++p) {
             select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
-                                                      hist.as<uint32_t>());
+                                                      hist.as<uint32_t>(), 1);
             check_launch();
         }
         sc = read_back<SelectCtl>(&c->select);
@@ -353,12 +365,20 @@ double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t n
     PB_DISPATCH_W(W, remap_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
                                                                partials.as<double>(), &c->ticket, c->out));
     check_launch();
-    return read_back<double>(c->out);
+    const double d = read_back<double>(c->out);
+    return world > 1 ? allreduce_host(d) : d;
 }
 
 // ------------------------------------------------------------------------------------------------
 void Engine::expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite) {
     Ctl* c = dctl();
+    if (world > 1) {
+        // the SpMV reads halo columns: stage x next to its halo
+        term[0].ensure((size_t(sp.n) + sp.halo_n) * 16 + 16);
+        PB_CUDA(cudaMemcpyAsync(term[0].p, x, size_t(sp.n) * 16, cudaMemcpyDeviceToDevice, stream));
+        halo_exchange(sp, term[0].as<double2>());
+        x = term[0].as<double2>();
+    }
     expectation_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                           sp.val.as<double>(), x, partials.as<double>(), &c->ticket,
                                                           c->out);
@@ -367,6 +387,7 @@ void Engine::expectation(const Space& sp, const double2* x, double* exp_out, dou
         double v[3];
     };
     R r = read_back<R>(c->out);
+    if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, r.v, 3), "allreduce_f64_host");
     if (exp_out) *exp_out = r.v[0];
     if (norm2_out) *norm2_out = r.v[1];
     if (check_finite && r.v[2] != 0.0) throw PacesError("expmv: non-finite input coefficient");
@@ -416,7 +437,7 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                 taylor_order_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                           sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
                                                           term[order & 1].as<double2>(), c_vec, b, order, rtol,
-                                                          partials.as<double>(), &c->taylor, 0);
+                                                          partials.as<double>(), &c->taylor, 0, nullptr);
                 check_launch();
             }
             tc = read_back<TaylorCtl>(&c->taylor);
@@ -468,9 +489,10 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
     const uint32_t rows_per_block = 4096;
     const uint32_t nb = (n + rows_per_block - 1) / rows_per_block;
     aux_vec.ensure((size_t(nb) * L + size_t(L) * 3 + 8) * 8);
-    double* block_part = aux_vec.as<double>();
-    double* d_out = block_part + size_t(nb) * L;     // L doubles
-    double2* d_found = reinterpret_cast<double2*>(d_out + L);  // L double2
+    // layout: [found: L double2 (16-byte aligned)] [out: L doubles] [per-CTA partials: nb * L doubles]
+    double2* d_found = aux_vec.as<double2>();
+    double* d_out = reinterpret_cast<double*>(d_found + L);
+    double* block_part = d_out + L;
     if (density) {
         PB_CUDA(cudaMemsetAsync(block_part, 0, size_t(nb) * L * 8, stream));
         if (nb) {
@@ -481,6 +503,7 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
         check_launch();
         PB_CUDA(cudaMemcpyAsync(density, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
         sync();
+        if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, density, uint64_t(L)), "allreduce_f64_host");
     }
     if (phonons) {
         if (md.kind != 1) throw PacesError("phonon numbers: not a Holstein model");
@@ -494,12 +517,18 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
         check_launch();
         PB_CUDA(cudaMemcpyAsync(phonons, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
         sync();
+        if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, phonons, uint64_t(L)), "allreduce_f64_host");
     }
     if (amp) {
         PB_DISPATCH_W(W, dipole_kernel<W><<<1, 256, 0, stream>>>(md, words, cvec, n, d_found, d_out));
         check_launch();
         PB_CUDA(cudaMemcpyAsync(amp, d_out, 16, cudaMemcpyDeviceToHost, stream));
         sync();
+        if (world > 1) {
+            // the L vacuum keys share one phonon configuration, hence one owner; the others contribute zeros,
+            // but the 1/sqrt(L) factor was applied per rank, which is exact for the single non-zero term
+            comm_check(ops.allreduce_f64_host(ops.user, amp, 2), "allreduce_f64_host");
+        }
     }
 }
 
@@ -534,20 +563,34 @@ void Engine::run_begin(const pb200_run_cfg& c) {
     std::vector<uint32_t> words;
     std::vector<cplx> amps;
     build_seed_state(hm, c.init_kind, c.init_site, c.n_entries, c.entry_occ, c.entry_amp, words, amps);
-    const uint32_t ns = uint32_t(amps.size());
     const int W = md.W;
-    aux_words.ensure(words.size() * 4);
-    aux_coeff.ensure(amps.size() * 16);
+    if (world > 1) {
+        // every rank builds the same normalised seed list and keeps the keys it owns
+        std::vector<uint32_t> w2;
+        std::vector<cplx> a2;
+        for (size_t k = 0; k < amps.size(); ++k)
+            if (host_owner(hm, words.data() + k * W, uint32_t(world)) == uint32_t(rank)) {
+                w2.insert(w2.end(), words.begin() + k * W, words.begin() + (k + 1) * W);
+                a2.push_back(amps[k]);
+            }
+        words.swap(w2);
+        amps.swap(a2);
+    }
+    const uint32_t ns = uint32_t(amps.size());
+    aux_words.ensure(words.size() * 4 + 16);
+    aux_coeff.ensure(amps.size() * 16 + 16);
     PB_CUDA(cudaMemcpyAsync(aux_words.p, words.data(), words.size() * 4, cudaMemcpyHostToDevice, stream));
     PB_CUDA(cudaMemcpyAsync(aux_coeff.p, amps.data(), amps.size() * 16, cudaMemcpyHostToDevice, stream));
     sync();
     Space& sp = space[cur];
-    grow(aux_words.as<uint32_t>(), ns, c.m_init, sp);
+    if (world > 1)
+        grow_sharded(aux_words.as<uint32_t>(), ns, c.m_init, sp);
+    else
+        grow(aux_words.as<uint32_t>(), ns, c.m_init, sp);
     coeff[ccur].ensure(size_t(sp.n) * 16 + 16);
     const double discarded = remap(aux_words.as<uint32_t>(), aux_coeff.as<double2>(), ns, sp.words.as<uint32_t>(),
                                    sp.n, coeff[ccur].as<double2>());
     if (discarded != 0) throw PacesError("initialize: seed keys lost during growth");
-    (void)W;
     t = 0;
     steps_done = 0;
     last_order = 0;
@@ -571,14 +614,17 @@ void Engine::run_step(pb200_diag* out) {
         PB_CUDA(cudaEventRecord(ev[5], stream));
         rec.norm_pre = std::sqrt(n2);
         rec.norm_post = rec.norm_pre;
-        rec.q_true = old.n;
+        rec.q_true = world > 1 ? old.n_global : old.n;
         rec.energy = e;
         coeff[ccur ^ 1].ensure(size_t(old.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
         PB_CUDA(cudaMemcpyAsync(psi, c_old, size_t(old.n) * 16, cudaMemcpyDeviceToDevice, stream));
         int order = 0;
         double ltn = 0, lcn = 0;
-        expmv(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        if (world > 1)
+            expmv_sharded(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        else
+            expmv(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         PB_CUDA(cudaEventRecord(ev[6], stream));
         sync();
         rec.taylor_order = order;
@@ -596,14 +642,19 @@ void Engine::run_step(pb200_diag* out) {
         // engine.hpp:268-291
         Space& next = space[cur ^ 1];
         double n2_pre = 0;
-        const uint32_t kept = select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, pb200_mix_seed(cfg.seed + s),
-                                     &n2_pre);
+        const uint64_t sel_seed = pb200_mix_seed(cfg.seed + s);
+        const uint32_t kept = world > 1
+                                  ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
+                                  : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre);
         rec.norm_pre = std::sqrt(n2_pre);
         PB_CUDA(cudaEventRecord(ev[1], stream));
         // grow() = expansion + assembly; split the timer inside via ev[2]
-        grow(seeds.as<uint32_t>(), kept, cfg.m, next);
+        if (world > 1)
+            grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
+        else
+            grow(seeds.as<uint32_t>(), kept, cfg.m, next);
         PB_CUDA(cudaEventRecord(ev[3], stream));
-        require_memory(uint64_t(next.n) * 16 * 4, "state vectors");
+        require_memory((world > 1 ? next.n_global : uint64_t(next.n)) * 16 * 4, "state vectors");
         coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
         rec.discarded_weight =
@@ -613,11 +664,14 @@ void Engine::run_step(pb200_diag* out) {
         expectation(next, psi, &e, &n2, true);
         PB_CUDA(cudaEventRecord(ev[5], stream));
         rec.norm_post = std::sqrt(n2);
-        rec.q_true = next.n;
+        rec.q_true = world > 1 ? next.n_global : next.n;
         rec.energy = e;
         int order = 0;
         double ltn = 0, lcn = 0;
-        expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        if (world > 1)
+            expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        else
+            expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         PB_CUDA(cudaEventRecord(ev[6], stream));
         sync();
         rec.taylor_order = order;

@@ -13,6 +13,7 @@
 #include "../../include/paces_b200.h"
 #include "host_model.hpp"
 #include "kernels.cuh"
+#include "sharded.cuh"
 
 namespace pb {
 
@@ -80,6 +81,14 @@ struct DevBuf {
         }
         cap = want;
     }
+    /// Grows while preserving the first keep_bytes bytes.
+    void ensure_keep(size_t bytes, size_t keep_bytes) {
+        if (bytes <= cap) return;
+        DevBuf bigger;
+        bigger.ensure(bytes);
+        if (p && keep_bytes) cudaMemcpy(bigger.p, p, keep_bytes, cudaMemcpyDeviceToDevice);
+        swap(bigger);
+    }
     void swap(DevBuf& o) {
         std::swap(p, o.p);
         std::swap(cap, o.cap);
@@ -101,6 +110,12 @@ struct Space {
     uint64_t q_nom = 0;
     int order = 0;
     bool has_h = false;
+    // sharded runs: columns >= n index the halo (values received from other ranks every SpMV)
+    uint32_t halo_n = 0;
+    uint32_t send_total = 0;
+    DevBuf send_idx;                          // local rows to pack, grouped by destination rank
+    std::vector<uint64_t> halo_send, halo_recv;  // per-peer element counts
+    uint64_t n_global = 0, nnz_global = 0;
 };
 
 struct Engine {
@@ -144,8 +159,39 @@ struct Engine {
     void* pinned = nullptr;  // 4 KiB pinned host scratch for read-backs
     cudaEvent_t ev[10]{};
 
+    // multi-GPU (one context per rank); world == 1 is the single-GPU path
+    int rank = 0, world = 1;
+    pb200_comm_ops ops{};
+    DevBuf out_keys, out_dest, route_pos, route_ctr, sendbuf, recvbuf, req_keys, req_dest, req_pos, reply, answer,
+        found, halo_flag, tmp_cnt, halo_stage, sel_keys;
+    std::vector<uint64_t> h_send, h_recv;
+
     explicit Engine(int dev);
     ~Engine();
+
+    // ---- collectives (thin wrappers over ops with error translation)
+    void comm_check(int rc, const char* what) const {
+        if (rc != 0) throw CudaFail(std::string("collective failed: ") + what);
+    }
+    double allreduce_host(double v) {
+        comm_check(ops.allreduce_f64_host(ops.user, &v, 1), "allreduce_f64_host");
+        return v;
+    }
+    uint64_t allreduce_host_u64(uint64_t v) {
+        comm_check(ops.allreduce_u64_host(ops.user, &v, 1), "allreduce_u64_host");
+        return v;
+    }
+    /// dest[] -> bucketed positions; returns per-destination counts in h_send
+    void route(const uint32_t* dest, uint32_t cnt, uint32_t* pos);
+    /// exchanges h_send -> h_recv and the bucketed device buffer; returns total received elements
+    uint64_t exchange(const void* send, void* recv_buf_owner, DevBuf& recv, uint64_t elem_bytes);
+    void halo_exchange(const Space& sp, double2* x);
+    void grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out);
+    void assemble_sharded(Space& sp);
+    uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
+                            double* norm2_out);
+    void expmv_sharded(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps,
+                       int* order_used, double* last_term_norm, double* last_c_norm);
 
     // ---- helpers
     int grid_for(uint64_t n) const {
@@ -202,6 +248,8 @@ struct Engine {
 
     // ---- operators on device data
     void grow(const uint32_t* d_seeds, uint32_t n_seeds_, int order, Space& out);
+    /// dedup + merge of the nc candidates of one BFS order into out.words (n rows); returns the number of new keys
+    uint32_t merge_level(Space& out, uint32_t n, uint32_t nc, int& fcur);
     void assemble(Space& sp);
     /// returns kept count; result in this->seeds
     uint32_t select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,

@@ -166,6 +166,20 @@ inline bool host_row_less(const uint32_t* a, const uint32_t* b, uint32_t w) {
     return false;
 }
 
+/// Shard owner: identical arithmetic to owner_of() in keys.cuh (hash of the key with the exciton register zeroed).
+inline uint32_t host_owner(const HostModel& m, const uint32_t* key, uint32_t P) {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (uint32_t i = 0; i < m.W; ++i) {
+        uint32_t w = key[i];
+        if (i == 0 && m.b0 > 0) w = (m.b0 >= 32) ? 0u : (w & (0xffffffffu >> m.b0));
+        h = (h ^ w) * 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+    }
+    h *= 0x94D049BB133111EBull;
+    h ^= h >> 32;
+    return uint32_t(h % P);
+}
+
 /// Strictly ascending rows (PackedBasisTable::sorted).
 inline bool host_rows_sorted(const uint32_t* words, uint64_t rows, uint32_t w) {
     for (uint64_t i = 1; i < rows; ++i)

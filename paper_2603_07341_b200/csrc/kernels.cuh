@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint
                                                           double2* __restrict__ term_out, double2* __restrict__ c,
                                                           double b, int order, double rtol,
                                                           double* __restrict__ partials, TaylorCtl* ctl,
-                                                          int ignore_stop) {
+                                                          int ignore_stop, double* __restrict__ tot_out) {
     __shared__ double smem[NT / 32];
     if (!ignore_stop && *(volatile int*)&ctl->done) return;
     double acc[2] = {0.0, 0.0};
@@ -279,6 +279,11 @@ __global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint
     }
     double tot[2];
     if (grid_sum<2>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+        if (tot_out) {  // sharded: the sums are all-reduced first, taylor_stop_kernel applies the rule
+            tot_out[0] = tot[0];
+            tot_out[1] = tot[1];
+            return;
+        }
         const double tn = __dsqrt_rn(tot[0]), rn = __dsqrt_rn(tot[1]);
         if (order > ctl->order_used) ctl->order_used = order;
         ctl->last_order = order;
@@ -384,7 +389,7 @@ constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 
 __global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restrict__ w, uint32_t n, int shift, int width,
-                                                         SelectCtl* ctl, uint32_t* __restrict__ hist) {
+                                                         SelectCtl* ctl, uint32_t* __restrict__ hist, int fuse_pick) {
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ uint32_t wsum[NT / 32];
     __shared__ bool is_last;
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restric
         const uint32_t v = sh[i];
         if (v) atomicAdd(hist + i, v);
     }
+    if (!fuse_pick) return;  // sharded: the histogram is all-reduced, then select_pick_global_kernel
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) is_last = (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1);

@@ -121,6 +121,20 @@ __device__ __forceinline__ bool find_row(const uint32_t* __restrict__ table, uin
     return find_row_in<W>(table, 0, n, k, pos);
 }
 
+/// 64-bit mix of a key (splitmix-style), used for shard ownership.
+template <int W>
+__host__ __device__ __forceinline__ uint64_t key_hash_words(const uint32_t* w) {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        h = (h ^ w[i]) * 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+    }
+    h *= 0x94D049BB133111EBull;
+    h ^= h >> 32;
+    return h;
+}
+
 /// b-bit field at bit offset off (get_site, basis_codec.hpp:90-108).  b in [0, 32].
 template <int W>
 __device__ __forceinline__ uint32_t get_bits(const Key<W>& k, int off, int b) {
@@ -163,6 +177,16 @@ __device__ __forceinline__ uint32_t exciton_site(const ModelDev& m, const Key<W>
 template <int W>
 __device__ __forceinline__ uint32_t phonon_occ(const ModelDev& m, const Key<W>& k, int j) {
     return get_bits<W>(k, m.b0 + j * m.bp, m.bp);
+}
+
+/// Shard owner of a key: hash of its PHONON part (exciton register masked to zero) mod P.  Hop neighbours
+/// keep the phonon configuration, so they live on the same rank; only ladder neighbours travel
+/// (halo 0.5-0.9 columns per row instead of 1.8-2.2 with a whole-key hash).
+template <int W>
+__device__ __forceinline__ uint32_t owner_of(const ModelDev& m, const Key<W>& k, uint32_t P) {
+    Key<W> z = k;
+    if (m.b0 > 0) z.w[0] = (m.b0 >= 32) ? 0u : (z.w[0] & (0xffffffffu >> m.b0));
+    return uint32_t(key_hash_words<W>(z.w) % P);
 }
 
 /// Diagonal element: eps[e] first, then omega[j]*n_j for ascending j, separate multiply and add

@@ -1,0 +1,459 @@
+// sharded.cu -- multi-GPU orchestration: one context per rank, rows sharded by owner_of(key).
+// Every method here is COLLECTIVE: all ranks call it in the same order.  Data-path exchanges:
+//   expansion   : candidate keys owned elsewhere            (all-to-all-v of keys, once per BFS order)
+//   assembly    : neighbour key -> owner-local row look-ups (all-to-all-v of keys, all-to-all-v of u32 replies)
+//   Taylor order: complex128 halo values                    (all-to-all-v, once per order) + 2-double all-reduce
+//   selection   : 2048-bin histogram all-reduce per radix pass; tie keys gathered and drawn identically everywhere
+// Row sums keep the reference's order (entries sorted by neighbour key), so amplitudes do not depend on P.
+#include "engine.cuh"
+
+namespace pb {
+
+#define PB_DISPATCH_WS(Wv, ...)                                 \
+    switch (Wv) {                                               \
+        case 1: { constexpr int W = 1; __VA_ARGS__; } break;    \
+        case 2: { constexpr int W = 2; __VA_ARGS__; } break;    \
+        case 3: { constexpr int W = 3; __VA_ARGS__; } break;    \
+        case 4: { constexpr int W = 4; __VA_ARGS__; } break;    \
+        case 5: { constexpr int W = 5; __VA_ARGS__; } break;    \
+        case 6: { constexpr int W = 6; __VA_ARGS__; } break;    \
+        case 7: { constexpr int W = 7; __VA_ARGS__; } break;    \
+        case 8: { constexpr int W = 8; __VA_ARGS__; } break;    \
+        case 9: { constexpr int W = 9; __VA_ARGS__; } break;    \
+        case 10: { constexpr int W = 10; __VA_ARGS__; } break;  \
+        case 11: { constexpr int W = 11; __VA_ARGS__; } break;  \
+        case 12: { constexpr int W = 12; __VA_ARGS__; } break;  \
+        case 13: { constexpr int W = 13; __VA_ARGS__; } break;  \
+        case 14: { constexpr int W = 14; __VA_ARGS__; } break;  \
+        case 15: { constexpr int W = 15; __VA_ARGS__; } break;  \
+        case 16: { constexpr int W = 16; __VA_ARGS__; } break;  \
+        default: throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build"); \
+    }
+
+// ------------------------------------------------------------------------------------------------
+// routing helpers
+// ------------------------------------------------------------------------------------------------
+void Engine::route(const uint32_t* dest, uint32_t cnt, uint32_t* pos) {
+    const uint32_t P = uint32_t(world);
+    route_ctr.ensure(3 * 64 * 4);
+    uint32_t* counts = route_ctr.as<uint32_t>();
+    uint32_t* displ = counts + 64;
+    uint32_t* fill = counts + 128;
+    PB_CUDA(cudaMemsetAsync(counts, 0, 3 * 64 * 4, stream));
+    route_count_kernel<<<grid_for(cnt), NT, 0, stream>>>(dest, cnt, P, counts);
+    check_launch();
+    PB_CUDA(cudaMemcpyAsync(pinned, counts, P * 4, cudaMemcpyDeviceToHost, stream));
+    sync();
+    h_send.assign(P, 0);
+    uint32_t hd[64];
+    uint32_t acc = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+        h_send[p] = static_cast<uint32_t*>(pinned)[p];
+        hd[p] = acc;
+        acc += uint32_t(h_send[p]);
+    }
+    std::memcpy(pinned, hd, P * 4);
+    PB_CUDA(cudaMemcpyAsync(displ, pinned, P * 4, cudaMemcpyHostToDevice, stream));
+    route_place_kernel<<<grid_for(cnt), NT, 0, stream>>>(dest, cnt, displ, fill, pos);
+    check_launch();
+    sync();  // pinned is reused by the next read-back
+}
+
+uint64_t Engine::exchange(const void* send, void*, DevBuf& recv, uint64_t elem_bytes) {
+    const uint32_t P = uint32_t(world);
+    h_recv.assign(P, 0);
+    comm_check(ops.alltoall_u64_host(ops.user, h_send.data(), h_recv.data()), "alltoall_u64_host");
+    uint64_t total = 0;
+    for (uint32_t p = 0; p < P; ++p) total += h_recv[p];
+    recv.ensure(total * elem_bytes + 16);
+    comm_check(ops.alltoallv_dev(ops.user, send, h_send.data(), recv.p, h_recv.data(), elem_bytes, stream),
+               "alltoallv_dev");
+    return total;
+}
+
+void Engine::halo_exchange(const Space& sp, double2* x) {
+    halo_stage.ensure(size_t(sp.send_total) * 16 + 16);
+    if (sp.send_total) {
+        halo_pack_kernel<<<grid_for(sp.send_total), NT, 0, stream>>>(x, sp.send_idx.as<uint32_t>(), sp.send_total,
+                                                                     halo_stage.as<double2>());
+        check_launch();
+    }
+    comm_check(ops.alltoallv_dev(ops.user, halo_stage.p, sp.halo_send.data(), x + sp.n, sp.halo_recv.data(), 16, stream),
+               "alltoallv_dev(halo)");
+}
+
+// ------------------------------------------------------------------------------------------------
+// grow_subspace on shards
+// ------------------------------------------------------------------------------------------------
+void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
+    require_model();
+    if (order < 0) throw PacesError("grow_subspace: neighbor order must be >= 0");
+    const uint64_t ns_global = allreduce_host_u64(ns);
+    if (ns_global == 0) throw PacesError("grow_subspace: empty seed set");
+    const int W = md.W;
+    const uint32_t P = uint32_t(world);
+    const int nmoves = md.max_deg + (md.kind == 1 ? 2 : 0);
+    out.words.ensure(size_t(ns) * W * 4 + 4);
+    if (ns) PB_CUDA(cudaMemcpyAsync(out.words.p, d_seeds, size_t(ns) * W * 4, cudaMemcpyDeviceToDevice, stream));
+    uint32_t n = ns, nf = ns;
+    bool identity_frontier = true;
+    int fcur = 0;
+    Ctl* c = dctl();
+    route_ctr.ensure(3 * 64 * 4 + sizeof(ShardCounters));
+    ShardCounters* dsc = reinterpret_cast<ShardCounters*>(route_ctr.as<uint32_t>() + 3 * 64);
+
+    for (int k = 0; k < order; ++k) {
+        if (allreduce_host_u64(nf) == 0) break;  // every frontier is empty: the ball is complete
+        const uint64_t cap64 = uint64_t(nf) * uint64_t(nmoves) + 1;
+        if (cap64 > 0x7ffffff0ull) throw PacesError("subspace growth: candidate count exceeds 32-bit indexing");
+        const uint32_t cap = uint32_t(cap64);
+        cand_keys.ensure(size_t(cap) * W * 4);
+        cand_gap.ensure(size_t(cap) * 4);
+        out_keys.ensure(size_t(cap) * W * 4);
+        out_dest.ensure(size_t(cap) * 4);
+        route_pos.ensure(size_t(cap) * 4);
+        gap.ensure((size_t(n) + 2) * 4);
+        PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
+        PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
+        PB_CUDA(cudaMemsetAsync(dsc, 0, sizeof(ShardCounters), stream));
+        const uint32_t* fr = identity_frontier ? nullptr : frontier[fcur].as<uint32_t>();
+        const uint32_t xchunk = chunk_for(nf);
+        if (nf) {
+            PB_DISPATCH_WS(W, expand_level_sharded_kernel<W><<<grid_chunked(nf, xchunk), NT, 0, stream>>>(
+                                  md, uint32_t(rank), P, out.words.as<uint32_t>(), n, fr, nf, xchunk,
+                                  cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cap, gap.as<uint32_t>(), &c->grow,
+                                  out_keys.as<uint32_t>(), out_dest.as<uint32_t>(), cap, dsc));
+            check_launch();
+        }
+        const ShardCounters hsc = read_back<ShardCounters>(dsc);
+        GrowCounters gc = read_back<GrowCounters>(&c->grow);
+        if (gc.overflow || hsc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
+        // ship the keys owned by other ranks
+        route(out_dest.as<uint32_t>(), hsc.n_out, route_pos.as<uint32_t>());
+        sendbuf.ensure(size_t(hsc.n_out) * W * 4 + 16);
+        if (hsc.n_out) {
+            PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(hsc.n_out), NT, 0, stream>>>(
+                                  out_keys.as<uint32_t>(), route_pos.as<uint32_t>(), hsc.n_out, sendbuf.as<uint32_t>()));
+            check_launch();
+        }
+        const uint64_t nr = exchange(sendbuf.p, nullptr, recvbuf, uint64_t(W) * 4);
+        if (nr) {
+            const uint64_t need = uint64_t(gc.n_cand) + nr;
+            if (need > 0x7ffffff0ull) throw PacesError("subspace growth: candidate count exceeds 32-bit indexing");
+            sync();
+            cand_keys.ensure_keep(size_t(need) * W * 4, size_t(gc.n_cand) * W * 4);
+            cand_gap.ensure_keep(size_t(need) * 4, size_t(gc.n_cand) * 4);
+            PB_DISPATCH_WS(W, classify_received_kernel<W><<<grid_for(nr), NT, 0, stream>>>(
+                                  out.words.as<uint32_t>(), n, recvbuf.as<uint32_t>(), uint32_t(nr),
+                                  cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), uint32_t(need), gap.as<uint32_t>(),
+                                  &c->grow));
+            check_launch();
+            gc = read_back<GrowCounters>(&c->grow);
+            if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow while classifying received keys");
+        }
+        const uint32_t nc = gc.n_cand;
+        uint32_t n_new = 0;
+        if (nc) n_new = merge_level(out, n, nc, fcur);
+        identity_frontier = false;
+        if (!nc) {
+            // nothing new on this rank: the next frontier is empty, the table is unchanged
+            frontier[fcur].ensure(4);
+        }
+        n += n_new;
+        nf = n_new;
+    }
+    out.n = n;
+    out.q_nom = ns_global;
+    out.order = order;
+    PB_CUDA(cudaEventRecord(ev[2], stream));
+    assemble_sharded(out);
+}
+
+// ------------------------------------------------------------------------------------------------
+// row-wise assembly on shards + halo plan
+// ------------------------------------------------------------------------------------------------
+void Engine::assemble_sharded(Space& sp) {
+    const int W = md.W;
+    const uint32_t P = uint32_t(world);
+    const uint32_t n = sp.n;
+    const int width = row_width;
+    Ctl* c = dctl();
+    tmp_col.ensure(size_t(n) * width * 4 + 4);
+    tmp_val.ensure(size_t(n) * width * 8 + 8);
+    tmp_cnt.ensure(size_t(n) * 4 + 4);
+    sp.row_ptr.ensure((size_t(n) + 1) * 4);
+    const uint64_t req_cap64 = uint64_t(n) * uint64_t(width) + 1;
+    if (req_cap64 > 0x7ffffff0ull) throw PacesError("assembly: request count exceeds 31-bit indexing");
+    const uint32_t req_cap = uint32_t(req_cap64);
+    req_keys.ensure(size_t(req_cap) * W * 4);
+    req_dest.ensure(size_t(req_cap) * 4);
+    req_pos.ensure(size_t(req_cap) * 4);
+    route_ctr.ensure(3 * 64 * 4 + sizeof(ShardCounters));
+    ShardCounters* dsc = reinterpret_cast<ShardCounters*>(route_ctr.as<uint32_t>() + 3 * 64);
+    PB_CUDA(cudaMemsetAsync(dsc, 0, sizeof(ShardCounters), stream));
+    const uint32_t achunk = chunk_for(n);
+    if (n) {
+        PB_DISPATCH_WS(W, assemble_rows_sharded_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
+                              md, uint32_t(rank), P, sp.words.as<uint32_t>(), n, achunk, width, tmp_col.as<uint32_t>(),
+                              tmp_val.as<double>(), tmp_cnt.as<uint32_t>(), req_keys.as<uint32_t>(),
+                              req_dest.as<uint32_t>(), req_cap, dsc));
+        check_launch();
+    }
+    const ShardCounters hsc = read_back<ShardCounters>(dsc);
+    if (hsc.overflow) throw CudaFail("internal error: request buffer overflow during assembly");
+    const uint32_t nreq = hsc.n_req;
+
+    // requests -> owners
+    route(req_dest.as<uint32_t>(), nreq, req_pos.as<uint32_t>());
+    const std::vector<uint64_t> req_send = h_send;  // requests I send per peer
+    sendbuf.ensure(size_t(nreq) * W * 4 + 16);
+    if (nreq) {
+        PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(nreq), NT, 0, stream>>>(
+                              req_keys.as<uint32_t>(), req_pos.as<uint32_t>(), nreq, sendbuf.as<uint32_t>()));
+        check_launch();
+    }
+    const uint64_t nr = exchange(sendbuf.p, nullptr, recvbuf, uint64_t(W) * 4);
+    const std::vector<uint64_t> req_recv = h_recv;  // requests I answer per peer
+
+    // owner side: answers + the list of local rows to pack for every later SpMV
+    answer.ensure(size_t(nr) * 4 + 4);
+    found.ensure((size_t(nr) + 1) * 4);
+    PB_DISPATCH_WS(W, answer_requests_kernel<W><<<grid_for(nr), NT, 0, stream>>>(
+                          sp.words.as<uint32_t>(), n, recvbuf.as<uint32_t>(), uint32_t(nr), answer.as<uint32_t>(),
+                          found.as<uint32_t>()));
+    check_launch();
+    exclusive_scan(found.as<uint32_t>(), nr + 1);
+    // per-requester found counts = differences of the scan at the bucket boundaries
+    sp.halo_send.assign(P, 0);
+    {
+        uint64_t off = 0;
+        uint32_t* pin = static_cast<uint32_t*>(pinned);
+        for (uint32_t p = 0; p <= P; ++p) {
+            PB_CUDA(cudaMemcpyAsync(pin + p, found.as<uint32_t>() + off, 4, cudaMemcpyDeviceToHost, stream));
+            if (p < P) off += req_recv[p];
+        }
+        sync();
+        for (uint32_t p = 0; p < P; ++p) sp.halo_send[p] = pin[p + 1] - pin[p];
+        sp.send_total = pin[P];
+    }
+    sp.send_idx.ensure(size_t(sp.send_total) * 4 + 4);
+    build_send_list_kernel<<<grid_for(nr), NT, 0, stream>>>(answer.as<uint32_t>(), found.as<uint32_t>(), uint32_t(nr),
+                                                            sp.send_idx.as<uint32_t>());
+    check_launch();
+
+    // replies -> requesters (same buckets, reversed roles)
+    h_send = req_recv;
+    const uint64_t nrep = exchange(answer.p, nullptr, reply, 4);
+    if (nrep != nreq) throw CudaFail("internal error: look-up replies do not match the requests");
+    halo_flag.ensure((size_t(nreq) + 1) * 4);
+    reply_flags_kernel<<<grid_for(nreq), NT, 0, stream>>>(reply.as<uint32_t>(), nreq, halo_flag.as<uint32_t>());
+    check_launch();
+    exclusive_scan(halo_flag.as<uint32_t>(), uint64_t(nreq) + 1);
+    sp.halo_recv.assign(P, 0);
+    {
+        uint64_t off = 0;
+        uint32_t* pin = static_cast<uint32_t*>(pinned);
+        for (uint32_t p = 0; p <= P; ++p) {
+            PB_CUDA(cudaMemcpyAsync(pin + p, halo_flag.as<uint32_t>() + off, 4, cudaMemcpyDeviceToHost, stream));
+            if (p < P) off += req_send[p];
+        }
+        sync();
+        for (uint32_t p = 0; p < P; ++p) sp.halo_recv[p] = pin[p + 1] - pin[p];
+        sp.halo_n = pin[P];
+    }
+    if (uint64_t(n) + sp.halo_n > 0x7fffffffull) throw PacesError("assembly: local rows + halo exceed int32 columns");
+    resolve_requests_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_cnt.as<uint32_t>(),
+                                                            req_pos.as<uint32_t>(), reply.as<uint32_t>(),
+                                                            halo_flag.as<uint32_t>(), sp.row_ptr.as<uint32_t>());
+    check_launch();
+    PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
+    exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
+    const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
+    sp.col.ensure(size_t(nnz) * 4 + 4);
+    sp.val.ensure(size_t(nnz) * 8 + 8);
+    assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
+                                                                    tmp_cnt.as<uint32_t>(), sp.row_ptr.as<uint32_t>(),
+                                                                    sp.col.as<int32_t>(), sp.val.as<double>());
+    check_launch();
+    sp.nnz = nnz;
+    sp.has_h = true;
+    uint64_t g[2] = {n, nnz};
+    comm_check(ops.allreduce_u64_host(ops.user, g, 2), "allreduce_u64_host");
+    sp.n_global = g[0];
+    sp.nnz_global = g[1];
+    require_memory(sp.nnz_global * 2 * 16, "matrix assembly buffer");
+    (void)c;
+}
+
+// ------------------------------------------------------------------------------------------------
+// truncate_select on shards: global k-th largest weight, ties drawn identically on every rank
+// ------------------------------------------------------------------------------------------------
+uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
+                                double* norm2_out) {
+    require_model();
+    if (q_nom < 1) throw PacesError("truncate_select: q_nom must be >= 1");
+    const int W = md.W;
+    const uint32_t P = uint32_t(world);
+    Ctl* c = dctl();
+    weights.ensure(size_t(n) * 8 + 8);
+    flag_keep.ensure((size_t(n) + 1) * 4);
+    PB_CUDA(cudaMemsetAsync(hist.p, 0, SEL_BINS * sizeof(uint32_t), stream));
+    const int g = grid_for(n);
+    SelectCtl init{};
+    init.k = q_nom;
+    std::memcpy(pinned, &init, sizeof(init));
+    PB_CUDA(cudaMemcpyAsync(&c->select, pinned, sizeof(SelectCtl), cudaMemcpyHostToDevice, stream));
+    weights_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select);
+    check_launch();
+    SelectCtl sc = read_back<SelectCtl>(&c->select);
+    const double norm2 = allreduce_host(sc.norm2);
+    const uint64_t support = allreduce_host_u64(sc.support);
+    if (norm2_out) *norm2_out = norm2;
+    if (support == 0) throw PacesError("truncate_select: state has no support");
+
+    uint32_t* keep = flag_keep.as<uint32_t>();
+    if (support <= q_nom) {
+        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
+        check_launch();
+    } else {
+        static const int shifts[6] = {53, 42, 31, 20, 9, 0};
+        static const int widths[6] = {11, 11, 11, 11, 11, 9};
+        const int sg = std::min(g, sm_count * 2);
+        for (int p = 0; p < 6; ++p) {
+            select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
+                                                      hist.as<uint32_t>(), 0);
+            check_launch();
+            comm_check(ops.allreduce_u32_dev(ops.user, hist.as<uint32_t>(), SEL_BINS, stream), "allreduce_u32_dev");
+            select_pick_global_kernel<<<1, NT, 0, stream>>>(hist.as<uint32_t>(), widths[p], &c->select);
+            check_launch();
+        }
+        sc = read_back<SelectCtl>(&c->select);  // identical on every rank: derived from all-reduced histograms
+        const uint64_t need = q_nom - sc.count_gt;
+        if (need >= sc.count_eq) {
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr);
+            check_launch();
+        } else {
+            // gather the tie KEYS of all ranks, order them canonically, draw exactly as engine.hpp:137-142
+            flag_tie.ensure((size_t(n) + 1) * 4);
+            pos_a.ensure((size_t(n) + 1) * 4);
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 0, keep,
+                                                      flag_tie.as<uint32_t>());
+            check_launch();
+            PB_CUDA(cudaMemcpyAsync(pos_a.p, flag_tie.p, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
+            exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+            const uint32_t nt_local = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
+            sel_keys.ensure(size_t(std::max<uint64_t>(nt_local, sc.count_eq)) * W * 4 + 16);
+            PB_DISPATCH_WS(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, flag_tie.as<uint32_t>(),
+                                                                          pos_a.as<uint32_t>(), n,
+                                                                          sel_keys.as<uint32_t>()));
+            check_launch();
+            std::vector<uint32_t> mine(size_t(nt_local) * W);
+            if (nt_local)
+                PB_CUDA(cudaMemcpyAsync(mine.data(), sel_keys.p, mine.size() * 4, cudaMemcpyDeviceToHost, stream));
+            sync();
+            // fixed-size all-gather: counts first, then keys padded to the largest contribution
+            std::vector<uint64_t> cnts(P, 0);
+            uint64_t my = nt_local;
+            comm_check(ops.allgather_host(ops.user, &my, 8, cnts.data()), "allgather_host");
+            uint64_t mx = 0;
+            for (uint64_t v : cnts) mx = std::max(mx, v);
+            std::vector<uint32_t> padded(size_t(mx) * W, 0), all(size_t(mx) * W * P, 0);
+            std::copy(mine.begin(), mine.end(), padded.begin());
+            if (mx) comm_check(ops.allgather_host(ops.user, padded.data(), mx * W * 4, all.data()), "allgather_host");
+            std::vector<std::vector<uint32_t>> ties;
+            for (uint32_t p = 0; p < P; ++p)
+                for (uint64_t j = 0; j < cnts[p]; ++j) {
+                    const uint32_t* k = all.data() + (size_t(p) * mx + j) * W;
+                    ties.emplace_back(k, k + W);
+                }
+            std::sort(ties.begin(), ties.end());  // vector<uint32_t> compares word-lexicographically = canonical order
+            std::mt19937_64 rng(seed);
+            for (size_t i = ties.size(); i > 1 && need < ties.size(); --i) {
+                const size_t j = size_t(rng() % i);
+                std::swap(ties[i - 1], ties[j]);
+            }
+            std::vector<uint32_t> chosen;
+            for (uint64_t i = 0; i < need; ++i) chosen.insert(chosen.end(), ties[i].begin(), ties[i].end());
+            sel_keys.ensure(chosen.size() * 4 + 16);
+            PB_CUDA(cudaMemcpyAsync(sel_keys.p, chosen.data(), chosen.size() * 4, cudaMemcpyHostToDevice, stream));
+            PB_DISPATCH_WS(W, mark_selected_kernel<W><<<grid_for(need), NT, 0, stream>>>(
+                                  md, uint32_t(rank), P, d_words, n, sel_keys.as<uint32_t>(), uint32_t(need), keep));
+            check_launch();
+            sync();
+        }
+    }
+    pos_a.ensure((size_t(n) + 1) * 4);
+    PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
+    exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+    const uint32_t kept = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
+    seeds.ensure(size_t(kept) * W * 4 + 4);
+    PB_DISPATCH_WS(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,
+                                                                  seeds.as<uint32_t>()));
+    check_launch();
+    n_seeds = kept;
+    return kept;
+}
+
+// ------------------------------------------------------------------------------------------------
+// expmv on shards: halo exchange before every SpMV, all-reduced norms before the stop rule
+// ------------------------------------------------------------------------------------------------
+void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
+                           int* order_used, double* last_term_norm, double* last_c_norm) {
+    if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
+    if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
+    if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
+    if (substeps < 1) throw PacesError("propagator: substeps must be >= 1");
+    const uint32_t n = sp.n;
+    Ctl* c = dctl();
+    const size_t ext = (size_t(n) + sp.halo_n) * 16 + 16;
+    term[0].ensure(ext);
+    term[1].ensure(ext);
+    const double dt_sub = dt / substeps;
+    const int g = grid_for(n);
+    TaylorCtl tc{};
+    PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
+    for (int s = 0; s < substeps; ++s) {
+        PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
+        if (s > 0) {
+            tc.done = 0;
+            tc.streak = 0;
+            tc.ticket = 0;
+            std::memcpy(pinned, &tc, sizeof(tc));
+            PB_CUDA(cudaMemcpyAsync(&c->taylor, pinned, sizeof(TaylorCtl), cudaMemcpyHostToDevice, stream));
+        }
+        int order = 1;
+        bool converged = false;
+        int batch = last_order > 2 ? last_order : 8;
+        while (order <= max_order) {
+            const int end = std::min(max_order, order + batch - 1);
+            for (; order <= end; ++order) {
+                const double b = -dt_sub / double(order);
+                halo_exchange(sp, term[(order - 1) & 1].as<double2>());
+                taylor_order_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                          sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
+                                                          term[order & 1].as<double2>(), c_vec, b, order, rtol,
+                                                          partials.as<double>(), &c->taylor, 0, c->out);
+                check_launch();
+                comm_check(ops.allreduce_f64_dev(ops.user, c->out, 2, stream), "allreduce_f64_dev");
+                taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
+                check_launch();
+            }
+            tc = read_back<TaylorCtl>(&c->taylor);
+            if (tc.done) {
+                converged = true;
+                break;
+            }
+            batch = 2;
+        }
+        times.taylor_orders += uint64_t(tc.last_order);
+        if (!converged)
+            throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
+                             "; reduce dt or increase substeps");
+    }
+    last_order = tc.order_used;
+    if (order_used) *order_used = tc.order_used;
+    if (last_term_norm) *last_term_norm = tc.last_term_norm;
+    if (last_c_norm) *last_c_norm = tc.last_c_norm;
+}
+
+}  // namespace pb

@@ -1,0 +1,315 @@
+// sharded.cuh -- kernels that exist only on the multi-GPU path: the table is sharded over P ranks by
+// owner_of(key) (hash of the phonon part of the key); every rank keeps ITS rows in canonical order and runs
+// the single-GPU kernels on them.  What is added here is the routing of keys that belong to another rank
+// (expansion candidates, assembly look-up requests), the halo pack for the SpMV, and the split of the
+// reductions whose global value needs an all-reduce.
+#pragma once
+#include "kernels.cuh"
+
+namespace pb {
+
+constexpr uint32_t COL_ABSENT = 0xffffffffu;
+constexpr uint32_t COL_REQ = 0x80000000u;  // tmp_col marker: (COL_REQ | request id), resolved after the exchange
+
+struct ShardCounters {
+    uint32_t n_out;     // keys routed to other ranks
+    uint32_t overflow;
+    uint32_t n_req;     // assembly look-up requests
+    uint32_t pad;
+};
+
+/// Expansion of one BFS order on a shard.  Neighbours owned by this rank take the local path of
+/// expand_level_kernel (look-up, candidate + gap when absent); the others are appended to the outgoing list
+/// with their destination rank.
+template <int W>
+__global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
+    ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n,
+    const uint32_t* __restrict__ frontier, uint32_t nf, uint32_t chunk, uint32_t* __restrict__ cand_keys,
+    uint32_t* __restrict__ cand_gap, uint32_t cand_cap, uint32_t* __restrict__ gap_count, GrowCounters* ctr,
+    uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_dest, uint32_t out_cap, ShardCounters* sc) {
+    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
+    MoveCursors cur;
+    cur.reset(0xffffffffu);
+    for (uint64_t f = wbase; f < min(uint64_t(nf), uint64_t(wbase + 32ull * chunk)); f += 32) {
+        const uint32_t row = frontier ? __ldg(frontier + f) : uint32_t(f);
+        const Key<W> k = load_key<W>(table + size_t(row) * W);
+        const uint32_t e = exciton_site<W>(m, k);
+        if (e != cur.site) cur.reset(e);
+        for_each_neighbor<W>(m, k, false, [&](int move, const Key<W>& kk, double, bool) {
+            const uint32_t dest = owner_of<W>(m, kk, P);
+            if (dest == rank) {
+                uint32_t pos;
+                if (!cursor_find<W>(table, n, cur, move, kk, pos)) {
+                    const uint32_t slot = append_slot(&ctr->n_cand);
+                    if (slot < cand_cap) {
+                        store_key<W>(cand_keys + size_t(slot) * W, kk);
+                        cand_gap[slot] = pos;
+                        atomicAdd(gap_count + pos, 1u);
+                    } else {
+                        ctr->overflow = 1;
+                    }
+                }
+            } else {
+                const uint32_t slot = append_slot(&sc->n_out);
+                if (slot < out_cap) {
+                    store_key<W>(out_keys + size_t(slot) * W, kk);
+                    out_dest[slot] = dest;
+                } else {
+                    sc->overflow = 1;
+                }
+            }
+        });
+    }
+}
+
+/// counts[dest[i]]++ (P is tiny: shared-memory histogram per CTA).
+__global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restrict__ dest, uint32_t cnt, uint32_t P,
+                                                         uint32_t* __restrict__ counts) {
+    __shared__ uint32_t sh[64];
+    if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) atomicAdd(&sh[dest[i]], 1u);
+    __syncthreads();
+    if (threadIdx.x < P && sh[threadIdx.x]) atomicAdd(counts + threadIdx.x, sh[threadIdx.x]);
+}
+
+/// pos[i] = displ[dest[i]] + arrival order inside the bucket; fill[] starts at zero.
+__global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restrict__ dest, uint32_t cnt,
+                                                         const uint32_t* __restrict__ displ,
+                                                         uint32_t* __restrict__ fill, uint32_t* __restrict__ pos) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) {
+        const uint32_t d = dest[i];
+        pos[i] = displ[d] + atomicAdd(fill + d, 1u);
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(NT) route_scatter_keys_kernel(const uint32_t* __restrict__ keys,
+                                                                const uint32_t* __restrict__ pos, uint32_t cnt,
+                                                                uint32_t* __restrict__ send) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT)
+        store_key<W>(send + size_t(pos[i]) * W, load_key<W>(keys + size_t(i) * W));
+}
+
+/// Keys received from other ranks during expansion: those absent from the local table become candidates.
+template <int W>
+__global__ void __launch_bounds__(NT) classify_received_kernel(const uint32_t* __restrict__ table, uint32_t n,
+                                                               const uint32_t* __restrict__ recv, uint32_t nr,
+                                                               uint32_t* __restrict__ cand_keys,
+                                                               uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
+                                                               uint32_t* __restrict__ gap_count, GrowCounters* ctr) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < nr; i += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(recv + size_t(i) * W);
+        uint32_t pos;
+        if (!find_row<W>(table, n, k, pos)) {
+            const uint32_t slot = append_slot(&ctr->n_cand);
+            if (slot < cand_cap) {
+                store_key<W>(cand_keys + size_t(slot) * W, k);
+                cand_gap[slot] = pos;
+                atomicAdd(gap_count + pos, 1u);
+            } else {
+                ctr->overflow = 1;
+            }
+        }
+    }
+}
+
+/// Assembly pass 1 on a shard: like assemble_rows_kernel, but a neighbour owned by another rank becomes a
+/// look-up request; its scratch column holds COL_REQ | request id until the replies arrive.  Entries stay
+/// in ascending NEIGHBOUR-KEY order (the reference's summation order), whatever their final column.
+template <int W>
+__global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
+    ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n, uint32_t chunk, int width,
+    uint32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, uint32_t* __restrict__ tmp_cnt,
+    uint32_t* __restrict__ req_keys, uint32_t* __restrict__ req_dest, uint32_t req_cap, ShardCounters* sc) {
+    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
+    MoveCursors cur;
+    cur.reset(0xffffffffu);
+    for (uint64_t ii = wbase; ii < min(uint64_t(n), uint64_t(wbase + 32ull * chunk)); ii += 32) {
+        const uint32_t i = uint32_t(ii);
+        const Key<W> k = load_key<W>(table + size_t(i) * W);
+        const uint32_t e = exciton_site<W>(m, k);
+        if (e != cur.site) cur.reset(e);
+        int len = 0;
+        uint32_t* tc = tmp_col + size_t(i) * width;
+        double* tv = tmp_val + size_t(i) * width;
+        for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
+            uint32_t pos = i;
+            bool keep = true;
+            if (!is_diag) {
+                const uint32_t dest = owner_of<W>(m, kk, P);
+                if (dest == rank) {
+                    keep = cursor_find<W>(table, n, cur, move, kk, pos);
+                } else {
+                    const uint32_t r = append_slot(&sc->n_req);
+                    if (r < req_cap) {
+                        store_key<W>(req_keys + size_t(r) * W, kk);
+                        req_dest[r] = dest;
+                    } else {
+                        sc->overflow = 1;
+                    }
+                    pos = COL_REQ | r;
+                }
+            }
+            if (keep) {
+                tc[len] = pos;
+                tv[len] = amp;
+                ++len;
+            }
+        });
+        tmp_cnt[i] = uint32_t(len);
+    }
+}
+
+/// Owner side of the look-up exchange: answer[j] = local row of the requested key or COL_ABSENT;
+/// found[j] = 1/0 (scanned afterwards to build the halo send list).
+template <int W>
+__global__ void __launch_bounds__(NT) answer_requests_kernel(const uint32_t* __restrict__ table, uint32_t n,
+                                                             const uint32_t* __restrict__ recv, uint32_t nr,
+                                                             uint32_t* __restrict__ answer,
+                                                             uint32_t* __restrict__ found) {
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < nr; j += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(recv + size_t(j) * W);
+        uint32_t pos;
+        const bool f = find_row<W>(table, n, k, pos);
+        answer[j] = f ? pos : COL_ABSENT;
+        found[j] = f ? 1u : 0u;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) found[nr] = 0;
+}
+
+/// send_idx[found_pos[j]] = answer[j] for found requests (order preserving).
+__global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __restrict__ answer,
+                                                             const uint32_t* __restrict__ found_pos, uint32_t nr,
+                                                             uint32_t* __restrict__ send_idx) {
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < nr; j += gridDim.x * NT)
+        if (answer[j] != COL_ABSENT) send_idx[found_pos[j]] = answer[j];
+}
+
+/// Requester side: reply[] is in send (bucketed) order.  flag[p] = reply found; scanned into halo slots.
+__global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* __restrict__ reply, uint32_t nreq,
+                                                         uint32_t* __restrict__ flag) {
+    for (uint32_t p = blockIdx.x * NT + threadIdx.x; p < nreq; p += gridDim.x * NT)
+        flag[p] = (reply[p] != COL_ABSENT) ? 1u : 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag[nreq] = 0;
+}
+
+/// Resolves the COL_REQ markers: found -> n_local + halo slot, absent -> COL_ABSENT; counts the surviving
+/// entries per row.
+__global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int width, uint32_t* __restrict__ tmp_col,
+                                                              const uint32_t* __restrict__ tmp_cnt,
+                                                              const uint32_t* __restrict__ req_pos,
+                                                              const uint32_t* __restrict__ reply,
+                                                              const uint32_t* __restrict__ halo_slot,
+                                                              uint32_t* __restrict__ row_len) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        uint32_t* tc = tmp_col + size_t(i) * width;
+        const uint32_t cnt = tmp_cnt[i];
+        uint32_t len = 0;
+        for (uint32_t s = 0; s < cnt; ++s) {
+            uint32_t c = tc[s];
+            if (c != COL_ABSENT && (c & COL_REQ)) {
+                const uint32_t p = req_pos[c & ~COL_REQ];
+                c = (reply[p] != COL_ABSENT) ? n + halo_slot[p] : COL_ABSENT;
+                tc[s] = c;
+            }
+            if (c != COL_ABSENT) ++len;
+        }
+        row_len[i] = len;
+    }
+}
+
+/// Pass 2 on a shard: compacts the scratch into CSR, skipping absent remote neighbours.
+__global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
+                                                                      const uint32_t* __restrict__ tmp_col,
+                                                                      const double* __restrict__ tmp_val,
+                                                                      const uint32_t* __restrict__ tmp_cnt,
+                                                                      const uint32_t* __restrict__ row_ptr,
+                                                                      int32_t* __restrict__ col,
+                                                                      double* __restrict__ val) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        uint32_t k = row_ptr[i];
+        const uint32_t* tc = tmp_col + size_t(i) * width;
+        const double* tv = tmp_val + size_t(i) * width;
+        const uint32_t cnt = tmp_cnt[i];
+        for (uint32_t s = 0; s < cnt; ++s) {
+            if (tc[s] != COL_ABSENT) {
+                col[k] = int32_t(tc[s]);
+                val[k] = tv[s];
+                ++k;
+            }
+        }
+    }
+}
+
+/// Halo pack: send[j] = x[send_idx[j]].
+__global__ void __launch_bounds__(NT) halo_pack_kernel(const double2* __restrict__ x,
+                                                       const uint32_t* __restrict__ send_idx, uint32_t cnt,
+                                                       double2* __restrict__ send) {
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < cnt; j += gridDim.x * NT) send[j] = x[send_idx[j]];
+}
+
+/// Stop rule of propagator.hpp:76-84 on globally reduced sums tot = (|term|^2, |c|^2).
+__global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restrict__ tot, int order, double rtol) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (ctl->done) return;
+    const double tn = __dsqrt_rn(tot[0]), rn = __dsqrt_rn(tot[1]);
+    if (order > ctl->order_used) ctl->order_used = order;
+    ctl->last_order = order;
+    ctl->last_term_norm = tn;
+    ctl->last_c_norm = rn;
+    const int streak = (tn <= __dmul_rn(rtol, rn)) ? ctl->streak + 1 : 0;
+    ctl->streak = streak;
+    if (streak >= 2) ctl->done = 1;
+}
+
+/// Marks the locally owned keys among the globally selected tie keys (truncate_select, engine.hpp:137-142).
+template <int W>
+__global__ void __launch_bounds__(NT) mark_selected_kernel(ModelDev m, uint32_t rank, uint32_t P,
+                                                           const uint32_t* __restrict__ table, uint32_t n,
+                                                           const uint32_t* __restrict__ sel, uint32_t ns,
+                                                           uint32_t* __restrict__ keep) {
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < ns; j += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(sel + size_t(j) * W);
+        if (owner_of<W>(m, k, P) != rank) continue;
+        uint32_t pos;
+        if (find_row<W>(table, n, k, pos)) keep[pos] = 1u;
+    }
+}
+
+/// Gathers the keys of flagged rows (order preserving): out[pos[i]] = table[i].  (= compact_rows_kernel)
+
+/// Pick step of the radix select on an ALL-REDUCED histogram (one CTA); see select_pass_kernel.
+__global__ void __launch_bounds__(NT) select_pick_global_kernel(uint32_t* __restrict__ hist, int width, SelectCtl* ctl) {
+    __shared__ uint32_t wsum[NT / 32];
+    constexpr int PER = SEL_BINS / NT;
+    uint32_t loc[PER];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        loc[j] = hist[SEL_BINS - 1 - (threadIdx.x * PER + j)];
+        s += loc[j];
+    }
+    uint32_t tot;
+    const uint32_t before = block_exclusive_scan_u32(s, wsum, tot);
+    const unsigned long long k = ctl->k;
+    const unsigned long long prefix = ctl->prefix;
+    if (k > before && k <= (unsigned long long)before + s) {
+        unsigned long long kk = k - before, gt = ctl->count_gt + before;
+        int j = 0;
+        for (; j < PER - 1; ++j) {
+            if (kk <= loc[j]) break;
+            kk -= loc[j];
+            gt += loc[j];
+        }
+        const uint32_t d = SEL_BINS - 1 - (threadIdx.x * PER + j);
+        ctl->count_eq = loc[j];
+        ctl->prefix = (prefix << width) | (unsigned long long)d;
+        ctl->k = kk;
+        ctl->count_gt = gt;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) hist[i] = 0;
+}
+
+}  // namespace pb

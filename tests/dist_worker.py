@@ -1,0 +1,84 @@
+"""Worker of the sharded-path test: launched by torch.distributed.run with WORLD_SIZE ranks that all use cuda:0
+(gloo backend, exchanges staged through host memory), it runs the sharded trajectory and rank 0 compares the
+gathered global state with the CPU oracle step by step."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import paper_2603_07341_b200 as pb  # noqa: E402
+from paper_2603_07341_b200.dist import TorchComm, gather_state  # noqa: E402
+from cases import CASES  # noqa: E402
+
+
+def close(a, b, rtol=1e-10, atol=0.0):
+    return abs(a - b) <= atol + rtol * max(abs(a), abs(b))
+
+
+def main():
+    names = sys.argv[1].split(",")
+    max_steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    comm = TorchComm(device=0)
+    report = {}
+    port = None
+    if rank == 0:
+        from oracle import pyoracle
+
+        port = pyoracle.load_port()
+    for name in names:
+        case = CASES[name]
+        ctx = pb.Context(pb.ModelDef(**case["model"]), device=0, comm=comm)
+        run = ctx.run(**case["run"])
+        ro = None
+        if rank == 0:
+            ro = port.model(pyoracle.ModelDef(**case["model"])).run(**case["run"])
+        w, c = gather_state(run)
+        sizes = []
+        if rank == 0:
+            wo, co = ro.state()
+            assert np.array_equal(w, wo), (name, "init table")
+            assert c.tobytes() == co.tobytes(), (name, "init coeff")
+        for s in range(1, min(case["steps"], max_steps) + 1):
+            d = run.step()
+            w, c = gather_state(run)
+            local_rows = run.info()[0]
+            sizes.append(local_rows)
+            if rank == 0:
+                do = ro.step()
+                wo, co = ro.state()
+                assert d["q_true"] == do["q_true"], (name, s, d["q_true"], do["q_true"])
+                assert np.array_equal(w, wo), (name, s, "table")
+                assert c.tobytes() == co.tobytes(), (name, s, "coefficients not bit-identical")
+                assert d["taylor_order"] == do["taylor_order"], (name, s)
+                for k in ("norm_pre", "norm_post"):
+                    assert close(d[k], do[k]), (name, s, k, d[k], do[k])
+                assert close(d["energy"], do["energy"], 1e-10, 1e-12), (name, s, d["energy"], do["energy"])
+                assert close(d["discarded_weight"], do["discarded_weight"], 1e-9, 1e-30), (name, s)
+        ob = run.observe()
+        if rank == 0:
+            oo = ro.observe()
+            assert np.allclose(ob["density"], oo["density"], rtol=1e-10, atol=1e-18), name
+            assert abs(ob["amp"] - oo["amp"]) <= 1e-12, (name, ob["amp"], oo["amp"])
+            for k in ("norm", "energy", "rmsd", "xbar"):
+                assert close(ob[k], oo[k], 1e-10, 1e-12), (name, k, ob[k], oo[k])
+        allsizes = [None] * world
+        dist.all_gather_object(allsizes, sizes[-1] if sizes else 0)
+        report[name] = dict(steps=len(sizes), shard_rows=allsizes, calls=dict(comm.calls))
+    if rank == 0:
+        print("SHARDED_OK " + json.dumps(report), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
