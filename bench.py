@@ -208,18 +208,29 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device; the B200 path has no CPU fallback (use --impl reference)")
+    if os.environ.get("PB200_BENCH_SAME_DEVICE"):  # test hook: several ranks on one GPU (needs the gloo transport)
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     import paper_2603_07341_b200 as pb
 
+    comm = None
+    if world > 1:
+        # one process per GPU; ONE trajectory whose state and subspace are sharded by hash of the basis key
+        # (DESIGN.md section 6).  torch.distributed is the plumbing: NCCL for the device exchanges, gloo for the
+        # few-byte host collectives.
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if os.environ.get("PB200_BENCH_BACKEND") == "gloo":  # test hook: host-staged exchanges
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        from paper_2603_07341_b200.dist import TorchComm
+
+        comm = TorchComm(device=local)
+
     stream = torch.cuda.Stream()
-    ctx = pb.Context(pb.ModelDef(**MODEL), device=local)
+    ctx = pb.Context(pb.ModelDef(**MODEL), device=local, comm=comm)
     ctx.set_stream(stream.cuda_stream)
-    # N > 1: independent replicas, one per rank (weak scaling); each rank draws its own tie-break seed.
-    run_kw = dict(RUN, q_nom=args.q_nom, seed=RUN["seed"] + rank)
+    run_kw = dict(RUN, q_nom=args.q_nom)
 
     with torch.cuda.stream(stream):
         run = ctx.run(**run_kw)
@@ -248,20 +259,20 @@ def main():
         dev_ms = ev0.elapsed_time(ev1)
         times = run.times()
         launches = ctx.kernel_launches - launches0
-        # keep the same loop running so NVML (10 ms period) sees the clocks under this load
-        t_probe = time.perf_counter()
-        while time.perf_counter() - t_probe < 1.0:
-            run.step()
-        torch.cuda.synchronize()
-        clocks = sampler.stop()
-        clocks["window"] = "timed steps + 1 s continuation of the same step loop (NVML, 10 ms period)"
-
-        rows, nnz, t_now, steps_done = run.info()
-        t_ms = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        t_ms = torch.tensor([dev_ms], dtype=torch.float64)  # CPU tensor: gloo carries the scalar reductions
         if world > 1:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         step_ms = float(t_ms.item()) / args.steps
-        value = world * args.steps / (float(t_ms.item()) * 1e-3)
+        value = args.steps / (float(t_ms.item()) * 1e-3)  # one sharded trajectory: job throughput, not per rank
+        # keep the same loop running for ~1 s so NVML (10 ms period) sees the clocks under this load; the count is
+        # derived from the all-reduced step time so every rank runs the same number of (collective) steps
+        for _ in range(max(1, min(2000, int(1000.0 / max(step_ms, 1e-3))))):
+            run.step()
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        clocks["window"] = "timed steps + ~1 s continuation of the same step loop (NVML, 10 ms period)"
+        rows, nnz, t_now, steps_done = run.info()
+        rows_g, nnz_g = run.global_sizes()
 
         # ---- roofline of the dominant kernel (fused Taylor order) inside the timed steps
         peak, peak_src = measured_peak()
@@ -282,7 +293,13 @@ def main():
                                       "nnz_per_s": nnz / (spmv_ms * 1e-3)},
             "share_of_step": times["expmv_ms"] / max(times["total_ms"], 1e-9),
         }
-        spmv_rate = times["spmv_nnz"] / (times["expmv_ms"] * 1e-3) * world
+        spmv_rate = times["spmv_nnz"] / (times["expmv_ms"] * 1e-3)
+        if world > 1:  # job-wide nnz x orders per second: sum of the ranks' shares over the slowest rank's time
+            r_t = torch.tensor([float(times["spmv_nnz"]), 0.0], dtype=torch.float64)
+            m_t = torch.tensor([times["expmv_ms"]], dtype=torch.float64)
+            dist.all_reduce(r_t)
+            dist.all_reduce(m_t, op=dist.ReduceOp.MAX)
+            spmv_rate = float(r_t[0].item()) / (float(m_t.item()) * 1e-3)
 
         # ---- e2e: paces::step with a host SparseState in and out, every step (pinned host buffers)
         e2e = None
@@ -319,10 +336,10 @@ def main():
                 cur, n_cur, t_cur, sidx = cur ^ 1, n_next, dd["t"], sidx + 1
             ev1.record(stream)
             barrier()
-            e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+            e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64)
             if world > 1:
                 dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-            e2e = {"value": world * k_e2e / (float(e_ms.item()) * 1e-3), "unit": "timesteps/s",
+            e2e = {"value": k_e2e / (float(e_ms.item()) * 1e-3), "unit": "timesteps/s",
                    "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e, "steps": k_e2e,
                    "api": "pb200_step + pb200_run_state (paces::step on a host SparseState, pinned buffers)"}
 
@@ -356,11 +373,14 @@ def main():
         line = {
             "metric": "timesteps_per_sec", "value": value, "unit": "timesteps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128 amplitudes, u32 packed keys)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128 amplitudes, u32 packed keys)",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "q_nom": args.q_nom, "q_true": rows, "nnz": nnz,
+            "config": {"workload": WORKLOAD, "q_nom": args.q_nom, "q_true": rows_g, "nnz": nnz_g,
+                       "rank0_rows": rows, "rank0_nnz": nnz,
                        "taylor_order": d["taylor_order"], "spinup_steps": spin,
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+                       "parallelism": "single GPU" if world == 1 else
+                       f"state and subspace sharded over {world} GPUs by hash of the basis key (phonon part); "
+                       "NCCL all-to-all of candidate keys / look-ups / halos",
                        "l2": "per-step working set (~150 B/row x q_true ~ 0.5 GB) exceeds the 126 MB L2; no flush"},
             "spmv_nnz_per_sec": spmv_rate,
             "wall_ms_per_step": 1e3 * wall / args.steps,

@@ -177,6 +177,8 @@ int pb200_run_begin(pb200_ctx* ctx, const pb200_run_cfg* cfg);
 int pb200_run_step(pb200_ctx* ctx, pb200_diag* out);
 int pb200_run_info(const pb200_ctx* ctx, uint64_t* rows, uint64_t* nnz, double* t,
                    uint64_t* steps_done);
+/* Sharded runs: pb200_run_info/_state/_csr describe THIS rank's shard; the job-wide sizes are here. */
+int pb200_run_global(const pb200_ctx* ctx, uint64_t* rows_global, uint64_t* nnz_global);
 /* Canonical-order download: keys ascending, coefficients aligned (checkpoint order, io.hpp:77-99). */
 int pb200_run_state(pb200_ctx* ctx, uint32_t* words, double* coeff);
 int pb200_run_csr(pb200_ctx* ctx, int64_t* row_ptr, int32_t* col, double* val);

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
-    "pb200_run_state", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_run_observe", "pb200_run_times",
+    "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_run_observe", "pb200_run_times",
     "pb200_run_reset_times", "pb200_bench_taylor", "pb200_bench_spmv",
 ]
 
@@ -141,6 +141,7 @@ def load_library():
     L.pb200_run_step.argtypes = [vp, C.POINTER(Diag)]
     L.pb200_run_info.argtypes = [vp, u64p, u64p, f64p, u64p]
     L.pb200_run_state.argtypes = [vp, u32p, f64p]
+    L.pb200_run_global.argtypes = [vp, u64p, u64p]
     L.pb200_run_csr.argtypes = [vp, i64p, i32p, f64p]
     L.pb200_run_load_state.argtypes = [vp, C.POINTER(RunCfg), u32p, f64p, C.c_uint64, C.c_double, C.c_uint64]
     L.pb200_step.argtypes = [vp, C.POINTER(RunCfg), C.c_uint64, u32p, f64p, C.c_uint64, C.c_double, C.POINTER(Diag), u64p,
@@ -426,6 +427,12 @@ class Run:
         rows, nnz, t, s = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_uint64()
         self.ctx.lib.pb200_run_info(self.ctx.h, C.byref(rows), C.byref(nnz), C.byref(t), C.byref(s))
         return rows.value, nnz.value, t.value, s.value
+
+    def global_sizes(self):
+        """(q_true, nnz) of the whole job (equal to info()[:2] on one GPU)."""
+        rows, nnz = C.c_uint64(), C.c_uint64()
+        self.ctx.lib.pb200_run_global(self.ctx.h, C.byref(rows), C.byref(nnz))
+        return rows.value, nnz.value
 
     def state(self):
         rows, _, _, _ = self.info()

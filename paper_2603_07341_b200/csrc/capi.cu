@@ -390,6 +390,15 @@ int pb200_run_info(const pb200_ctx* ctx, uint64_t* rows, uint64_t* nnz, double* 
     return PB200_OK;
 }
 
+int pb200_run_global(const pb200_ctx* ctx, uint64_t* rows_global, uint64_t* nnz_global) {
+    if (!ctx || !ctx->eng.has_state) return PB200_ERR_ARG;
+    const Engine& e = ctx->eng;
+    const Space& sp = e.space[e.cur];
+    if (rows_global) *rows_global = e.world > 1 ? sp.n_global : sp.n;
+    if (nnz_global) *nnz_global = e.world > 1 ? sp.nnz_global : sp.nnz;
+    return PB200_OK;
+}
+
 int pb200_run_state(pb200_ctx* ctx, uint32_t* words, double* coeff) {
     return guarded(ctx, [&](Engine& e) {
         need(e.has_state, "no resident state");
@@ -454,9 +463,6 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
         e.cfg = c;
         e.has_cfg = true;
         e.has_state = false;
-        // the caller's table must be sorted (engine.hpp:110); checked on the device copy would cost a kernel, the
-        // host pass is a streaming compare of data that is about to cross PCIe anyway
-        if (!host_rows_sorted(words, rows, e.hm.W)) throw PacesError("truncate_select: state table must be sorted");
         Space& sp = e.space[e.cur];
         const size_t W = e.hm.W;
         sp.words.ensure(rows * W * 4 + 4);
@@ -466,6 +472,9 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
         sp.n = uint32_t(rows);
         sp.nnz = 0;
         sp.has_h = false;
+        // engine.hpp:110: the caller's table must be sorted -- checked on the device copy (one streaming kernel)
+        if (!e.rows_sorted_on_device(sp.words.as<uint32_t>(), sp.n))
+            throw PacesError("truncate_select: state table must be sorted");
         e.t = t;
         e.steps_done = step_index - 1;
         e.has_state = true;

@@ -71,6 +71,15 @@ void Engine::exclusive_scan(uint32_t* data, uint64_t n) {
     check_launch();
 }
 
+bool Engine::rows_sorted_on_device(const uint32_t* table, uint32_t n) {
+    Ctl* c = dctl();
+    uint32_t* bad = reinterpret_cast<uint32_t*>(&c->pad[0]);
+    PB_CUDA(cudaMemsetAsync(bad, 0, 4, stream));
+    PB_DISPATCH_W(md.W, check_sorted_kernel<W><<<grid_for(n), NT, 0, stream>>>(table, n, bad));
+    check_launch();
+    return read_back<uint32_t>(bad) == 0;
+}
+
 // ------------------------------------------------------------------------------------------------
 void Engine::set_model(const HostModel& m) {
     hm = m;

@@ -228,6 +228,7 @@ struct Engine {
         return v;
     }
     void exclusive_scan(uint32_t* data, uint64_t n);  // in place over n elements
+    bool rows_sorted_on_device(const uint32_t* table, uint32_t n);
     void require_model() const {
         if (!has_model) throw ArgError("no model set: call pb200_model_set first");
     }

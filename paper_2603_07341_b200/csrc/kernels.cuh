@@ -646,6 +646,16 @@ __global__ void apply_terms_kernel(ModelDev m, const uint32_t* __restrict__ keys
     }
 }
 
+/// bad[0] != 0 unless the rows are strictly ascending (PackedBasisTable::sorted, basis_codec.hpp:211).
+template <int W>
+__global__ void __launch_bounds__(NT) check_sorted_kernel(const uint32_t* __restrict__ table, uint32_t n,
+                                                          uint32_t* __restrict__ bad) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i + 1 < n; i += gridDim.x * NT) {
+        const Key<W> a = load_key<W>(table + size_t(i) * W), b = load_key<W>(table + size_t(i + 1) * W);
+        if (key_cmp<W>(a, b) >= 0) bad[0] = 1u;
+    }
+}
+
 /// L2 flush for benchmarking: streams a buffer larger than L2.
 __global__ void flush_kernel(double* __restrict__ buf, size_t n) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
