@@ -64,7 +64,7 @@ static void compare_runs(const char* name, const RunConfig& cfg) {
         CHECK(x.step == y.step && x.q_true == y.q_true && x.taylor_order == y.taylor_order, "%s: diag %zu ints", name, i);
         CHECK(close(x.t, y.t, 1e-14) && close(x.norm_pre, y.norm_pre) && close(x.norm_post, y.norm_post) &&
                   close(x.energy, y.energy, 1e-10, 1e-12) && close(x.discarded_weight, y.discarded_weight, 1e-9, 1e-30) &&
-                  std::fabs(x.delta_norm_expmv - y.delta_norm_expmv) <= 1e-14,
+                  std::fabs(x.delta_norm_expmv - y.delta_norm_expmv) <= 1e-12,
               "%s: diag %zu values", name, i);
     }
     for (std::size_t i = 0; i < std::min(a.trajectory.size(), b.trajectory.size()); ++i) {

@@ -42,7 +42,9 @@ def _check_diag(d, g, name, s):
     assert _close(d["energy"], g["energy"], RTOL, 1e-12), (name, s, "energy", d["energy"], g["energy"])
     assert _close(d["discarded_weight"], g["discarded_weight"], 1e-9, 1e-30), (name, s, d["discarded_weight"],
                                                                                 g["discarded_weight"])
-    assert abs(d["delta_norm_expmv"] - g["delta_norm_expmv"]) <= 1e-14, (name, s, "delta_norm_expmv")
+    # a difference of two norms ~1: reassociated sums move it by a few ulp of 1 per 1e5 rows (reference bound on
+    # the quantity itself: |delta| <= 1e-12, acceptance C2)
+    assert abs(d["delta_norm_expmv"] - g["delta_norm_expmv"]) <= 1e-12, (name, s, "delta_norm_expmv")
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -280,3 +282,60 @@ def test_large_step_properties(gpu, port):
     # select with q_nom >= support keeps exactly the support
     kept = ctx.truncate_select(w, c, len(w), 0)
     assert np.array_equal(kept, w[np.abs(c) ** 2 > 0])
+
+
+@pytest.mark.parametrize("name,model,run_kw,steps", [
+    # BASELINE config 3: 2D 6x6 aggregate, one mode per site, optical start (150-bit keys, 5 words); the
+    # autocorrelation <mu(t)mu(0)> is ObservablesRow.amp
+    ("cfg3_2d_6x6", dict(kind=1, extents=(6, 6), eps=(0.0,), hop=(-0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+     dict(init="optical", m_init=5, m=2, q_nom=20000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 8),
+    # BASELINE config 4: 3D 4x4x4 aggregate, localized start at the centre site (262-bit keys, 9 words)
+    ("cfg4_3d_4x4x4", dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+     dict(init="localized", site=-1, m_init=6, m=2, q_nom=20000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 8),
+    # paper regime key width: 1D N=75, d_pho=16 -> 7 + 300 bits = 10 words
+    ("wide_1d_75", dict(kind=1, extents=(75,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+     dict(init="localized", site=-1, m_init=6, m=2, q_nom=5000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 6),
+])
+def test_baseline_configs_against_oracle(gpu, port, name, model, run_kw, steps):
+    """BASELINE.json configs 3 and 4 (and a 10-word key) in lockstep with the oracle: tables, CSR and coefficients
+    bit-exact at every step, observables (density, autocorrelation amplitude) within 1e-10."""
+    from oracle.pyoracle import ModelDef
+
+    ctx = _ctx(gpu, model)
+    rg = ctx.run(**run_kw)
+    ro = port.model(ModelDef(**model)).run(**run_kw)
+    assert rg.info()[:2] == ro.info()[:2]
+    for s in range(1, steps + 1):
+        dg, do = rg.step(), ro.step()
+        wg, cg = rg.state()
+        wo, co = ro.state()
+        assert np.array_equal(wg, wo), (name, s)
+        assert cg.tobytes() == co.tobytes(), (name, s)
+        _check_diag(dg, do, name, s)
+        og, oo = rg.observe(), ro.observe()
+        assert _close(og["density"], oo["density"], RTOL, 1e-18), (name, s)
+        assert abs(og["amp"] - oo["amp"]) <= 1e-12, (name, s, og["amp"], oo["amp"])
+    for a, b in zip(rg.csr(), ro.csr()):
+        assert a.tobytes() == b.tobytes()
+    assert dg["q_true"] > run_kw["q_nom"]
+
+
+def test_checkpoint_resume_roundtrip(gpu, port):
+    """download (canonical order = checkpoint order, io.hpp:77-99), reload into a fresh context
+    with pb200_run_load_state and continue: identical to the uninterrupted run."""
+    case = CASES["disordered_L5_d6_optical"]
+    ctx = _ctx(gpu, case["model"])
+    run = ctx.run(**case["run"])
+    for _ in range(10):
+        run.step()
+    w, c = run.state()
+    _, _, t, sd = run.info()
+    cont = [run.step() for _ in range(10)]
+    w_end, c_end = run.state()
+    ctx2 = _ctx(gpu, case["model"])
+    kw = {k: v for k, v in case["run"].items() if k not in ("init", "site")}
+    run2 = ctx2.load_state(w, c, t=t, steps_done=sd, **kw)
+    resumed = [run2.step() for _ in range(10)]
+    w2, c2 = run2.state()
+    assert resumed == cont
+    assert w2.tobytes() == w_end.tobytes() and c2.tobytes() == c_end.tobytes()
