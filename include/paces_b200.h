@@ -194,6 +194,13 @@ int pb200_run_load_state(pb200_ctx* ctx, const pb200_run_cfg* cfg, const uint32_
 int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
                const double* coeff, uint64_t rows, double t, pb200_diag* out, uint64_t* rows_out,
                uint64_t* nnz_out);
+/* Same operator with the transfers overlapped with the step: the key upload runs beside the weight/selection
+ * kernels (which only need the coefficients), the download of the new table runs beside remap + <H> + expmv, and only
+ * the new coefficients cross PCIe after the last Taylor order.  out_words/out_coeff must hold out_cap_rows rows
+ * (pinned host memory for full PCIe speed); fails with PB200_ERR_ARG if the new state has more rows. */
+int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
+                  const double* coeff, uint64_t rows, double t, uint32_t* out_words, double* out_coeff,
+                  uint64_t out_cap_rows, pb200_diag* out, uint64_t* rows_out, uint64_t* nnz_out);
 /* detail::observe (engine.hpp:299-311): ObservablesRow of the resident state; density has
  * lattice_sites entries, amp is (re, im). */
 int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar,

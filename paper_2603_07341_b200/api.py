@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
-    "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_run_observe", "pb200_run_times",
+    "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_step_io", "pb200_run_observe", "pb200_run_times",
     "pb200_run_reset_times", "pb200_bench_taylor", "pb200_bench_spmv",
 ]
 
@@ -146,6 +146,8 @@ def load_library():
     L.pb200_run_load_state.argtypes = [vp, C.POINTER(RunCfg), u32p, f64p, C.c_uint64, C.c_double, C.c_uint64]
     L.pb200_step.argtypes = [vp, C.POINTER(RunCfg), C.c_uint64, u32p, f64p, C.c_uint64, C.c_double, C.POINTER(Diag), u64p,
                              u64p]
+    L.pb200_step_io.argtypes = [vp, C.POINTER(RunCfg), C.c_uint64, u32p, f64p, C.c_uint64, C.c_double, u32p, f64p,
+                                C.c_uint64, C.POINTER(Diag), u64p, u64p]
     L.pb200_run_observe.argtypes = [vp, f64p, f64p, f64p, f64p, f64p, f64p]
     L.pb200_run_times.argtypes = [vp, C.POINTER(PhaseTimes)]
     L.pb200_run_reset_times.argtypes = [vp]
@@ -385,11 +387,19 @@ class Context:
         cfg, keep = make_cfg(self.layout_sites, **kw)
         d = Diag()
         rows, nnz = C.c_uint64(), C.c_uint64()
+        if out_words is not None and out_coeff is not None:
+            # caller-owned (ideally pinned) result buffers: transfers overlap the step (pb200_step_io)
+            cap = min(out_words.size // self.words, out_coeff.size)
+            self._ck(self.lib.pb200_step_io(self.h, C.byref(cfg), step_index, _p(w, u32p), _p(cf, f64p), w.shape[0], t,
+                                            _p(out_words, u32p), _p(out_coeff.view(np.float64), f64p), cap, C.byref(d),
+                                            C.byref(rows), C.byref(nnz)))
+            n = rows.value
+            return out_words[: n * self.words].reshape(n, self.words), out_coeff[:n], d.as_dict()
         self._ck(self.lib.pb200_step(self.h, C.byref(cfg), step_index, _p(w, u32p), _p(cf, f64p), w.shape[0], t,
                                      C.byref(d), C.byref(rows), C.byref(nnz)))
         n = rows.value
-        ow = np.zeros((n, self.words), np.uint32) if out_words is None else out_words[: n * self.words].reshape(n, self.words)
-        oc = np.zeros(n, np.complex128) if out_coeff is None else out_coeff[:n]
+        ow = np.zeros((n, self.words), np.uint32)
+        oc = np.zeros(n, np.complex128)
         self._ck(self.lib.pb200_run_state(self.h, _p(ow, u32p), _p(oc.view(np.float64), f64p)))
         return ow, oc, d.as_dict()
 

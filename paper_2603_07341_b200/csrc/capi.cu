@@ -485,6 +485,62 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
     });
 }
 
+int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
+                  const double* coeff, uint64_t rows, double t, uint32_t* out_words, double* out_coeff,
+                  uint64_t out_cap_rows, pb200_diag* out, uint64_t* rows_out, uint64_t* nnz_out) {
+    return guarded(ctx, [&](Engine& e) {
+        e.require_model();
+        need(cfg && words && coeff && out_words && out_coeff, "step_io: null pointer");
+        need(step_index >= 2, "step: step_index must be >= 2 (step 1 evolves on the initial space, use pb200_run_*)");
+        if (rows == 0) throw PacesError("truncate_select: state has no support");
+        need(rows <= 0x7fffffffull, "too many rows");
+        pb200_run_cfg c = *cfg;
+        c.init_kind = 0;
+        c.n_entries = 0;
+        c.entry_occ = nullptr;
+        c.entry_amp = nullptr;
+        e.cfg = c;
+        e.has_cfg = true;
+        e.has_state = false;
+        Space& sp = e.space[e.cur];
+        const size_t W = e.hm.W;
+        sp.words.ensure(rows * W * 4 + 4);
+        e.coeff[e.ccur].ensure(rows * 16 + 16);
+        // coefficients first on the compute stream (the weight / selection kernels need only them); the keys travel
+        // on the copy stream and are awaited right before the compaction of the kept rows
+        PB_CUDA(cudaMemcpyAsync(e.coeff[e.ccur].p, coeff, rows * 16, cudaMemcpyHostToDevice, e.stream));
+        // both uploads share one PCIe direction: let the coefficients through first, then the keys
+        PB_CUDA(cudaEventRecord(e.ev_table, e.stream));
+        PB_CUDA(cudaStreamWaitEvent(e.copy_stream, e.ev_table, 0));
+        PB_CUDA(cudaMemcpyAsync(sp.words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.copy_stream));
+        PB_CUDA(cudaEventRecord(e.ev_words, e.copy_stream));
+        e.pending_words = true;
+        sp.n = uint32_t(rows);
+        sp.nnz = 0;
+        sp.has_h = false;
+        e.t = t;
+        e.steps_done = step_index - 1;
+        e.has_state = true;
+        Engine::StepIO io;
+        io.out_words = out_words;
+        io.out_coeff = out_coeff;
+        io.out_cap_rows = out_cap_rows;
+        struct Guard {
+            Engine& e;
+            ~Guard() {
+                e.io = nullptr;
+                e.pending_words = false;
+                cudaStreamSynchronize(e.copy_stream);  // never leave a transfer into caller memory in flight
+            }
+        } guard{e};
+        e.io = &io;
+        e.run_step(out);
+        const Space& nsp = e.space[e.cur];
+        if (rows_out) *rows_out = nsp.n;
+        if (nnz_out) *nnz_out = nsp.nnz;
+    });
+}
+
 int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar, double* amp,
                       double* density) {
     return guarded(ctx, [&](Engine& e) {

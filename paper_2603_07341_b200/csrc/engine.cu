@@ -42,6 +42,9 @@ Engine::Engine(int dev) : device(dev) {
     PB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PB_CUDA(cudaMallocHost(&pinned, 4096));
     for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
+    PB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    PB_CUDA(cudaEventCreateWithFlags(&ev_words, cudaEventDisableTiming));
+    PB_CUDA(cudaEventCreateWithFlags(&ev_table, cudaEventDisableTiming));
     ctl.ensure(sizeof(Ctl));
     PB_CUDA(cudaMemsetAsync(ctl.p, 0, sizeof(Ctl), stream));
     partials.ensure(sizeof(double) * 4 * size_t(sm_count) * 8);
@@ -55,6 +58,12 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& x : ev)
         if (x) cudaEventDestroy(x);
+    if (copy_stream) {
+        cudaStreamSynchronize(copy_stream);
+        cudaStreamDestroy(copy_stream);
+    }
+    if (ev_words) cudaEventDestroy(ev_words);
+    if (ev_table) cudaEventDestroy(ev_table);
     if (pinned) cudaFreeHost(pinned);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -352,6 +361,12 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
     pos_a.ensure((size_t(n) + 1) * 4);
     PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
     exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+    if (pending_words) {
+        // pb200_step_io: the keys were uploaded beside the kernels above; from here on they are needed
+        PB_CUDA(cudaStreamWaitEvent(stream, ev_words, 0));
+        pending_words = false;
+        if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
+    }
     const uint32_t kept = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
     seeds.ensure(size_t(kept) * W * 4 + 4);
     PB_DISPATCH_W(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,
@@ -663,6 +678,15 @@ void Engine::run_step(pb200_diag* out) {
         else
             grow(seeds.as<uint32_t>(), kept, cfg.m, next);
         PB_CUDA(cudaEventRecord(ev[3], stream));
+        if (io) {
+            // the new table is final: ship it to the host beside remap + <H> + expmv
+            if (next.n > io->out_cap_rows) throw ArgError("step_io: output buffers too small for the new state");
+            PB_CUDA(cudaEventRecord(ev_table, stream));
+            PB_CUDA(cudaStreamWaitEvent(copy_stream, ev_table, 0));
+            if (next.n)
+                PB_CUDA(cudaMemcpyAsync(io->out_words, next.words.p, size_t(next.n) * md.W * 4, cudaMemcpyDeviceToHost,
+                                        copy_stream));
+        }
         require_memory((world > 1 ? next.n_global : uint64_t(next.n)) * 16 * 4, "state vectors");
         coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
@@ -682,7 +706,10 @@ void Engine::run_step(pb200_diag* out) {
         else
             expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         PB_CUDA(cudaEventRecord(ev[6], stream));
+        if (io && next.n)
+            PB_CUDA(cudaMemcpyAsync(io->out_coeff, psi, size_t(next.n) * 16, cudaMemcpyDeviceToHost, stream));
         sync();
+        if (io) PB_CUDA(cudaStreamSynchronize(copy_stream));
         rec.taylor_order = order;
         rec.delta_norm_expmv = lcn - rec.norm_post;
         cur ^= 1;

@@ -158,6 +158,16 @@ struct Engine {
     DevBuf flush;
     void* pinned = nullptr;  // 4 KiB pinned host scratch for read-backs
     cudaEvent_t ev[10]{};
+    // host-buffer step with overlapped transfers (pb200_step_io)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_words = nullptr, ev_table = nullptr;
+    bool pending_words = false;   // the key upload of the current step is still in flight on copy_stream
+    struct StepIO {
+        uint32_t* out_words = nullptr;
+        double* out_coeff = nullptr;
+        uint64_t out_cap_rows = 0;
+    };
+    const StepIO* io = nullptr;
 
     // multi-GPU (one context per rank); world == 1 is the single-GPU path
     int rank = 0, world = 1;

@@ -334,6 +334,11 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
             check_launch();
         } else {
             // gather the tie KEYS of all ranks, order them canonically, draw exactly as engine.hpp:137-142
+            if (pending_words) {
+                PB_CUDA(cudaStreamWaitEvent(stream, ev_words, 0));
+                pending_words = false;
+                if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
+            }
             flag_tie.ensure((size_t(n) + 1) * 4);
             pos_a.ensure((size_t(n) + 1) * 4);
             select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 0, keep,
@@ -385,6 +390,11 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
     pos_a.ensure((size_t(n) + 1) * 4);
     PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
     exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
+    if (pending_words) {
+        PB_CUDA(cudaStreamWaitEvent(stream, ev_words, 0));
+        pending_words = false;
+        if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
+    }
     const uint32_t kept = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
     seeds.ensure(size_t(kept) * W * 4 + 4);
     PB_DISPATCH_WS(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,

@@ -339,3 +339,33 @@ def test_checkpoint_resume_roundtrip(gpu, port):
     w2, c2 = run2.state()
     assert resumed == cont
     assert w2.tobytes() == w_end.tobytes() and c2.tobytes() == c_end.tobytes()
+
+
+def test_host_step_operator(gpu, port):
+    """paces::step on host buffers (pb200_step) and its overlapped-transfer form (pb200_step_io) against the oracle."""
+    from oracle.pyoracle import ModelDef
+
+    case = CASES["cfg2_layout_L16_d16_small"]
+    ctx = _ctx(gpu, case["model"])
+    ro = port.model(ModelDef(**case["model"])).run(**case["run"])
+    for _ in range(5):
+        ro.step()
+    kw = {k: v for k, v in case["run"].items() if k not in ("init", "site")}
+    ow = np.zeros(200000 * ctx.words, np.uint32)
+    oc = np.zeros(200000, np.complex128)
+    for s in range(6, 12):
+        w, c = ro.state()
+        t = ro.info()[2]
+        a = ctx.step(w, c, t, s, **kw)
+        b = ctx.step(w, c, t, s, out_words=ow, out_coeff=oc, **kw)
+        do = ro.step()
+        wo, co = ro.state()
+        for got in (a, b):
+            assert np.array_equal(got[0], wo) and got[1].tobytes() == co.tobytes(), s
+            _check_diag(got[2], do, "host_step", s)
+    with pytest.raises(gpu.PacesError, match="must be sorted"):
+        ctx.step(w[::-1].copy(), c, t, 12, out_words=ow, out_coeff=oc, **kw)
+    with pytest.raises(gpu.PacesError, match="too small"):
+        ctx.step(w, c, t, 12, out_words=ow[: 10 * ctx.words], out_coeff=oc[:10], **kw)
+    # the context is still usable after the failures
+    assert np.array_equal(ctx.step(w, c, t, 12, **kw)[0], ctx.step(w, c, t, 12, out_words=ow, out_coeff=oc, **kw)[0])
