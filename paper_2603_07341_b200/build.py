@@ -15,10 +15,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpaces_b200.so")
 SOURCES = ["paces_b200.cu"]
-DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "keys.cuh", "primitives.cuh",
+DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "keys.cuh",
+        "primitives.cuh",
         "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
-              "-Xcompiler", "-fPIC,-O2", "-shared"]
+              "-Xcompiler", "-fPIC,-O2", "-shared", "-split-compile", "0"]
 
 
 def _nvcc() -> str:
@@ -39,6 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    if os.environ.get("PB200_ONLY_W"):  # development / profiling build restricted to one key width
+        cmd += ["-DPB_ONLY_W=" + str(int(os.environ["PB200_ONLY_W"]))]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)

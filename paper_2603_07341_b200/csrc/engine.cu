@@ -3,6 +3,13 @@
 
 namespace pb {
 
+#ifdef PB_ONLY_W  // development / profiling builds: one key width, small module, fast compile
+#define PB_DISPATCH_W(Wv, ...)                                  \
+    switch (Wv) {                                               \
+        case PB_ONLY_W: { constexpr int W = PB_ONLY_W; __VA_ARGS__; } break; \
+        default: throw PacesError("this development build only supports one key width (PB_ONLY_W)"); \
+    }
+#else
 #define PB_DISPATCH_W(Wv, ...)                                  \
     switch (Wv) {                                               \
         case 1: { constexpr int W = 1; __VA_ARGS__; } break;    \
@@ -23,6 +30,7 @@ namespace pb {
         case 16: { constexpr int W = 16; __VA_ARGS__; } break;  \
         default: throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build"); \
     }
+#endif
 
 // ------------------------------------------------------------------------------------------------
 Engine::Engine(int dev) : device(dev) {
@@ -139,6 +147,24 @@ void Engine::set_model(const HostModel& m) {
     md.g = d_g.as<double>();
     md.nb_site = d_nbs.as<int>();
     md.nb_amp = d_nba.as<double>();
+    for (int w = 0; w <= 16; ++w) {
+        // first phonon register whose leading bit (offset b0 + j*bp) is at or beyond bit 32*w
+        int j = 0;
+        if (md.bp > 0 && 32 * w > md.b0) j = (32 * w - md.b0 + md.bp - 1) / md.bp;
+        md.wfirst[w] = std::min(j, md.nph);
+    }
+    {
+        // omega[j] * double(n): the products the diagonal sums, tabulated once (same IEEE multiply as
+        // lattice_models.hpp:234; the host compiler contracts no FMA)
+        const int nph = (m.kind == 1) ? int(L) : 0;
+        const size_t per = size_t(1) << m.bp;
+        std::vector<double> tab(std::max<size_t>(1, size_t(nph) * per), 0.0);
+        for (int j = 0; j < nph; ++j)
+            for (size_t q = 0; q < per; ++q) tab[size_t(j) * per + q] = om[size_t(j)] * double(q);
+        d_omega_n.ensure(tab.size() * 8);
+        PB_CUDA(cudaMemcpy(d_omega_n.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+        md.omega_n = d_omega_n.as<double>();
+    }
     row_width = max_deg + (m.kind == 1 ? 2 : 0) + 1;
     has_model = true;
     has_state = false;
@@ -230,7 +256,7 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
         PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
         const uint32_t* fr = identity_frontier ? nullptr : frontier[fcur].as<uint32_t>();
         const uint32_t xchunk = chunk_for(nf);
-        PB_DISPATCH_W(W, expand_level_kernel<W><<<grid_chunked(nf, xchunk), NT, 0, stream>>>(
+        PB_DISPATCH_W(W, expand_window_kernel<W><<<grid_chunked(nf, xchunk), NT, 0, stream>>>(
                              md, out.words.as<uint32_t>(), n, fr, nf, xchunk, cand_keys.as<uint32_t>(),
                              cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow, count_emitted));
         check_launch();
@@ -268,7 +294,7 @@ void Engine::assemble(Space& sp) {
     tmp_val.ensure(size_t(n) * width * 8);
     sp.row_ptr.ensure((size_t(n) + 1) * 4);
     const uint32_t achunk = chunk_for(n);
-    PB_DISPATCH_W(W, assemble_rows_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
+    PB_DISPATCH_W(W, assemble_window_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
                          md, sp.words.as<uint32_t>(), n, achunk, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                          sp.row_ptr.as<uint32_t>()));
     check_launch();
@@ -384,9 +410,9 @@ double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t n
     const int W = md.W;
     Ctl* c = dctl();
     PB_CUDA(cudaMemsetAsync(dst_c, 0, size_t(nd) * 16, stream));
-    const uint32_t rchunk = 1;
-    const int rgrid = grid_for(ns);
-    PB_DISPATCH_W(W, remap_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
+    const uint32_t rchunk = chunk_for(ns);
+    const int rgrid = grid_chunked(ns, rchunk);
+    PB_DISPATCH_W(W, remap_window_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
                                                                partials.as<double>(), &c->ticket, c->out));
     check_launch();
     const double d = read_back<double>(c->out);

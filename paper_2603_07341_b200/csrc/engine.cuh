@@ -13,6 +13,7 @@
 #include "../../include/paces_b200.h"
 #include "host_model.hpp"
 #include "kernels.cuh"
+#include "window.cuh"
 #include "sharded.cuh"
 
 namespace pb {
@@ -129,7 +130,7 @@ struct Engine {
     bool has_model = false;
     HostModel hm;
     ModelDev md{};
-    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba;
+    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n;
     int row_width = 1;  // max entries of an H_eff row for this model
 
     // resident trajectory

@@ -27,53 +27,7 @@ struct GrowCounters {
     uint32_t max_seg;        // longest gap segment seen (diagnostic)
 };
 
-/// For every frontier row: generate the off-diagonal neighbours (apply_terms,
-/// lattice_models.hpp:212-267; apply_to_rows, subspace.hpp:102-134), look each one up in the sorted
-/// table and append those that are absent, together with their insertion gap.  gap_count[g] counts the
-/// candidates that fall between table rows g-1 and g.
-/// Each thread walks `chunk` CONSECUTIVE frontier rows (ascending keys) with one cursor per move, so all
-/// look-ups after the first are short forward gallops (per-thread merge join with the table).
-/// frontier == nullptr means "all rows" (order 0: the seeds are the table).
-template <int W>
-__global__ void __launch_bounds__(NT) expand_level_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
-                                                          const uint32_t* __restrict__ frontier, uint32_t nf,
-                                                          uint32_t chunk, uint32_t* __restrict__ cand_keys,
-                                                          uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
-                                                          uint32_t* __restrict__ gap_count, GrowCounters* ctr,
-                                                          int count_emitted) {
-    unsigned long long emitted = 0;
-    // a warp covers 32*chunk consecutive frontier rows; lane l takes rows base + 32 j + l, so every step of
-    // the warp reads 32 consecutive rows (coalesced) while each lane still sees ascending keys
-    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
-    MoveCursors cur;
-    cur.reset(0xffffffffu);
-    for (uint64_t f = wbase; f < min(uint64_t(nf), uint64_t(wbase + 32ull * chunk)); f += 32) {
-        const uint32_t row = frontier ? __ldg(frontier + f) : uint32_t(f);
-        const Key<W> k = load_key<W>(table + size_t(row) * W);
-        const uint32_t e = exciton_site<W>(m, k);
-        if (e != cur.site) cur.reset(e);
-        if (count_emitted && diagonal_element<W>(m, k, e) != 0.0) ++emitted;
-        for_each_neighbor<W>(m, k, false, [&](int move, const Key<W>& kk, double, bool) {
-            ++emitted;
-            uint32_t pos;
-            if (!cursor_find<W>(table, n, cur, move, kk, pos)) {
-                const uint32_t slot = append_slot(&ctr->n_cand);
-                if (slot < cand_cap) {
-                    store_key<W>(cand_keys + size_t(slot) * W, kk);
-                    cand_gap[slot] = pos;
-                    atomicAdd(gap_count + pos, 1u);
-                } else {
-                    ctr->overflow = 1;
-                }
-            }
-        });
-    }
-    // transcript size bookkeeping (feeds the reference's memory-cap check, subspace.hpp:215-217)
-    if (count_emitted) {
-        for (int o = 16; o > 0; o >>= 1) emitted += __shfl_xor_sync(0xffffffffu, emitted, o);
-        if ((threadIdx.x & 31) == 0 && emitted) atomicAdd(&ctr->emitted, emitted);
-    }
-}
+// The expansion kernel itself (expand_window_kernel) lives in window.cuh.
 
 // ================================================================================================
 // K2  dedup: counting sort by insertion gap, then exact dedup + ranking inside each (tiny) gap segment
@@ -181,39 +135,7 @@ __global__ void __launch_bounds__(NT) merge_new_rows_kernel(const uint32_t* __re
 // ================================================================================================
 constexpr int MAX_ROW = 2 * 3 + 3;  // hops (<= 6) + 2 ladder + diagonal
 
-/// Pass 1: row i of H_eff = {(index(k'), a) : (k', a) in apply_terms(key_i), k' in table}
-/// (replaces assemble_effective_hamiltonian, subspace.hpp:142-187, and the
-/// final-frontier filter, :225-241).  Neighbours are generated in ascending key order, so the found
-/// columns are already ascending.  Each thread walks `chunk` consecutive rows with per-move cursors
-/// (see expand_level_kernel).  Results are parked in fixed-width scratch (stride `width`).
-template <int W>
-__global__ void __launch_bounds__(NT) assemble_rows_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
-                                                           uint32_t chunk, int width, uint32_t* __restrict__ tmp_col,
-                                                           double* __restrict__ tmp_val,
-                                                           uint32_t* __restrict__ row_len) {
-    const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
-    MoveCursors cur;
-    cur.reset(0xffffffffu);
-    for (uint64_t ii = wbase; ii < min(uint64_t(n), uint64_t(wbase + 32ull * chunk)); ii += 32) {
-        const uint32_t i = uint32_t(ii);
-        const Key<W> k = load_key<W>(table + size_t(i) * W);
-        const uint32_t e = exciton_site<W>(m, k);
-        if (e != cur.site) cur.reset(e);
-        int len = 0;
-        uint32_t* tc = tmp_col + size_t(i) * width;
-        double* tv = tmp_val + size_t(i) * width;
-        for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
-            uint32_t pos = i;
-            const bool found = is_diag ? true : cursor_find<W>(table, n, cur, move, kk, pos);
-            if (found) {
-                tc[len] = pos;
-                tv[len] = amp;
-                ++len;
-            }
-        });
-        row_len[i] = uint32_t(len);
-    }
-}
+// Pass 1 (assemble_window_kernel) lives in window.cuh.
 
 /// Pass 2: compact the fixed-width scratch into CSR (row_ptr from the scan of row_len).
 __global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int width, const uint32_t* __restrict__ tmp_col,
@@ -504,31 +426,7 @@ __global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __rest
     }
 }
 
-// ================================================================================================
-// K7  remap (remap_state, subspace.hpp:281-305): look every old key up in the new table; copy the
-//     coefficient when present, otherwise add |c|^2 to the discarded weight.  dst must be zeroed.
-// ================================================================================================
-template <int W>
-__global__ void __launch_bounds__(NT) remap_kernel(const uint32_t* __restrict__ src_table,
-                                                   const double2* __restrict__ src_c, uint32_t ns,
-                                                   const uint32_t* __restrict__ dst_table, uint32_t nd, uint32_t chunk,
-                                                   double2* __restrict__ dst_c, double* __restrict__ partials,
-                                                   unsigned* ticket, double* __restrict__ out) {
-    __shared__ double smem[NT / 32];
-    double acc[1] = {0.0};
-    (void)chunk;
-    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < ns; i += gridDim.x * NT) {
-        const Key<W> k = load_key<W>(src_table + size_t(i) * W);
-        const double2 x = src_c[i];
-        uint32_t pos;
-        if (find_row<W>(dst_table, nd, k, pos))
-            dst_c[pos] = x;
-        else
-            acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
-    }
-    double tot[1];
-    if (grid_sum<1>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) out[0] = tot[0];
-}
+// K7 (remap_window_kernel) lives in window.cuh.
 
 // ================================================================================================
 // K8  observables: norm^2 + exciton density (observables.hpp:26-37), dipole overlap (:99-112),

@@ -32,6 +32,8 @@ struct ModelDev {
     const double* g;       // [L]   vibronic couplings (0 where absent)
     const int* nb_site;    // [L*MAX_NB] hop partners sorted ascending, -1 padded; zero-amplitude bonds removed
     const double* nb_amp;  // [L*MAX_NB] bond amplitude J
+    const double* omega_n;  // [nph << bp] omega[j] * double(n), the product the diagonal sums (same IEEE multiply)
+    int wfirst[17];        // wfirst[w] = first phonon register whose leading bit lies in key word >= w (nph past the end)
 };
 
 template <int W>
@@ -198,11 +200,22 @@ __device__ __forceinline__ double diagonal_element(const ModelDev& m, const Key<
     const double ee = __ldg(m.eps + e);
     if (ee != 0.0) diag = __dadd_rn(diag, ee);
     if (m.nph > 0 && m.bp > 0) {
-        for (int j = 0; j < m.nph; ++j) {
-            const uint32_t n = phonon_occ<W>(m, k, j);
-            if (n != 0) {
-                const double om = __ldg(m.omega + j);
-                if (om != 0.0) diag = __dadd_rn(diag, __dmul_rn(om, double(n)));
+        const uint64_t fmask = (m.bp >= 32) ? 0xffffffffull : ((1ull << m.bp) - 1);
+        // word by word (compile-time word index, so the key stays in registers); registers are visited in
+        // ascending j because register j starts at bit b0 + j*bp
+#pragma unroll
+        for (int wi = 0; wi < W; ++wi) {
+            const uint32_t cur = k.w[wi];
+            const uint32_t nxt = (wi + 1 < W) ? k.w[wi + 1] : 0u;
+            if ((cur | nxt) == 0u) continue;  // every register starting in this word is empty
+            const uint64_t win = (uint64_t(cur) << 32) | nxt;
+            const int j1 = m.wfirst[wi + 1];
+            for (int j = m.wfirst[wi]; j < j1; ++j) {
+                const int sh = 64 - (m.b0 + j * m.bp - 32 * wi) - m.bp;
+                const uint32_t n = uint32_t((win >> sh) & fmask);
+                // omega[j] * double(n) from the table; a zero product (omega[j] == 0: the term does not exist,
+                // lattice_models.hpp:169) adds +0.0, which leaves diag unchanged bit for bit
+                if (n != 0) diag = __dadd_rn(diag, __ldg(m.omega_n + (size_t(j) << m.bp) + n));
             }
         }
     }

@@ -9,6 +9,13 @@
 
 namespace pb {
 
+#ifdef PB_ONLY_W  // development / profiling builds: one key width, small module, fast compile
+#define PB_DISPATCH_WS(Wv, ...)                                  \
+    switch (Wv) {                                               \
+        case PB_ONLY_W: { constexpr int W = PB_ONLY_W; __VA_ARGS__; } break; \
+        default: throw PacesError("this development build only supports one key width (PB_ONLY_W)"); \
+    }
+#else
 #define PB_DISPATCH_WS(Wv, ...)                                 \
     switch (Wv) {                                               \
         case 1: { constexpr int W = 1; __VA_ARGS__; } break;    \
@@ -29,6 +36,7 @@ namespace pb {
         case 16: { constexpr int W = 16; __VA_ARGS__; } break;  \
         default: throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build"); \
     }
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // routing helpers

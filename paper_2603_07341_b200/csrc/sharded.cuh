@@ -19,7 +19,7 @@ struct ShardCounters {
 };
 
 /// Expansion of one BFS order on a shard.  Neighbours owned by this rank take the local path of
-/// expand_level_kernel (look-up, candidate + gap when absent); the others are appended to the outgoing list
+/// expand_window_kernel (look-up, candidate + gap when absent); the others are appended to the outgoing list
 /// with their destination rank.
 template <int W>
 __global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) classify_received_kernel(const uint32_t* _
     }
 }
 
-/// Assembly pass 1 on a shard: like assemble_rows_kernel, but a neighbour owned by another rank becomes a
+/// Assembly pass 1 on a shard: like assemble_window_kernel, but a neighbour owned by another rank becomes a
 /// look-up request; its scratch column holds COL_REQ | request id until the replies arrive.  Entries stay
 /// in ascending NEIGHBOUR-KEY order (the reference's summation order), whatever their final column.
 template <int W>
