@@ -330,27 +330,40 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
     init.k = q_nom;
     std::memcpy(pinned, &init, sizeof(init));
     PB_CUDA(cudaMemcpyAsync(&c->select, pinned, sizeof(SelectCtl), cudaMemcpyHostToDevice, stream));
-    weights_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select);
+    // pass 1 (weights + top digit) -> pass 2 -> gather the surviving group -> single-CTA tail; ONE read-back
+    sel_list.ensure(size_t(SEL_LIST_CAP) * 8);
+    weights_hist_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select,
+                                              hist.as<uint32_t>());
+    check_launch();
+    select_pass_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 42, 11, &c->select, hist.as<uint32_t>(), 2);
+    check_launch();
+    select_gather_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 42, &c->select,
+                                               sel_list.as<unsigned long long>());
+    check_launch();
+    select_tail_kernel<<<1, NT, 0, stream>>>(sel_list.as<unsigned long long>(), &c->select);
     check_launch();
     SelectCtl sc = read_back<SelectCtl>(&c->select);
     if (norm2_out) *norm2_out = sc.norm2;
     if (sc.support == 0) throw PacesError("truncate_select: state has no support");
 
     uint32_t* keep = flag_keep.as<uint32_t>();
+    uint64_t kept64 = sc.support;
     if (sc.support <= q_nom) {
         select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
         check_launch();
     } else {
-        // 6 passes over 64 bits: 11-bit digits from the top, the last one 9 bits wide
-        static const int shifts[6] = {53, 42, 31, 20, 9, 0};
-        static const int widths[6] = {11, 11, 11, 11, 11, 9};
-        const int sg = std::min(g, sm_count * 2);
-        for (int p = 0; p < 6; ++p) {
-            select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
-                                                      hist.as<uint32_t>(), 1);
-            check_launch();
+        kept64 = q_nom;
+        if (!sc.tail_done) {
+            // the group sharing the first 22 bits did not fit the list (massive exact ties): full passes
+            static const int shifts[4] = {31, 20, 9, 0};
+            static const int widths[4] = {11, 11, 11, 9};
+            for (int p = 0; p < 4; ++p) {
+                select_pass_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
+                                                         hist.as<uint32_t>(), 1);
+                check_launch();
+            }
+            sc = read_back<SelectCtl>(&c->select);
         }
-        sc = read_back<SelectCtl>(&c->select);
         const uint64_t need = q_nom - sc.count_gt;  // 1 <= need <= count_eq
         if (need >= sc.count_eq) {
             // every tie is admitted: the shuffle loop of engine.hpp:138-141 does not run
@@ -393,7 +406,7 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         pending_words = false;
         if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
     }
-    const uint32_t kept = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
+    const uint32_t kept = uint32_t(kept64);  // = popcount of keep[]: support when nothing is cut, else q_nom
     seeds.ensure(size_t(kept) * W * 4 + 4);
     PB_DISPATCH_W(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,
                                                                   seeds.as<uint32_t>()));

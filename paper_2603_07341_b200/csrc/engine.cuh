@@ -153,7 +153,7 @@ struct Engine {
     uint32_t n_seeds = 0;
     DevBuf tab_tmp, frontier[2], cand_keys, cand_gap, perm, seg_rank, gap, scan_tiles;
     DevBuf tmp_col, tmp_val, row_len;
-    DevBuf weights, flag_keep, flag_tie, pos_a, idx_tmp, hist;
+    DevBuf weights, flag_keep, flag_tie, pos_a, idx_tmp, hist, sel_list;
     DevBuf term[2], partials, ctl;  // ctl: small device control block
     DevBuf aux_words, aux_coeff, aux2_words, aux2_coeff, aux_vec;  // staging for the host-buffer operators
     DevBuf flush;

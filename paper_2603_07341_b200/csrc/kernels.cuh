@@ -280,8 +280,10 @@ struct SelectCtl {
     unsigned long long count_eq;  // weights equal to the cutoff
     unsigned long long support;   // weights > 0
     unsigned ticket;
-    unsigned pad;
+    unsigned list_n;              // candidates gathered for the single-CTA tail (select_gather_kernel)
     double norm2;                 // sum of weights
+    unsigned tail_done;           // 1: prefix is the full 64-bit cutoff (select_tail_kernel finished the digits)
+    unsigned pad;
 };
 
 /// w_i = re^2 + im^2 (std::norm), sum and support count.
@@ -315,6 +317,7 @@ __global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restric
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ uint32_t wsum[NT / 32];
     __shared__ bool is_last;
+    if (fuse_pick == 2 && ctl->support <= ctl->k) return;  // single-GPU pipeline: nothing is cut
     for (int i = threadIdx.x; i < SEL_BINS; i += NT) sh[i] = 0;
     __syncthreads();
     const unsigned long long prefix = ctl->prefix;
@@ -367,6 +370,133 @@ __global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restric
     __syncthreads();
     for (int i = threadIdx.x; i < SEL_BINS; i += NT) hist[i] = 0;
     if (threadIdx.x == 0) ctl->ticket = 0;
+}
+
+/// Pick step shared by the select kernels: the calling CTA (NT threads) walks the `width`-bit histogram from
+/// the top bin down until the wanted rank ctl->k falls inside a bin, extends ctl->prefix by that digit and
+/// updates k / count_gt / count_eq.  Bins are read from `bins` (global or shared).
+__device__ __forceinline__ void select_pick_block(const uint32_t* bins, int width, SelectCtl* ctl, uint32_t* wsum) {
+    constexpr int PER = SEL_BINS / NT;
+    uint32_t loc[PER];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        loc[j] = bins[SEL_BINS - 1 - (threadIdx.x * PER + j)];
+        s += loc[j];
+    }
+    uint32_t tot;
+    const uint32_t before = block_exclusive_scan_u32(s, wsum, tot);  // weights in higher bins owned by earlier threads
+    const unsigned long long k = ctl->k;
+    const unsigned long long prefix = ctl->prefix;
+    __syncthreads();  // everyone has read k / prefix before the owner rewrites them
+    if (k > before && k <= (unsigned long long)before + s) {
+        unsigned long long kk = k - before, gt = ctl->count_gt + before;
+        int j = 0;
+        for (; j < PER - 1; ++j) {
+            if (kk <= loc[j]) break;
+            kk -= loc[j];
+            gt += loc[j];
+        }
+        const uint32_t d = SEL_BINS - 1 - (threadIdx.x * PER + j);
+        ctl->count_eq = loc[j];
+        ctl->prefix = (prefix << width) | (unsigned long long)d;
+        ctl->k = kk;
+        ctl->count_gt = gt;
+    }
+    __syncthreads();
+}
+
+/// Adds one to sh[digit] for every active lane, one shared-memory atomic per distinct digit in the warp (weights
+/// cluster in a few exponents, so plain per-lane atomics would serialise 32 ways on the top digit).
+__device__ __forceinline__ void hist_add_aggregated(uint32_t* sh, uint32_t digit) {
+    const unsigned peers = __match_any_sync(__activemask(), digit);
+    if ((threadIdx.x & 31) == uint32_t(__ffs(peers) - 1)) atomicAdd(&sh[digit], uint32_t(__popc(peers)));
+}
+
+/// Selection pass 1 fused with the weights: w_i = re^2 + im^2 (std::norm, engine.hpp:113-116), their sum, the
+/// support count, and the histogram of the top 11 bits (sign + exponent) of the positive weights.  The last CTA
+/// to finish stores norm2 / support and, when support > q_nom (= ctl->k on entry), picks the first digit.
+__global__ void __launch_bounds__(NT) weights_hist_kernel(const double2* __restrict__ c, uint32_t n,
+                                                          double* __restrict__ w, double* __restrict__ partials,
+                                                          SelectCtl* ctl, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[SEL_BINS];
+    __shared__ double smem[NT / 32];
+    __shared__ uint32_t wsum[NT / 32];
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) sh[i] = 0;
+    __syncthreads();
+    double acc[2] = {0.0, 0.0};
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const double2 x = c[i];
+        const double ww = __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y));
+        w[i] = ww;
+        acc[0] = __dadd_rn(acc[0], ww);
+        if (ww > 0.0) {
+            acc[1] = acc[1] + 1.0;  // exact for counts < 2^53
+            hist_add_aggregated(sh, uint32_t((unsigned long long)__double_as_longlong(ww) >> 53));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) {
+        const uint32_t v = sh[i];
+        if (v) atomicAdd(hist + i, v);
+    }
+    __threadfence();  // the histogram contributions are visible before this CTA takes its ticket (inside grid_sum)
+    double tot[2];
+    if (!grid_sum<2>(acc, partials, &ctl->ticket, tot, smem)) return;
+    const unsigned long long support = (unsigned long long)tot[1];
+    if (threadIdx.x == 0) {
+        ctl->norm2 = tot[0];
+        ctl->support = support;
+    }
+    __syncthreads();
+    if (support > ctl->k) {
+        for (int i = threadIdx.x; i < SEL_BINS; i += NT) sh[i] = __ldcg(hist + i);
+        __syncthreads();
+        select_pick_block(sh, 11, ctl, wsum);
+    }
+    for (int i = threadIdx.x; i < SEL_BINS; i += NT) hist[i] = 0;
+}
+
+constexpr uint32_t SEL_LIST_CAP = 1u << 16;
+
+/// After the first two digits (22 bits) the group that still contains the cutoff is almost always tiny: gather
+/// its members' bit patterns so one CTA can finish the remaining 42 bits.  Does nothing when the group is larger
+/// than the list (massive exact ties): the host then falls back to full passes.
+__global__ void __launch_bounds__(NT) select_gather_kernel(const double* __restrict__ w, uint32_t n, int hi_shift,
+                                                           SelectCtl* ctl, unsigned long long* __restrict__ list) {
+    if (ctl->support <= ctl->k) return;  // nothing is cut (after a pick the wanted rank is below the support)
+    if (ctl->count_eq > SEL_LIST_CAP) return;
+    const unsigned long long prefix = ctl->prefix;
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const double ww = w[i];
+        if (!(ww > 0.0)) continue;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(ww);
+        if ((bits >> hi_shift) == prefix) list[append_slot(&ctl->list_n)] = bits;
+    }
+}
+
+/// Single CTA: remaining digits (shifts 31, 20, 9, 0; widths 11, 11, 11, 9) over the gathered list.
+__global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long long* __restrict__ list, SelectCtl* ctl) {
+    __shared__ uint32_t sh[SEL_BINS];
+    __shared__ uint32_t wsum[NT / 32];
+    const uint32_t cnt = ctl->list_n;
+    if (cnt == 0 || ctl->count_eq > SEL_LIST_CAP) return;
+    const int shifts[4] = {31, 20, 9, 0};
+    const int widths[4] = {11, 11, 11, 9};
+    for (int p = 0; p < 4; ++p) {
+        for (int i = threadIdx.x; i < SEL_BINS; i += NT) sh[i] = 0;
+        __syncthreads();
+        const unsigned long long prefix = ctl->prefix;
+        const int hi_shift = shifts[p] + widths[p];
+        const uint32_t dmask = (1u << widths[p]) - 1u;
+        for (uint32_t i = threadIdx.x; i < cnt; i += NT) {
+            const unsigned long long bits = list[i];
+            if ((bits >> hi_shift) == prefix) atomicAdd(&sh[uint32_t(bits >> shifts[p]) & dmask], 1u);
+        }
+        __syncthreads();
+        select_pick_block(sh, widths[p], ctl, wsum);
+    }
+    if (threadIdx.x == 0) ctl->tail_done = 1;
 }
 
 /// mode 0: keep every supported row (w > 0).  mode 1: keep w > cutoff, and w == cutoff too when
