@@ -179,43 +179,64 @@ void Engine::set_model(const HostModel& m) {
 // scatter that writes the merged sorted table plus the next (sorted) frontier.  Expects gap[] (n+2 counters)
 // filled by the expansion kernel; the new frontier ends up in frontier[fcur] (fcur is flipped).
 // ------------------------------------------------------------------------------------------------
-uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc, int& fcur) {
+uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcur, bool deferred,
+                             GrowCounters* counters) {
     const int W = md.W;
     Ctl* c = dctl();
+    const uint32_t* nc_ptr = &c->grow.n_cand;  // exact candidate count, on the device
+    const int gc_grid = grid_for(nc_bound);
     // counting sort by insertion gap: gap[] (counts) -> segment starts; row_len[] is the per-gap cursor
     // during placement and then the per-gap survivor count
     exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
-    perm.ensure(size_t(nc) * 4);
-    seg_rank.ensure(size_t(nc) * 4);
+    perm.ensure(size_t(nc_bound) * 4 + 4);
+    seg_rank.ensure(size_t(nc_bound) * 4 + 4);
     row_len.ensure((size_t(n) + 2) * 4);
     PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
-    place_candidates_kernel<<<grid_for(nc), NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc, gap.as<uint32_t>(),
-                                                              row_len.as<uint32_t>(), perm.as<uint32_t>());
+    place_candidates_kernel<<<gc_grid, NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc_ptr, gap.as<uint32_t>(),
+                                                        row_len.as<uint32_t>(), perm.as<uint32_t>());
     check_launch();
     PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
-    PB_DISPATCH_W(W, segment_dedup_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
-                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+    PB_DISPATCH_W(W, segment_dedup_kernel<W><<<gc_grid, NT, 0, stream>>>(
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr,
                          gap.as<uint32_t>(), seg_rank.as<uint32_t>(), row_len.as<uint32_t>(), &c->grow));
     check_launch();
-    PB_DISPATCH_W(W, segment_rank_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
-                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc,
+    PB_DISPATCH_W(W, segment_rank_kernel<W><<<gc_grid, NT, 0, stream>>>(
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr,
                          gap.as<uint32_t>(), seg_rank.as<uint32_t>()));
     check_launch();
     // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
     exclusive_scan(row_len.as<uint32_t>(), uint64_t(n) + 2);
-    const uint32_t n_new = read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
-    const uint64_t n_next64 = uint64_t(n) + n_new;
-    if (n_next64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
-    tab_tmp.ensure(size_t(n_next64) * W * 4);
-    frontier[fcur ^ 1].ensure(size_t(n_new) * 4 + 4);
+    uint32_t n_new = 0;
+    uint64_t rows_bound;
+    if (deferred) {
+        // size the merged table by the bound n + nc_bound and read the counts back once, after the scatter
+        PB_CUDA(cudaMemcpyAsync(&c->n_new, row_len.as<uint32_t>() + (size_t(n) + 1), 4, cudaMemcpyDeviceToDevice,
+                                stream));
+        rows_bound = uint64_t(n) + nc_bound;
+        frontier[fcur ^ 1].ensure(size_t(nc_bound) * 4 + 4);
+    } else {
+        n_new = read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
+        rows_bound = uint64_t(n) + n_new;
+        frontier[fcur ^ 1].ensure(size_t(n_new) * 4 + 4);
+    }
+    if (rows_bound > 0x7fffffffull && !deferred)
+        throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+    tab_tmp.ensure(size_t(rows_bound) * W * 4);
     PB_DISPATCH_W(W, merge_old_rows_kernel<W><<<grid_for(n), NT, 0, stream>>>(
                          out.words.as<uint32_t>(), n, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>()));
     check_launch();
-    PB_DISPATCH_W(W, merge_new_rows_kernel<W><<<grid_for(nc), NT, 0, stream>>>(
+    PB_DISPATCH_W(W, merge_new_rows_kernel<W><<<gc_grid, NT, 0, stream>>>(
                          cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
-                         seg_rank.as<uint32_t>(), nc, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>(),
+                         seg_rank.as<uint32_t>(), nc_ptr, row_len.as<uint32_t>(), tab_tmp.as<uint32_t>(),
                          frontier[fcur ^ 1].as<uint32_t>()));
     check_launch();
+    if (deferred) {
+        const Ctl snap = read_back<Ctl>(c);
+        if (counters) *counters = snap.grow;
+        n_new = snap.n_new;
+        if (uint64_t(n) + n_new > 0x7fffffffull)
+            throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+    }
     out.words.swap(tab_tmp);
     fcur ^= 1;
     return n_new;
@@ -260,20 +281,14 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
                              md, out.words.as<uint32_t>(), n, fr, nf, xchunk, cand_keys.as<uint32_t>(),
                              cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow, count_emitted));
         check_launch();
-        GrowCounters gc = read_back<GrowCounters>(&c->grow);
+        // dedup + merge run on the device-side candidate count; ONE read-back per BFS order brings the counters
+        GrowCounters gc{};
+        const uint32_t n_new = merge_level(out, n, cand_cap, fcur, true, &gc);
         if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
         emitted_total += gc.emitted;
-        const uint32_t nc = gc.n_cand;
-        if (nc == 0) {
-            nf = 0;
-            // the reference still runs its memory check for this order
-            require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
-            break;
-        }
-        const uint32_t n_new = merge_level(out, n, nc, fcur);
         identity_frontier = false;
         n += n_new;
-        nf = n_new;
+        nf = n_new;  // 0 when nothing new was found: the loop ends, the (re-copied) table is unchanged
         require_memory((uint64_t(n) * W + emitted_total * W * 2) * 4 + emitted_total * 8, "subspace growth");
     }
     out.n = n;
@@ -300,11 +315,19 @@ void Engine::assemble(Space& sp) {
     check_launch();
     PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
     exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
-    const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
-    // the reference's assembly buffer check: 2 entries of 16 bytes per transcript element (subspace.hpp:152)
-    require_memory(uint64_t(nnz) * 2 * 16, "matrix assembly buffer");
-    sp.col.ensure(size_t(nnz) * 4 + 4);
-    sp.val.ensure(size_t(nnz) * 8 + 8);
+    uint32_t nnz = 0;
+    if (defer_reads) {
+        // resident step: size col/val by the row-width bound and pick nnz up with the step's final read-back
+        PB_CUDA(cudaMemcpyAsync(&dctl()->nnz, sp.row_ptr.as<uint32_t>() + n, 4, cudaMemcpyDeviceToDevice, stream));
+        sp.col.ensure(size_t(n) * width * 4 + 4);
+        sp.val.ensure(size_t(n) * width * 8 + 8);
+    } else {
+        nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
+        // the reference's assembly buffer check: 2 entries of 16 bytes per transcript element (subspace.hpp:152)
+        require_memory(uint64_t(nnz) * 2 * 16, "matrix assembly buffer");
+        sp.col.ensure(size_t(nnz) * 4 + 4);
+        sp.val.ensure(size_t(nnz) * 8 + 8);
+    }
     assemble_compact_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                                                             sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                             sp.val.as<double>());
@@ -418,21 +441,34 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
 // ------------------------------------------------------------------------------------------------
 // remap_state (subspace.hpp:281-305)
 // ------------------------------------------------------------------------------------------------
-double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
-                     uint32_t nd, double2* dst_c) {
+void Engine::remap_async(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
+                         uint32_t nd, double2* dst_c) {
     const int W = md.W;
     Ctl* c = dctl();
     PB_CUDA(cudaMemsetAsync(dst_c, 0, size_t(nd) * 16, stream));
     const uint32_t rchunk = chunk_for(ns);
     const int rgrid = grid_chunked(ns, rchunk);
     PB_DISPATCH_W(W, remap_window_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
-                                                               partials.as<double>(), &c->ticket, c->out));
+                                                                      partials.as<double>(), &c->ticket, c->out));
     check_launch();
-    const double d = read_back<double>(c->out);
+}
+
+double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
+                     uint32_t nd, double2* dst_c) {
+    remap_async(src_words, src_c, ns, dst_words, nd, dst_c);
+    const double d = read_back<double>(dctl()->out);
     return world > 1 ? allreduce_host(d) : d;
 }
 
 // ------------------------------------------------------------------------------------------------
+void Engine::expectation_async(const Space& sp, const double2* x) {
+    Ctl* c = dctl();
+    expectation_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                          sp.val.as<double>(), x, partials.as<double>(), &c->ticket,
+                                                          c->out + 1);
+    check_launch();
+}
+
 void Engine::expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite) {
     Ctl* c = dctl();
     if (world > 1) {
@@ -442,14 +478,11 @@ void Engine::expectation(const Space& sp, const double2* x, double* exp_out, dou
         halo_exchange(sp, term[0].as<double2>());
         x = term[0].as<double2>();
     }
-    expectation_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                                          sp.val.as<double>(), x, partials.as<double>(), &c->ticket,
-                                                          c->out);
-    check_launch();
+    expectation_async(sp, x);
     struct R {
         double v[3];
     };
-    R r = read_back<R>(c->out);
+    R r = read_back<R>(c->out + 1);
     if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, r.v, 3), "allreduce_f64_host");
     if (exp_out) *exp_out = r.v[0];
     if (norm2_out) *norm2_out = r.v[1];
@@ -503,7 +536,8 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                                                           partials.as<double>(), &c->taylor, 0, nullptr);
                 check_launch();
             }
-            tc = read_back<TaylorCtl>(&c->taylor);
+            last_ctl = read_back<Ctl>(c);  // one read-back carries the stop flag AND the step's deferred scalars
+            tc = last_ctl.taylor;
             if (tc.done) {
                 converged = true;
                 break;
@@ -706,6 +740,12 @@ void Engine::run_step(pb200_diag* out) {
         Space& next = space[cur ^ 1];
         double n2_pre = 0;
         const uint64_t sel_seed = pb200_mix_seed(cfg.seed + s);
+        // one GPU: remap / <H> / nnz stay on the device and come back with expmv's final read-back
+        struct DeferGuard {
+            bool& flag;
+            ~DeferGuard() { flag = false; }
+        } defer_guard{defer_reads};
+        defer_reads = (world == 1);
         const uint32_t kept = world > 1
                                   ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
                                   : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre);
@@ -729,21 +769,43 @@ void Engine::run_step(pb200_diag* out) {
         require_memory((world > 1 ? next.n_global : uint64_t(next.n)) * 16 * 4, "state vectors");
         coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
-        rec.discarded_weight =
-            remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
-        PB_CUDA(cudaEventRecord(ev[4], stream));
         double e = 0, n2 = 0;
-        expectation(next, psi, &e, &n2, true);
-        PB_CUDA(cudaEventRecord(ev[5], stream));
+        if (defer_reads) {
+            remap_async(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+            PB_CUDA(cudaEventRecord(ev[4], stream));
+            expectation_async(next, psi);
+            PB_CUDA(cudaEventRecord(ev[5], stream));
+        } else {
+            rec.discarded_weight =
+                remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+            PB_CUDA(cudaEventRecord(ev[4], stream));
+            expectation(next, psi, &e, &n2, true);
+            PB_CUDA(cudaEventRecord(ev[5], stream));
+        }
+        int order = 0;
+        double ltn = 0, lcn = 0;
+        if (world > 1) {
+            expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+        } else {
+            try {
+                expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+            } catch (const PacesError&) {
+                // the reference checks its input before it iterates (propagator.hpp:55-57)
+                if (last_ctl.out[3] != 0.0) throw PacesError("expmv: non-finite input coefficient");
+                throw;
+            }
+            // deferred scalars, all produced before the read-back that filled last_ctl
+            rec.discarded_weight = last_ctl.out[0];
+            e = last_ctl.out[1];
+            n2 = last_ctl.out[2];
+            if (last_ctl.out[3] != 0.0) throw PacesError("expmv: non-finite input coefficient");
+            next.nnz = last_ctl.nnz;
+            // the reference's assembly buffer check: 2 entries of 16 bytes per transcript element (subspace.hpp:152)
+            require_memory(uint64_t(next.nnz) * 2 * 16, "matrix assembly buffer");
+        }
         rec.norm_post = std::sqrt(n2);
         rec.q_true = world > 1 ? next.n_global : next.n;
         rec.energy = e;
-        int order = 0;
-        double ltn = 0, lcn = 0;
-        if (world > 1)
-            expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
-        else
-            expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         PB_CUDA(cudaEventRecord(ev[6], stream));
         if (io && next.n)
             PB_CUDA(cudaMemcpyAsync(io->out_coeff, psi, size_t(next.n) * 16, cudaMemcpyDeviceToHost, stream));

@@ -251,8 +251,15 @@ struct Engine {
         SelectCtl select;
         unsigned ticket;  // generic reduction ticket
         unsigned pad[3];
-        double out[8];  // generic reduction outputs
+        double out[8];  // reduction outputs: [0] remap (discarded weight), [1..3] expectation, [4..] scratch
+        uint32_t nnz;   // row_ptr[n] of the last assembly (read with the step's final read-back)
+        uint32_t n_new; // unique new keys of the last merge (read together with the expansion counters)
+        uint32_t pad2[2];
     };
+    /// Snapshot of the control block taken by the last read-back of expmv(): the step's deferred scalars
+    /// (discarded weight, <H>, norm, nnz) ride along instead of costing a stream synchronisation each.
+    Ctl last_ctl{};
+    bool defer_reads = false;  // run_step on one GPU: leave scalars on the device until the final read-back
     Ctl* dctl() const { return ctl.as<Ctl>(); }
 
     // ---- model
@@ -261,13 +268,21 @@ struct Engine {
     // ---- operators on device data
     void grow(const uint32_t* d_seeds, uint32_t n_seeds_, int order, Space& out);
     /// dedup + merge of the nc candidates of one BFS order into out.words (n rows); returns the number of new keys
-    uint32_t merge_level(Space& out, uint32_t n, uint32_t nc, int& fcur);
+    /// nc_bound >= the candidate count (which the kernels read from Ctl::grow.n_cand).  deferred: no read-back until
+    /// the scatter is queued; the counters of the expansion come back through *counters.
+    uint32_t merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcur, bool deferred = false,
+                         GrowCounters* counters = nullptr);
     void assemble(Space& sp);
     /// returns kept count; result in this->seeds
     uint32_t select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
                     double* norm2_out);
     double remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
                  uint32_t nd, double2* dst_c);
+    /// launches only: the discarded weight lands in Ctl::out[0]
+    void remap_async(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
+                     uint32_t nd, double2* dst_c);
+    /// launches only: <x|H|x>, |x|^2, #non-finite land in Ctl::out[1..3]
+    void expectation_async(const Space& sp, const double2* x);
     /// out: <x|H|x>, |x|^2; throws on non-finite input when check_finite
     void expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite);
     void expmv(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps, int* order_used,

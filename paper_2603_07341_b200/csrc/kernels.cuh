@@ -34,10 +34,12 @@ struct GrowCounters {
 // ================================================================================================
 
 /// perm[seg_start[gap] + k] = candidate id, k = arrival order inside the gap (gap_fill starts at zero).
-__global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap, uint32_t nc,
+__global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap,
+                                                              const uint32_t* __restrict__ nc_ptr,
                                                               const uint32_t* __restrict__ seg_start,
                                                               uint32_t* __restrict__ gap_fill,
                                                               uint32_t* __restrict__ perm) {
+    const uint32_t nc = *nc_ptr;  // the candidate count stays on the device: no host round trip before the merge
     for (uint32_t c = blockIdx.x * NT + threadIdx.x; c < nc; c += gridDim.x * NT) {
         const uint32_t g = cand_gap[c];
         const uint32_t r = atomicAdd(gap_fill + g, 1u);
@@ -53,10 +55,12 @@ constexpr uint32_t SEG_DUP = 0xffffffffu;
 template <int W>
 __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __restrict__ cand_keys,
                                                            const uint32_t* __restrict__ cand_gap,
-                                                           const uint32_t* __restrict__ perm, uint32_t nc,
+                                                           const uint32_t* __restrict__ perm,
+                                                           const uint32_t* __restrict__ nc_ptr,
                                                            const uint32_t* __restrict__ seg_start,
                                                            uint32_t* __restrict__ seg_rank,
                                                            uint32_t* __restrict__ gap_kept, GrowCounters* ctr) {
+    const uint32_t nc = *nc_ptr;
     for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
         const uint32_t c = perm[s];
         const uint32_t g = cand_gap[c];
@@ -76,9 +80,11 @@ __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __res
 template <int W>
 __global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __restrict__ cand_keys,
                                                           const uint32_t* __restrict__ cand_gap,
-                                                          const uint32_t* __restrict__ perm, uint32_t nc,
+                                                          const uint32_t* __restrict__ perm,
+                                                          const uint32_t* __restrict__ nc_ptr,
                                                           const uint32_t* __restrict__ seg_start,
                                                           volatile uint32_t* seg_rank) {
+    const uint32_t nc = *nc_ptr;
     for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
         if (seg_rank[s] == SEG_DUP) continue;
         const uint32_t c = perm[s];
@@ -113,10 +119,12 @@ template <int W>
 __global__ void __launch_bounds__(NT) merge_new_rows_kernel(const uint32_t* __restrict__ cand_keys,
                                                             const uint32_t* __restrict__ cand_gap,
                                                             const uint32_t* __restrict__ perm,
-                                                            const uint32_t* __restrict__ seg_rank, uint32_t nc,
+                                                            const uint32_t* __restrict__ seg_rank,
+                                                            const uint32_t* __restrict__ nc_ptr,
                                                             const uint32_t* __restrict__ kept_before,
                                                             uint32_t* __restrict__ out,
                                                             uint32_t* __restrict__ next_frontier) {
+    const uint32_t nc = *nc_ptr;
     for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
         const uint32_t r = seg_rank[s];
         if (r == SEG_DUP) continue;

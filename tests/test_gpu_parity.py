@@ -131,6 +131,35 @@ def test_selection_ties_match_golden(gpu, golden_small):
     assert len(seen) > 1
 
 
+def test_selection_large_groups_against_oracle(gpu, port):
+    """Selection paths beyond the golden vectors, on a 1e5+-row table (engine.hpp:107-156): (a) the usual case --
+    the group sharing the cutoff's first 22 bits is tiny and one CTA finishes the digits; (b) > 65536 weights share
+    those bits but differ further down (full radix passes); (c) a massive exact tie cut by the seeded draw."""
+    from oracle.pyoracle import ModelDef
+
+    kw = dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16)
+    ctx = _ctx(gpu, kw)
+    om = port.model(ModelDef(**kw))
+    seed = om.pack([8] + [0] * 16).reshape(1, -1)
+    table = ctx.grow(seed, 14)[0]
+    n = table.shape[0]
+    assert n > 100000
+    rng = np.random.default_rng(5)
+    cases = {
+        "spread": (rng.standard_normal(n) + 1j * rng.standard_normal(n)) * np.exp(-8 * rng.random(n)),
+        "shared_prefix": np.sqrt(1.0 + np.arange(n) * 2.0 ** -40) + 0j,
+        "massive_tie": np.full(n, 0.5 + 0.5j),
+    }
+    cases["massive_tie"][:: 97] = 2.0
+    cases["massive_tie"][5:: 89] = 0.0
+    for name, c in cases.items():
+        c = np.ascontiguousarray(c.astype(np.complex128))
+        for q_nom, sd in ((1000, 3), (n // 2, 11), (n - 3, 2), (n + 5, 0)):
+            got = ctx.truncate_select(table, c, q_nom, sd)
+            want = om.truncate_select(table, c, q_nom, sd)
+            assert np.array_equal(got, want), (name, q_nom, got.shape, want.shape)
+
+
 @pytest.mark.parametrize("name", ["disordered_4x3_d7", "cube_2x2x2_d16", "tb_chain_31", "cfg2_layout_L16_d16_small",
                                   "square_3x3_d5"])
 def test_operators_against_oracle(gpu, port, name):
