@@ -78,13 +78,12 @@ Engine::~Engine() {
 
 void Engine::exclusive_scan(uint32_t* data, uint64_t n) {
     if (n == 0) return;
-    const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    scan_tiles.ensure(ntiles * sizeof(uint32_t));
-    scan_tile_sums_kernel<<<unsigned(ntiles), NT, 0, stream>>>(data, n, scan_tiles.as<uint32_t>());
-    check_launch();
-    scan_spine_kernel<<<1, 1024, 0, stream>>>(scan_tiles.as<uint32_t>(), uint32_t(ntiles));
-    check_launch();
-    scan_apply_kernel<<<unsigned(ntiles), NT, 0, stream>>>(data, n, scan_tiles.as<uint32_t>(), data);
+    const uint64_t ntiles = (n + LB_TILE - 1) / LB_TILE;
+    // [ticket (8 bytes)] [status: one 64-bit word per tile]
+    scan_tiles.ensure((ntiles + 1) * 8);
+    PB_CUDA(cudaMemsetAsync(scan_tiles.p, 0, (ntiles + 1) * 8, stream));
+    unsigned long long* st = scan_tiles.as<unsigned long long>();
+    scan_lookback_kernel<<<unsigned(ntiles), NT, 0, stream>>>(data, n, data, st + 1, reinterpret_cast<unsigned*>(st));
     check_launch();
 }
 

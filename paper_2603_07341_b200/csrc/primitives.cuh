@@ -1,5 +1,5 @@
 // primitives.cuh -- device-wide building blocks shared by the paces kernels: deterministic block
-// reductions with last-block finalisation, a three-kernel exclusive scan, and warp-aggregated appends.
+// reductions with last-block finalisation, a single-pass exclusive scan, and warp-aggregated appends.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -63,11 +63,8 @@ __device__ __forceinline__ bool grid_sum(const double (&v)[K], double* partials,
 }
 
 // ------------------------------------------------------------------------------------------------
-// exclusive scan of uint32 (three kernels: tile sums -> spine -> apply).  Callers pass n+1 elements
-// with in[n] == 0 so out[n] is the total.  out may alias in.
+// exclusive scan of uint32.  Callers pass n+1 elements with in[n] == 0 so out[n] is the total.  out may alias in.
 // ------------------------------------------------------------------------------------------------
-constexpr int SCAN_IPT = 8;
-constexpr int SCAN_TILE = NT * SCAN_IPT;
 
 __device__ __forceinline__ uint32_t block_exclusive_scan_u32(uint32_t v, uint32_t* smem, uint32_t& block_total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -91,67 +88,91 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_u32(uint32_t v, uint32_
     return woff + inc - v;
 }
 
-__global__ void __launch_bounds__(NT) scan_tile_sums_kernel(const uint32_t* __restrict__ in, uint64_t n,
-                                                            uint32_t* __restrict__ tile_sums) {
-    __shared__ uint32_t smem[NT / 32];
-    const uint64_t base = uint64_t(blockIdx.x) * SCAN_TILE + uint64_t(threadIdx.x) * SCAN_IPT;
-    uint32_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_IPT; ++i)
-        if (base + i < n) s += in[base + i];
-    uint32_t tot;
-    block_exclusive_scan_u32(s, smem, tot);
-    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
-}
+// ------------------------------------------------------------------------------------------------
+// single-pass exclusive scan (decoupled look-back): every element is read once and written once.  Tiles are
+// handed out through an atomic ticket so a tile's predecessors are always already running; each tile publishes
+// its aggregate, looks back over the published aggregates / inclusive prefixes of earlier tiles (one warp, 32
+// tiles per round) and then publishes its own inclusive prefix.  status[] and *ticket must be zero on entry.
+// ------------------------------------------------------------------------------------------------
+constexpr int LB_IPT = 16;
+constexpr int LB_TILE = NT * LB_IPT;
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PREFIX = 2ull << 62, LB_FLAGS = 3ull << 62;
 
-__global__ void __launch_bounds__(1024) scan_spine_kernel(uint32_t* __restrict__ tile_sums, uint32_t ntiles) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t carry_s;
-    if (threadIdx.x == 0) carry_s = 0;
+__global__ void __launch_bounds__(NT) scan_lookback_kernel(const uint32_t* in, uint64_t n, uint32_t* out,
+                                                           unsigned long long* status, unsigned* ticket) {
+    __shared__ uint32_t smem[NT / 32];
+    __shared__ uint32_t s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < ntiles; base += 1024) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t v = (i < ntiles) ? tile_sums[i] : 0;
-        uint32_t inc = v;
+    const uint32_t tile = s_tile;
+    const uint64_t base = uint64_t(tile) * LB_TILE + uint64_t(threadIdx.x) * LB_IPT;
+    uint32_t v[LB_IPT];
+    if (base + LB_IPT <= n) {
+        const uint4* p = reinterpret_cast<const uint4*>(in + base);
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
+        for (int i = 0; i < LB_IPT / 4; ++i) {
+            const uint4 x = p[i];
+            v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
         }
-        if (lane == 31) wsum[warp] = inc;
-        __syncthreads();
-        uint32_t woff = 0, tot = 0;
-        for (int w = 0; w < 32; ++w) {
-            const uint32_t s = wsum[w];
-            if (w < warp) woff += s;
-            tot += s;
-        }
-        const uint32_t carry = carry_s;
-        if (i < ntiles) tile_sums[i] = carry + woff + inc - v;
-        __syncthreads();
-        if (threadIdx.x == 0) carry_s = carry + tot;
-        __syncthreads();
+    } else {
+#pragma unroll
+        for (int i = 0; i < LB_IPT; ++i) v[i] = (base + i < n) ? in[base + i] : 0u;
     }
-}
-
-__global__ void __launch_bounds__(NT) scan_apply_kernel(const uint32_t* in, uint64_t n,
-                                                        const uint32_t* __restrict__ tile_off, uint32_t* out) {
-    __shared__ uint32_t smem[NT / 32];
-    const uint64_t base = uint64_t(blockIdx.x) * SCAN_TILE + uint64_t(threadIdx.x) * SCAN_IPT;
-    uint32_t v[SCAN_IPT];
     uint32_t s = 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; ++i) {
-        v[i] = (base + i < n) ? in[base + i] : 0;
-        s += v[i];
+    for (int i = 0; i < LB_IPT; ++i) s += v[i];
+    uint32_t total;
+    const uint32_t toff = block_exclusive_scan_u32(s, smem, total);
+    if (threadIdx.x == 0) {
+        // 64-bit aligned stores are single transactions: flag and value arrive together
+        *reinterpret_cast<volatile unsigned long long*>(status + tile) = (tile == 0 ? LB_PREFIX : LB_AGG) | total;
+        if (tile == 0) s_prefix = 0;
     }
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan_u32(s, smem, tot) + tile_off[blockIdx.x];
+    if (tile > 0 && threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        uint32_t prefix = 0;
+        int64_t idx = int64_t(tile) - 1;
+        for (;;) {
+            const int64_t j = idx - lane;
+            unsigned long long st = LB_PREFIX;  // before tile 0: an empty inclusive prefix
+            if (j >= 0) {
+                do {
+                    st = *reinterpret_cast<volatile unsigned long long*>(status + j);
+                } while ((st & LB_FLAGS) == 0);
+            }
+            const unsigned done = __ballot_sync(0xffffffffu, (st & LB_FLAGS) == LB_PREFIX);
+            const int stop = done ? __ffs(done) - 1 : 32;  // nearest tile that already knows its inclusive prefix
+            uint32_t part = (int(lane) <= stop) ? uint32_t(st) : 0u;
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; ++i) {
-        if (base + i < n) out[base + i] = run;
-        run += v[i];
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            prefix += part;
+            if (done) break;
+            idx -= 32;
+        }
+        if (lane == 0) {
+            *reinterpret_cast<volatile unsigned long long*>(status + tile) = LB_PREFIX | (uint32_t)(prefix + total);
+            s_prefix = prefix;
+        }
+    }
+    __syncthreads();
+    uint32_t run = s_prefix + toff;
+    if (base + LB_IPT <= n) {
+        uint4* q = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+        for (int i = 0; i < LB_IPT / 4; ++i) {
+            uint4 x;
+            x.x = run, run += v[4 * i];
+            x.y = run, run += v[4 * i + 1];
+            x.z = run, run += v[4 * i + 2];
+            x.w = run, run += v[4 * i + 3];
+            q[i] = x;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < LB_IPT; ++i) {
+            if (base + i < n) out[base + i] = run;
+            run += v[i];
+        }
     }
 }
 
