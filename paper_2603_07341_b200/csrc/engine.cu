@@ -55,7 +55,7 @@ Engine::Engine(int dev) : device(dev) {
     PB_CUDA(cudaEventCreateWithFlags(&ev_table, cudaEventDisableTiming));
     ctl.ensure(sizeof(Ctl));
     PB_CUDA(cudaMemsetAsync(ctl.p, 0, sizeof(Ctl), stream));
-    partials.ensure(sizeof(double) * 4 * size_t(sm_count) * 8);
+    partials.ensure(sizeof(double) * 8 * size_t(sm_count) * 8);
     hist.ensure(SEL_BINS * sizeof(uint32_t));
     PB_CUDA(cudaMemsetAsync(hist.p, 0, SEL_BINS * sizeof(uint32_t), stream));
     sync();
@@ -498,7 +498,7 @@ void Engine::spmv(const Space& sp, const double2* x, double2* y) {
 // expmv (propagator.hpp:52-92)
 // ------------------------------------------------------------------------------------------------
 void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
-                   int* order_used, double* last_term_norm, double* last_c_norm) {
+                   int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_expectation) {
     if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
     if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
     if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
@@ -529,10 +529,18 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
             const int end = std::min(max_order, order + batch - 1);
             for (; order <= end; ++order) {
                 const double b = -dt_sub / double(order);
-                taylor_order_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                                          sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
-                                                          term[order & 1].as<double2>(), c_vec, b, order, rtol,
-                                                          partials.as<double>(), &c->taylor, 0, nullptr);
+                if (fuse_expectation && s == 0 && order == 1)
+                    // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
+                    // (Ctl::out[1..3], read with the final read-back)
+                    taylor_order_kernel_t<true><<<g, NT, 0, stream>>>(
+                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
+                        term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
+                        partials.as<double>(), &c->taylor, 0, nullptr, c->out + 1);
+                else
+                    taylor_order_kernel_t<false><<<g, NT, 0, stream>>>(
+                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
+                        term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
+                        partials.as<double>(), &c->taylor, 0, nullptr, nullptr);
                 check_launch();
             }
             last_ctl = read_back<Ctl>(c);  // one read-back carries the stop flag AND the step's deferred scalars
@@ -772,8 +780,7 @@ void Engine::run_step(pb200_diag* out) {
         if (defer_reads) {
             remap_async(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
             PB_CUDA(cudaEventRecord(ev[4], stream));
-            expectation_async(next, psi);
-            PB_CUDA(cudaEventRecord(ev[5], stream));
+            PB_CUDA(cudaEventRecord(ev[5], stream));  // <H> is produced by the first Taylor order
         } else {
             rec.discarded_weight =
                 remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
@@ -787,7 +794,7 @@ void Engine::run_step(pb200_diag* out) {
             expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         } else {
             try {
-                expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+                expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, true);
             } catch (const PacesError&) {
                 // the reference checks its input before it iterates (propagator.hpp:55-57)
                 if (last_ctl.out[3] != 0.0) throw PacesError("expmv: non-finite input coefficient");

@@ -176,17 +176,26 @@ struct TaylorCtl {
     unsigned pad;
 };
 
-__global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double2* __restrict__ term_in,
-                                                          double2* __restrict__ term_out, double2* __restrict__ c,
-                                                          double b, int order, double rtol,
-                                                          double* __restrict__ partials, TaylorCtl* ctl,
-                                                          int ignore_stop, double* __restrict__ tot_out) {
+/// EXPECT: the launch of the FIRST order also produces what csr_expectation (subspace.hpp:46-55), state_norm and
+/// expmv's finiteness check (propagator.hpp:55-57) need from the input vector x = term_in -- the row sums (H x)_i
+/// are the very ones the first order computes -- so the resident step needs no separate <x|H|x> pass:
+/// expect_out[0] = sum_i Re(conj(x_i) (H x)_i), [1] = sum |x_i|^2, [2] = #non-finite coefficients.
+template <bool EXPECT>
+__global__ void __launch_bounds__(NT) taylor_order_kernel_t(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                            const int32_t* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double2* __restrict__ term_in,
+                                                            double2* __restrict__ term_out, double2* __restrict__ c,
+                                                            double b, int order, double rtol,
+                                                            double* __restrict__ partials, TaylorCtl* ctl,
+                                                            int ignore_stop, double* __restrict__ tot_out,
+                                                            double* __restrict__ expect_out) {
+    constexpr int K = EXPECT ? 5 : 2;
     __shared__ double smem[NT / 32];
     if (!ignore_stop && *(volatile int*)&ctl->done) return;
-    double acc[2] = {0.0, 0.0};
+    double acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.0;
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
         double ar = 0.0, ai = 0.0;
@@ -195,6 +204,13 @@ __global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint
             const double2 x = __ldg(term_in + __ldg(col + k));
             ar = __dadd_rn(ar, __dmul_rn(v, x.x));
             ai = __dadd_rn(ai, __dmul_rn(v, x.y));
+        }
+        if (EXPECT) {
+            const double2 xi = __ldg(term_in + i);
+            // real(conj(x) * row) = xr*rr - (-xi)*ri
+            acc[2] = __dadd_rn(acc[2], __dsub_rn(__dmul_rn(xi.x, ar), __dmul_rn(-xi.y, ai)));
+            acc[3] = __dadd_rn(acc[3], __dadd_rn(__dmul_rn(xi.x, xi.x), __dmul_rn(xi.y, xi.y)));
+            if (!isfinite(xi.x) || !isfinite(xi.y)) acc[4] = acc[4] + 1.0;
         }
         // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
         const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
@@ -207,8 +223,13 @@ __global__ void __launch_bounds__(NT) taylor_order_kernel(uint32_t n, const uint
         acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti)));
         acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
     }
-    double tot[2];
-    if (grid_sum<2>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+    double tot[K];
+    if (grid_sum<K>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+        if (EXPECT) {
+            expect_out[0] = tot[2];
+            expect_out[1] = tot[3];
+            expect_out[2] = tot[4];
+        }
         if (tot_out) {  // sharded: the sums are all-reduced first, taylor_stop_kernel applies the rule
             tot_out[0] = tot[0];
             tot_out[1] = tot[1];
