@@ -41,6 +41,17 @@ WORKLOAD = "C2: 1D Holstein chain L=16, g=1, J=1, omega=1, d_pho=16 (68-bit keys
 SPINUP_MAX = 40
 
 
+def measured_traffic(bytes_per_launch):
+    """DRAM bytes per launch of the Taylor kernel from the committed ncu --set full capture
+    (profiles/r1_taylor_traffic.json), scaled to this run's algorithmic bytes (same kernel, same workload family)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_taylor_traffic.json")) as f:
+            t = json.load(f)
+        return float(t["traffic_over_algorithmic"]) * bytes_per_launch, t["report"]
+    except Exception:
+        return None, None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -249,12 +260,14 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         sampler.start()
+        torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off captures exactly the timed steps
         t0 = time.perf_counter()
         ev0.record(stream)
         for _ in range(args.steps):
             d = run.step()
         ev1.record(stream)
         barrier()
+        torch.cuda.cudart().cudaProfilerStop()
         wall = time.perf_counter() - t0
         dev_ms = ev0.elapsed_time(ev1)
         times = run.times()
@@ -280,12 +293,14 @@ def main():
         avg_launch_ms = times["expmv_ms"] / orders
         bytes_per_launch = 12.0 * (times["spmv_nnz"] / orders) + 72.0 * rows
         achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+        traffic, traffic_src = measured_traffic(bytes_per_launch)
         iso_ms, _, _ = run.bench_taylor(orders=20, flush_l2=True, dt=RUN["dt"])
         spmv_ms = run.bench_spmv(reps=20, flush_l2=True)
         roofline = {
-            "kernel": "taylor_order_kernel (y=H_eff x fused with term'=(0,-dt/n) y, c+=term', |term'|^2, |c|^2)",
+            "kernel": "taylor_order_kernel_t (y=H_eff x fused with term'=(0,-dt/n) y, c+=term', |term'|^2, |c|^2; the "
+                      "first order also yields <x|H|x>)",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "peak_source": peak_src,
+            "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
             "launches_timed": int(orders),
             "isolated_l2_flushed": {"ms": iso_ms, "GB/s": (12.0 * nnz + 72.0 * rows) / (iso_ms * 1e-3) / 1e9},
