@@ -168,6 +168,21 @@ int pb200_dipole_amplitude(pb200_ctx* ctx, const uint32_t* words, const double* 
 int pb200_phonon_numbers(pb200_ctx* ctx, const uint32_t* words, const double* coeff, uint64_t rows,
                          double* n_out);
 
+/* weight_histogram (observables.hpp:114-176): descending |c|^2 curve of the non-zero
+ * coefficients, the counts reaching 50 / 90 / 99 / 99.99 % of the total weight, the log-log tail slope, and the
+ * curve sampled at `bins` ranks (0 = every rank).  The O(q log q) sort runs on the GPU; the serial running sums
+ * of the reference are replayed on the host over the sorted weights, so every field equals the reference's bit
+ * for bit.  rank/weight receive min(cap, *npts) points.  pb200_run_weight_histogram works on the resident state. */
+typedef struct {
+    uint64_t support, q50, q90, q99, q9999;
+    double tail_exponent;
+} pb200_weight_hist;
+int pb200_weight_histogram(pb200_ctx* ctx, const double* coeff, uint64_t rows, uint64_t bins,
+                           pb200_weight_hist* out, uint64_t* rank, double* weight, uint64_t cap,
+                           uint64_t* npts);
+int pb200_run_weight_histogram(pb200_ctx* ctx, uint64_t bins, pb200_weight_hist* out, uint64_t* rank,
+                               double* weight, uint64_t cap, uint64_t* npts);
+
 /* ---- device-resident trajectory: initialize / step / run (engine.hpp:235-291, 318-375) ----------
  * pb200_run_begin = initialize(): seed state, grow to m_init, remap.  pb200_run_step advances one
  * timestep exactly as run() does: step 1 evolves on the m_init space (engine.hpp:335-352), steps >= 2

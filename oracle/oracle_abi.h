@@ -130,6 +130,15 @@ int po_dipole_amplitude(const po_model* m, const uint32_t* words, const double* 
 int po_phonon_numbers(const po_model* m, const uint32_t* words, const double* coeff, uint64_t rows,
                       double* n_out);
 
+/* "next" row (observables.hpp:114-176): sorted |c|^2 curve, cumulative-weight quantiles, tail slope.
+ * rank/weight receive min(cap, npts) sampled points; npts = support when bins == 0 or support <= bins. */
+typedef struct {
+    uint64_t support, q50, q90, q99, q9999;
+    double tail_exponent;
+} po_weight_hist;
+int po_weight_histogram(const double* coeff, uint64_t rows, uint64_t bins, po_weight_hist* out,
+                        uint64_t* rank, double* weight, uint64_t cap, uint64_t* npts);
+
 /* ---- stepping (engine.hpp:235-291, 318-375) ---------------------------- */
 /* po_run_begin = initialize(); po_run_step advances one timestep exactly as
  * run() does (step 1 evolves on the m_init space, steps >= 2 call step()). */

@@ -828,6 +828,62 @@ int po_phonon_numbers(const po_model* m, const uint32_t* words, const double* co
     return guarded([&] { phonons(m->m, words, coeff, rows, n_out); });
 }
 
+// weight_histogram, observables.hpp:123-176: descending |c|^2 curve; counts reaching 50/90/99/99.99 % of the total
+// (serial running sum, tolerance 1e-15*total); least-squares slope of log w vs log rank over the last nine
+// deciles; curve sampled at ranks k*(n-1)/(npts-1).
+int po_weight_histogram(const double* coeff, uint64_t rows, uint64_t bins, po_weight_hist* out, uint64_t* rank,
+                        double* weight, uint64_t cap, uint64_t* npts_out) {
+    return guarded([&] {
+        std::vector<double> w;
+        w.reserve(rows);
+        for (uint64_t i = 0; i < rows; ++i) {
+            const double v = coeff[2 * i] * coeff[2 * i] + coeff[2 * i + 1] * coeff[2 * i + 1];  // std::norm
+            if (v > 0) w.push_back(v);
+        }
+        if (w.empty()) throw Fail("weight histogram: empty state");
+        std::sort(w.begin(), w.end(), std::greater<double>());
+        const size_t n = w.size();
+        double total = 0.0;
+        for (double v : w) total += v;
+        uint64_t marks[4] = {n, n, n, n};
+        const double frac[4] = {0.50, 0.90, 0.99, 0.9999};
+        double running = 0;
+        size_t done = 0;
+        for (size_t i = 0; i < n && done < 4; ++i) {
+            running += w[i];
+            while (done < 4 && running >= frac[done] * total - 1e-15 * total) marks[done++] = i + 1;
+        }
+        out->support = n;
+        out->q50 = marks[0];
+        out->q90 = marks[1];
+        out->q99 = marks[2];
+        out->q9999 = marks[3];
+        out->tail_exponent = 0;
+        const size_t lo = n / 10;
+        if (n - lo >= 2) {
+            double sx = 0, sy = 0, sxx = 0, sxy = 0;
+            size_t cnt = 0;
+            for (size_t i = lo; i < n; ++i) {
+                const double x = std::log(double(i + 1)), y = std::log(w[i]);
+                sx += x;
+                sy += y;
+                sxx += x * x;
+                sxy += x * y;
+                ++cnt;
+            }
+            const double denom = cnt * sxx - sx * sx;
+            out->tail_exponent = denom != 0 ? (cnt * sxy - sx * sy) / denom : 0.0;
+        }
+        const size_t npts = (bins == 0 || n <= bins) ? n : size_t(bins);
+        *npts_out = npts;
+        for (size_t k = 0; k < npts && k < cap; ++k) {
+            const size_t i = npts == 1 ? 0 : k * (n - 1) / (npts - 1);
+            rank[k] = i + 1;
+            weight[k] = w[i];
+        }
+    });
+}
+
 // initialize(), engine.hpp:165-251
 int po_run_begin(const po_model* pm, const po_run_cfg* c, po_run** out) {
     return guarded([&] {

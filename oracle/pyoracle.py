@@ -63,6 +63,11 @@ class Diag(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad_"}
 
 
+class WeightHist(C.Structure):
+    _fields_ = [("support", C.c_uint64), ("q50", C.c_uint64), ("q90", C.c_uint64), ("q99", C.c_uint64),
+                ("q9999", C.c_uint64), ("tail_exponent", C.c_double)]
+
+
 class PhaseTimes(C.Structure):
     _fields_ = [
         ("select", C.c_double),
@@ -145,6 +150,8 @@ class Oracle:
         L.po_exciton_density.argtypes = [C.c_void_p, u32p, f64p, C.c_uint64, f64p]
         L.po_dipole_amplitude.argtypes = [C.c_void_p, u32p, f64p, C.c_uint64, f64p]
         L.po_phonon_numbers.argtypes = [C.c_void_p, u32p, f64p, C.c_uint64, f64p]
+        L.po_weight_histogram.argtypes = [f64p, C.c_uint64, C.c_uint64, C.POINTER(WeightHist), u64p, f64p, C.c_uint64,
+                                          u64p]
         L.po_run_begin.argtypes = [C.c_void_p, C.POINTER(RunCfg), C.POINTER(C.c_void_p)]
         L.po_run_step.argtypes = [C.c_void_p, C.POINTER(Diag)]
         L.po_run_info.argtypes = [C.c_void_p, u64p, u64p, f64p, u64p]
@@ -409,6 +416,19 @@ def state_norm(orc: Oracle, coeff):
     out = C.c_double()
     orc.lib.po_state_norm(_p(c.view(np.float64), f64p), c.size, C.byref(out))
     return out.value
+
+
+def weight_histogram(orc: Oracle, coeff, bins=0):
+    """weight_histogram (observables.hpp:123-176) -> dict(support, q50, q90, q99, q9999, tail_exponent, rank, weight)."""
+    c = np.ascontiguousarray(coeff, np.complex128)
+    cap = c.size if bins == 0 else min(c.size, bins)
+    rank, weight = np.zeros(max(cap, 1), np.uint64), np.zeros(max(cap, 1), np.float64)
+    h, npts = WeightHist(), C.c_uint64()
+    orc._ck(orc.lib.po_weight_histogram(_p(c.view(np.float64), f64p), c.size, bins, C.byref(h), _p(rank, u64p),
+                                        _p(weight, f64p), cap, C.byref(npts)))
+    k = min(npts.value, cap)
+    return dict(support=h.support, q50=h.q50, q90=h.q90, q99=h.q99, q9999=h.q9999, tail_exponent=h.tail_exponent,
+                rank=rank[:k].copy(), weight=weight[:k].copy())
 
 
 def fnv1a64(arr: np.ndarray) -> str:

@@ -282,6 +282,27 @@ int po_phonon_numbers(const po_model* m, const uint32_t* words, const double* co
     });
 }
 
+int po_weight_histogram(const double* coeff, uint64_t rows, uint64_t bins, po_weight_hist* out,
+                        uint64_t* rank, double* weight, uint64_t cap, uint64_t* npts) {
+    return guarded([&] {
+        SparseState s;  // weight_histogram only reads the coefficients (observables.hpp:123-129)
+        s.coeff.resize(rows);
+        for (uint64_t i = 0; i < rows; ++i) s.coeff[i] = cplx(coeff[2 * i], coeff[2 * i + 1]);
+        const WeightHistogram h = weight_histogram(s, std::size_t(bins));
+        out->support = h.support;
+        out->q50 = h.q50;
+        out->q90 = h.q90;
+        out->q99 = h.q99;
+        out->q9999 = h.q9999;
+        out->tail_exponent = h.tail_exponent;
+        *npts = h.rank.size();
+        for (uint64_t k = 0; k < h.rank.size() && k < cap; ++k) {
+            rank[k] = h.rank[k];
+            weight[k] = h.weight[k];
+        }
+    });
+}
+
 static RunConfig to_run_config(const po_model* m, const po_run_cfg* c) {
     RunConfig cfg;
     cfg.model = m->spec;

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = [
     "pb200_kernel_launches", "pb200_mix_seed", "pb200_ctx_set_comm", "pb200_owner_of", "pb200_model_set", "pb200_model_info", "pb200_pack", "pb200_unpack",
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
-    "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
+    "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_weight_histogram", "pb200_run_weight_histogram", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
     "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_step_io", "pb200_run_observe", "pb200_run_times",
     "pb200_run_reset_times", "pb200_bench_taylor", "pb200_bench_spmv",
 ]
@@ -62,6 +62,12 @@ class Diag(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad_"}
+
+
+class WeightHist(C.Structure):
+    """WeightHistogram scalars (observables.hpp:115-121)."""
+    _fields_ = [("support", C.c_uint64), ("q50", C.c_uint64), ("q90", C.c_uint64), ("q99", C.c_uint64),
+                ("q9999", C.c_uint64), ("tail_exponent", C.c_double)]
 
 
 class PhaseTimes(C.Structure):
@@ -137,6 +143,9 @@ def load_library():
     L.pb200_exciton_density.argtypes = [vp, u32p, f64p, C.c_uint64, f64p]
     L.pb200_dipole_amplitude.argtypes = [vp, u32p, f64p, C.c_uint64, f64p]
     L.pb200_phonon_numbers.argtypes = [vp, u32p, f64p, C.c_uint64, f64p]
+    L.pb200_weight_histogram.argtypes = [vp, f64p, C.c_uint64, C.c_uint64, C.POINTER(WeightHist), u64p, f64p,
+                                         C.c_uint64, u64p]
+    L.pb200_run_weight_histogram.argtypes = [vp, C.c_uint64, C.POINTER(WeightHist), u64p, f64p, C.c_uint64, u64p]
     L.pb200_run_begin.argtypes = [vp, C.POINTER(RunCfg)]
     L.pb200_run_step.argtypes = [vp, C.POINTER(Diag)]
     L.pb200_run_info.argtypes = [vp, u64p, u64p, f64p, u64p]
@@ -377,6 +386,22 @@ class Context:
         self._ck(self.lib.pb200_phonon_numbers(self.h, _p(w, u32p), _p(cf, f64p), w.shape[0], _p(p, f64p)))
         return p
 
+    @staticmethod
+    def _hist_result(h, rank, weight, npts, cap):
+        k = min(npts.value, cap)
+        return dict(support=h.support, q50=h.q50, q90=h.q90, q99=h.q99, q9999=h.q9999,
+                    tail_exponent=h.tail_exponent, rank=rank[:k].copy(), weight=weight[:k].copy())
+
+    def weight_histogram(self, coeff, bins=0):
+        """weight_histogram (observables.hpp:123-176) of a host coefficient vector."""
+        c, cf = _cview(coeff)
+        cap = c.size if bins == 0 else min(c.size, bins)
+        rank, weight = np.zeros(max(cap, 1), np.uint64), np.zeros(max(cap, 1), np.float64)
+        h, npts = WeightHist(), C.c_uint64()
+        self._ck(self.lib.pb200_weight_histogram(self.h, _p(cf, f64p), c.size, bins, C.byref(h), _p(rank, u64p),
+                                                 _p(weight, f64p), cap, C.byref(npts)))
+        return self._hist_result(h, rank, weight, npts, cap)
+
     def step(self, words, coeff, t, step_index, out_words=None, out_coeff=None, **kw):
         """paces::step on host buffers (engine.hpp:268-291): (new words, new coeff, DiagnosticsRecord dict).
 
@@ -468,6 +493,16 @@ class Run:
                                                     _p(dens, f64p)))
         return dict(norm=s[0].value, energy=s[1].value, rmsd=s[2].value, xbar=s[3].value,
                     amp=complex(amp[0], amp[1]), density=dens)
+
+    def weight_histogram(self, bins=0):
+        """weight_histogram of the resident state (no download of the state)."""
+        rows = self.info()[0]
+        cap = rows if bins == 0 else min(rows, bins)
+        rank, weight = np.zeros(max(cap, 1), np.uint64), np.zeros(max(cap, 1), np.float64)
+        h, npts = WeightHist(), C.c_uint64()
+        self.ctx._ck(self.ctx.lib.pb200_run_weight_histogram(self.ctx.h, bins, C.byref(h), _p(rank, u64p),
+                                                             _p(weight, f64p), cap, C.byref(npts)))
+        return Context._hist_result(h, rank, weight, npts, cap)
 
     def times(self):
         t = PhaseTimes()

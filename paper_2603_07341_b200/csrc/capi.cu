@@ -367,6 +367,28 @@ int pb200_phonon_numbers(pb200_ctx* ctx, const uint32_t* words, const double* co
     });
 }
 
+int pb200_weight_histogram(pb200_ctx* ctx, const double* coeff, uint64_t rows, uint64_t bins, pb200_weight_hist* out,
+                           uint64_t* rank, double* weight, uint64_t cap, uint64_t* npts) {
+    return guarded(ctx, [&](Engine& e) {
+        need(coeff && out, "weight_histogram: null pointer");
+        if (rows == 0) throw PacesError("weight histogram: empty state");
+        if (rows > 0x7fffffffull) throw ArgError("weight_histogram: too many rows");
+        e.aux_coeff.ensure(rows * 16 + 16);
+        PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.stream));
+        e.weight_histogram(e.aux_coeff.as<double2>(), uint32_t(rows), bins, out, rank, weight, cap, npts);
+    });
+}
+
+int pb200_run_weight_histogram(pb200_ctx* ctx, uint64_t bins, pb200_weight_hist* out, uint64_t* rank, double* weight,
+                               uint64_t cap, uint64_t* npts) {
+    return guarded(ctx, [&](Engine& e) {
+        need(out != nullptr, "run_weight_histogram: null pointer");
+        if (!e.has_state) throw ArgError("no resident run: call pb200_run_begin first");
+        if (e.world > 1) throw ArgError("run_weight_histogram: gather the shards first (single-GPU operator)");
+        e.weight_histogram(e.coeff[e.ccur].as<double2>(), e.space[e.cur].n, bins, out, rank, weight, cap, npts);
+    });
+}
+
 // ---- resident trajectory -------------------------------------------------------------------------
 int pb200_run_begin(pb200_ctx* ctx, const pb200_run_cfg* cfg) {
     return guarded(ctx, [&](Engine& e) {

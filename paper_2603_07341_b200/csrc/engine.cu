@@ -1,6 +1,10 @@
 // engine.cu -- implementation of the device-resident paces step (see engine.cuh, kernels.cuh).
 #include "engine.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+
 namespace pb {
 
 #ifdef PB_ONLY_W  // development / profiling builds: one key width, small module, fast compile
@@ -633,6 +637,72 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
             // but the 1/sqrt(L) factor was applied per rank, which is exact for the single non-zero term
             comm_check(ops.allreduce_f64_host(ops.user, amp, 2), "allreduce_f64_host");
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// weight_histogram (observables.hpp:123-176).  Device: |c|^2 and a descending radix sort (CUB -- library code, off
+// the per-step path).  Host: the reference's serial loops over the sorted weights, so the quantile counts, the tail
+// slope (same libm log) and the sampled curve are the reference's bit for bit.
+// ------------------------------------------------------------------------------------------------
+void Engine::weight_histogram(const double2* cvec, uint32_t n, uint64_t bins, pb200_weight_hist* out, uint64_t* rank,
+                              double* weight, uint64_t cap, uint64_t* npts_out) {
+    Ctl* c = dctl();
+    weights.ensure(size_t(n) * 8 + 8);
+    sort_out.ensure(size_t(n) * 8 + 8);
+    PB_CUDA(cudaMemsetAsync(&c->select, 0, sizeof(SelectCtl), stream));
+    weights_kernel<<<grid_for(n), NT, 0, stream>>>(cvec, n, weights.as<double>(), partials.as<double>(), &c->select);
+    check_launch();
+    size_t tmp_bytes = 0;
+    PB_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp_bytes, weights.as<double>(), sort_out.as<double>(),
+                                                     int(n), 0, 64, stream));
+    sort_tmp.ensure(tmp_bytes + 16);
+    PB_CUDA(cub::DeviceRadixSort::SortKeysDescending(sort_tmp.p, tmp_bytes, weights.as<double>(),
+                                                     sort_out.as<double>(), int(n), 0, 64, stream));
+    ++launches;
+    const SelectCtl sc = read_back<SelectCtl>(&c->select);
+    const size_t m = size_t(sc.support);  // weights are >= 0: the positive ones lead the descending order
+    if (m == 0) throw PacesError("weight histogram: empty state");
+    std::vector<double> w(m);
+    PB_CUDA(cudaMemcpyAsync(w.data(), sort_out.p, m * 8, cudaMemcpyDeviceToHost, stream));
+    sync();
+    double total = 0.0;
+    for (double v : w) total += v;
+    uint64_t marks[4] = {m, m, m, m};
+    const double frac[4] = {0.50, 0.90, 0.99, 0.9999};
+    double running = 0;
+    size_t done = 0;
+    for (size_t i = 0; i < m && done < 4; ++i) {
+        running += w[i];
+        while (done < 4 && running >= frac[done] * total - 1e-15 * total) marks[done++] = i + 1;
+    }
+    out->support = m;
+    out->q50 = marks[0];
+    out->q90 = marks[1];
+    out->q99 = marks[2];
+    out->q9999 = marks[3];
+    out->tail_exponent = 0;
+    const size_t lo = m / 10;
+    if (m - lo >= 2) {
+        double sx = 0, sy = 0, sxx = 0, sxy = 0;
+        size_t cnt = 0;
+        for (size_t i = lo; i < m; ++i) {
+            const double x = std::log(double(i + 1)), y = std::log(w[i]);
+            sx += x;
+            sy += y;
+            sxx += x * x;
+            sxy += x * y;
+            ++cnt;
+        }
+        const double denom = cnt * sxx - sx * sx;
+        out->tail_exponent = denom != 0 ? (cnt * sxy - sx * sy) / denom : 0.0;
+    }
+    const size_t npts = (bins == 0 || m <= bins) ? m : size_t(bins);
+    if (npts_out) *npts_out = npts;
+    for (size_t k = 0; k < npts && k < cap; ++k) {
+        const size_t i = npts == 1 ? 0 : k * (m - 1) / (npts - 1);
+        if (rank) rank[k] = i + 1;
+        if (weight) weight[k] = w[i];
     }
 }
 

@@ -153,7 +153,7 @@ struct Engine {
     uint32_t n_seeds = 0;
     DevBuf tab_tmp, frontier[2], cand_keys, cand_gap, perm, seg_rank, gap, scan_tiles;
     DevBuf tmp_col, tmp_val, row_len;
-    DevBuf weights, flag_keep, flag_tie, pos_a, idx_tmp, hist, sel_list;
+    DevBuf weights, flag_keep, flag_tie, pos_a, idx_tmp, hist, sel_list, sort_out, sort_tmp;
     DevBuf term[2], partials, ctl;  // ctl: small device control block
     DevBuf aux_words, aux_coeff, aux2_words, aux2_coeff, aux_vec;  // staging for the host-buffer operators
     DevBuf flush;
@@ -291,6 +291,10 @@ struct Engine {
     void spmv(const Space& sp, const double2* x, double2* y);
     void upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val);
     void observe(const uint32_t* words, const double2* c, uint32_t n, double* density, double* amp, double* phonons);
+
+    /// weight_histogram (observables.hpp:123-176): GPU sort of the weights, reference loops on the host
+    void weight_histogram(const double2* c, uint32_t n, uint64_t bins, pb200_weight_hist* out, uint64_t* rank,
+                          double* weight, uint64_t cap, uint64_t* npts);
 
     // ---- resident trajectory
     void run_begin(const pb200_run_cfg& c);

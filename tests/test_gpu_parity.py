@@ -349,6 +349,32 @@ def test_baseline_configs_against_oracle(gpu, port, name, model, run_kw, steps):
     assert dg["q_true"] > run_kw["q_nom"]
 
 
+def test_weight_histogram_against_oracle(gpu, port):
+    """SURVEY 8f rank 1 (observables.hpp:123-176, test_observables.cpp:170-220): the GPU sorts, the host replays the
+    reference's serial sums -> every field bit-identical, on host vectors and on the resident state."""
+    from oracle import pyoracle
+
+    case = CASES["disordered_L5_d6_optical"]
+    ctx = _ctx(gpu, case["model"])
+    run = ctx.run(**case["run"])
+    for _ in range(12):
+        run.step()
+    _, c = run.state()
+    rng = np.random.default_rng(3)
+    big = (rng.standard_normal(200001) + 1j * rng.standard_normal(200001)) * np.exp(-9 * rng.random(200001))
+    big[::11] = 0
+    for vec, resident in ((c, True), (big, False), (np.array([0, 3 + 4j, 0]), False)):
+        for bins in (0, 1, 2, 50):
+            want = pyoracle.weight_histogram(port, vec, bins)
+            gots = [ctx.weight_histogram(vec, bins)] + ([run.weight_histogram(bins)] if resident else [])
+            for got in gots:
+                for k in want:
+                    same = (got[k].tobytes() == want[k].tobytes()) if hasattr(want[k], "tobytes") else got[k] == want[k]
+                    assert same, (k, bins, got[k], want[k])
+    with pytest.raises(gpu.PacesError, match="empty state"):
+        ctx.weight_histogram(np.zeros(4, np.complex128))
+
+
 def test_checkpoint_resume_roundtrip(gpu, port):
     """download (canonical order = checkpoint order, io.hpp:77-99), reload into a fresh context
     with pb200_run_load_state and continue: identical to the uninterrupted run."""

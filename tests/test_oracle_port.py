@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from cases import CASES
+from oracle import pyoracle
 from oracle.pyoracle import ModelDef, csr_expectation, csr_matvec, expmv, fnv1a64, state_norm
 
 
@@ -150,6 +151,9 @@ def test_port_vs_reference_functions(port, ref, name):
     assert mp.dipole_amplitude(w, c) == mr.dipole_amplitude(w, c)
     if case["model"]["kind"] == 1:
         assert mp.phonon_numbers(w, c).tobytes() == mr.phonon_numbers(w, c).tobytes()
+    for bins in (0, 1, 17):  # weight_histogram, observables.hpp:123-176 (test_observables.cpp:170-220)
+        a, b = pyoracle.weight_histogram(port, c, bins), pyoracle.weight_histogram(ref, c, bins)
+        assert all((a[k].tobytes() == b[k].tobytes()) if hasattr(a[k], "tobytes") else a[k] == b[k] for k in a)
     for q in (1, 7, len(c) // 3, len(c)):
         for seed in (0, 5):
             assert np.array_equal(mp.truncate_select(w, c, q, seed), mr.truncate_select(w, c, q, seed))

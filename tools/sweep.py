@@ -14,11 +14,23 @@ try:
     PEAK = float(json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"])
 except Exception:
     pass
-model = dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16)
-qs = [int(float(x)) for x in (sys.argv[1:] or ["3e4", "3e5", "3e6", "3e7"])]
+MODELS = {  # SURVEY 8d synthetic inputs
+    "c2": (dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+           dict(init="localized", site=-1, m_init=10)),
+    "c3": (dict(kind=1, extents=(6, 6), eps=(0.0,), hop=(-0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+           dict(init="optical", m_init=10)),
+    "c4": (dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+           dict(init="localized", site=-1, m_init=6)),
+}
+args = sys.argv[1:]
+name = "c2"
+if args and args[0] in MODELS:
+    name, args = args[0], args[1:]
+model, init_kw = MODELS[name]
+qs = [int(float(x)) for x in (args or ["3e4", "3e5", "3e6", "3e7"])]
 for q in qs:
     ctx = pb.Context(pb.ModelDef(**model))
-    run = ctx.run(init="localized", site=-1, m_init=10, m=2, q_nom=q, dt=0.05, rtol=1e-15, t_max=100.0, seed=7)
+    run = ctx.run(m=2, q_nom=q, dt=0.05, rtol=1e-15, t_max=100.0, seed=7, **init_kw)
     last = 0
     for s in range(60):
         d = run.step()
@@ -37,7 +49,7 @@ for q in qs:
     rows, nnz, _, _ = run.info()
     t_ms, _, _ = run.bench_taylor(10, True)
     s_ms = run.bench_spmv(10, True)
-    rec = dict(q_nom=q, q_true=rows, nnz=nnz, taylor_order=d["taylor_order"], ms_per_step=1e3 * wall,
+    rec = dict(model=name, words=ctx.words, q_nom=q, q_true=rows, nnz=nnz, taylor_order=d["taylor_order"], ms_per_step=1e3 * wall,
                timesteps_per_s=1.0 / wall,
                phase_ms={kk: tm[kk] / k for kk in ("select_ms", "grow_ms", "assemble_ms", "remap_ms", "expectation_ms", "expmv_ms")},
                taylor_ms=t_ms, taylor_GBs=(12 * nnz + 72 * rows) / t_ms / 1e6, taylor_frac=(12 * nnz + 72 * rows) / t_ms / 1e6 / PEAK,
