@@ -450,7 +450,8 @@ void Engine::remap_async(const uint32_t* src_words, const double2* src_c, uint32
     Ctl* c = dctl();
     PB_CUDA(cudaMemsetAsync(dst_c, 0, size_t(nd) * 16, stream));
     const uint32_t rchunk = chunk_for(ns);
-    const int rgrid = grid_chunked(ns, rchunk);
+    const int rgrid = std::min(grid_chunked(ns, rchunk), sm_count * 8);  // grid_sum partials: <= 8 CTAs per SM
+    if (size_t(rgrid) * 8 > partials.cap) throw CudaFail("internal error: reduction scratch too small for the grid");
     PB_DISPATCH_W(W, remap_window_kernel<W><<<rgrid, NT, 0, stream>>>(src_words, src_c, ns, dst_words, nd, rchunk, dst_c,
                                                                       partials.as<double>(), &c->ticket, c->out));
     check_launch();

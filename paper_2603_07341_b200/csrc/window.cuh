@@ -383,23 +383,29 @@ __global__ void __launch_bounds__(NT) remap_window_kernel(const uint32_t* __rest
     __shared__ double smem[NT / 32];
     uint32_t* win = win_all + (threadIdx.x >> 5) * WinRow<W>::WORDS;
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t wstart = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk;
-    const uint64_t wend = (wstart + 32ull * chunk < uint64_t(ns)) ? wstart + 32ull * chunk : uint64_t(ns);
     double acc[1] = {0.0};
-    uint32_t cursor = CUR_NONE;
-    for (uint64_t b = wstart; b < wend; b += 32) {
-        const uint64_t ii = b + lane;
-        const bool live = ii < ns;
-        const Key<W> k = load_key<W>(src_table + size_t(live ? ii : 0) * W);
-        const double2 x = live ? src_c[ii] : make_double2(0.0, 0.0);
-        uint32_t pos;
-        bool found;
-        warp_window_find<W>(dst_table, nd, win, cursor, k, live, pos, found);
-        if (live) {
-            if (found)
-                dst_c[pos] = x;
-            else
-                acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+    // the grid is bounded (grid_sum's partials are sized for <= 8 CTAs per SM): a warp takes every
+    // (total warps)-th run of 32*chunk consecutive rows and restarts its cursor for each run
+    const uint64_t span = 32ull * chunk;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    for (uint64_t wstart = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * span; wstart < ns;
+         wstart += nwarps * span) {
+        const uint64_t wend = (wstart + span < uint64_t(ns)) ? wstart + span : uint64_t(ns);
+        uint32_t cursor = CUR_NONE;
+        for (uint64_t b = wstart; b < wend; b += 32) {
+            const uint64_t ii = b + lane;
+            const bool live = ii < ns;
+            const Key<W> k = load_key<W>(src_table + size_t(live ? ii : 0) * W);
+            const double2 x = live ? src_c[ii] : make_double2(0.0, 0.0);
+            uint32_t pos;
+            bool found;
+            warp_window_find<W>(dst_table, nd, win, cursor, k, live, pos, found);
+            if (live) {
+                if (found)
+                    dst_c[pos] = x;
+                else
+                    acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+            }
         }
     }
     double tot[1];

@@ -349,6 +349,25 @@ def test_baseline_configs_against_oracle(gpu, port, name, model, run_kw, steps):
     assert dg["q_true"] > run_kw["q_nom"]
 
 
+def test_scale_beyond_reduction_grid(gpu):
+    """Regression (round 1): above ~3.9e7 rows the remap kernel's grid outgrew the reduction scratch and corrupted
+    the state.  BASELINE config 2 at q_nom = 1.5e7 (q_true ~ 4.5e7) must keep evolving sanely once truncation binds:
+    Taylor order in the low tens, norm conserved, q_true/q_nom near the measured kappa ~ 3.3-3.7."""
+    model = dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16)
+    ctx = _ctx(gpu, model)
+    run = ctx.run(init="localized", site=-1, m_init=10, m=2, q_nom=15_000_000, dt=0.05, rtol=1e-15, t_max=50.0, seed=7)
+    bound = 0
+    for s in range(1, 14):
+        d = run.step()
+        assert 10 <= d["taylor_order"] <= 40, (s, d)
+        assert abs(d["norm_post"] - 1.0) < 1e-9 and abs(d["delta_norm_expmv"]) < 1e-12, (s, d)
+        if d["discarded_weight"] > 0 and d["q_true"] > 39_000_000:
+            bound += 1
+            assert 2.5 * 15_000_000 < d["q_true"] < 4.5 * 15_000_000, (s, d)
+    assert bound >= 2
+    ctx.close()
+
+
 def test_weight_histogram_against_oracle(gpu, port):
     """SURVEY 8f rank 1 (observables.hpp:123-176, test_observables.cpp:170-220): the GPU sorts, the host replays the
     reference's serial sums -> every field bit-identical, on host vectors and on the resident state."""
