@@ -167,6 +167,24 @@ void Engine::set_model(const HostModel& m) {
         d_omega_n.ensure(tab.size() * 8);
         PB_CUDA(cudaMemcpy(d_omega_n.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
         md.omega_n = d_omega_n.as<double>();
+        // exact uniform-omega shortcut of the diagonal (see ModelDev::diag_uniform)
+        bool uniform = nph > 0 && m.bp > 0;
+        for (size_t s2 = 0; s2 < L && uniform; ++s2) uniform = (m.eps[s2] == 0.0);
+        const double w0 = nph > 0 ? om[0] : 0.0;
+        for (int j = 0; j < nph && uniform; ++j) uniform = (om[size_t(j)] == w0);
+        uniform = uniform && w0 == std::floor(w0) && std::fabs(w0) * double(nph) * double(per) < 9.0e15;
+        std::vector<uint32_t> masks(std::max<size_t>(1, size_t(m.bp) * m.W), 0u);
+        for (int j = 0; j < nph; ++j)
+            for (int b = 0; b < m.bp; ++b) {
+                // bit b (value 2^b) of register j sits at bit offset b0 + j*bp + (bp-1-b) from the top of word 0
+                const int off = m.b0 + j * m.bp + (m.bp - 1 - b);
+                masks[size_t(b) * m.W + size_t(off >> 5)] |= 1u << (31 - (off & 31));
+            }
+        d_diag_masks.ensure(masks.size() * 4);
+        PB_CUDA(cudaMemcpy(d_diag_masks.p, masks.data(), masks.size() * 4, cudaMemcpyHostToDevice));
+        md.diag_masks = d_diag_masks.as<uint32_t>();
+        md.diag_uniform = uniform ? 1 : 0;
+        md.omega_u = w0;
     }
     row_width = max_deg + (m.kind == 1 ? 2 : 0) + 1;
     has_model = true;

@@ -130,7 +130,7 @@ struct Engine {
     bool has_model = false;
     HostModel hm;
     ModelDev md{};
-    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n;
+    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n, d_diag_masks;
     int row_width = 1;  // max entries of an H_eff row for this model
 
     // resident trajectory

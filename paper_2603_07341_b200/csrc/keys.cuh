@@ -33,6 +33,12 @@ struct ModelDev {
     const int* nb_site;    // [L*MAX_NB] hop partners sorted ascending, -1 padded; zero-amplitude bonds removed
     const double* nb_amp;  // [L*MAX_NB] bond amplitude J
     const double* omega_n;  // [nph << bp] omega[j] * double(n), the product the diagonal sums (same IEEE multiply)
+    // exact shortcut for the diagonal: when eps == 0 everywhere and every omega[j] is the same integer-valued w,
+    // sum_j w*n_j is a sum of small integers -- exact in ANY order -- so it equals w * (total phonon number), and
+    // the total is sum_b 2^b * popcount(key & mask_b) with mask_b = bit b of every phonon register.
+    int diag_uniform;            // 1: shortcut valid
+    double omega_u;              // the common omega
+    const uint32_t* diag_masks;  // [bp * W] multi-word masks, bit plane b at diag_masks + b*W
     int wfirst[17];        // wfirst[w] = first phonon register whose leading bit lies in key word >= w (nph past the end)
 };
 
@@ -196,6 +202,16 @@ __device__ __forceinline__ uint32_t owner_of(const ModelDev& m, const Key<W>& k,
 /// Registers with n_j == 0 contribute +0.0 and are skipped; whole zero words are skipped at once.
 template <int W>
 __device__ __forceinline__ double diagonal_element(const ModelDev& m, const Key<W>& k, uint32_t e) {
+    if (m.diag_uniform) {
+        uint32_t total = 0;
+        for (int b = 0; b < m.bp; ++b) {
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) cnt += __popc(k.w[i] & __ldg(m.diag_masks + b * W + i));
+            total += cnt << b;
+        }
+        return __dmul_rn(m.omega_u, double(total));  // exact: integers below 2^53
+    }
     double diag = 0.0;
     const double ee = __ldg(m.eps + e);
     if (ee != 0.0) diag = __dadd_rn(diag, ee);

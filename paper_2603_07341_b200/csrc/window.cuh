@@ -5,9 +5,9 @@
 // identity for remap) and asks where the resulting keys sit in a sorted table.  The move adds a fixed multi-word
 // constant to keys that share the exciton site, so the 32 queries are ascending and their answers lie in a
 // window of the table only a little longer than 32 rows -- and the next 32 rows of the same warp continue where
-// this window ended.  So the warp keeps ONE cursor per move (a merge join), loads table[cursor, cursor + 64) into
-// its shared-memory window with coalesced loads, and each lane finishes with a 6-step binary search in shared
-// memory.  No per-lane chains of dependent global loads, no divergence inside the search, and global traffic is
+// this window ended.  So the warp keeps ONE cursor per move (a merge join), copies table[cursor, cursor + 64) into
+// its shared-memory window with coalesced asynchronous copies (LDGSTS), and each lane finishes with a 7-step binary
+// search in shared memory that compares only the last few words -- 64 consecutive sorted rows share the rest.  No per-lane chains of dependent global loads, no divergence inside the search, and global traffic is
 // one pass over the target range per move.
 //
 // Replaces the find_row calls (basis_codec.hpp:334-348) inside apply_to_rows/diff_rows (subspace.hpp:102-134,
@@ -21,41 +21,58 @@ namespace pb {
 constexpr int WIN_ROWS = 64;  // table rows per window
 constexpr unsigned FULL = 0xffffffffu;
 
-/// Window rows are padded to a multiple of 4 words so a row is read with 128-bit shared-memory loads.
+/// A window holds 64 consecutive table rows, unpadded (row r at win[r*W]).
 template <int W>
 struct WinRow {
-    static constexpr int WS = (W + 3) & ~3;
-    static constexpr int WORDS = WIN_ROWS * WS;  // per-warp window size in words
+    static constexpr int WORDS = WIN_ROWS * W;  // per-warp window size in words
 };
 
-template <int W>
-__device__ __forceinline__ void win_load_row(const uint32_t* row, uint32_t (&v)[WinRow<W>::WS]) {
-    const uint4* p = reinterpret_cast<const uint4*>(row);
+/// Asynchronous 4-byte global -> shared copy (LDGSTS): the issuing lane does not wait for the data.
+__device__ __forceinline__ void cp_async_u32(uint32_t* smem_dst, const uint32_t* gmem_src) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+/// Lower bound + equality of q among the cnt rows of a window whose rows all share their first W-S words
+/// (64 consecutive sorted rows of a large table differ only in their last few words): q is compared with that
+/// common prefix once, and the binary search then looks at the last S words only.
+template <int W, int S>
+__device__ __forceinline__ void win_search(const uint32_t* win, uint32_t cnt, const Key<W>& q, uint32_t& lo_out,
+                                           bool& eq_out) {
+    int c = 0;  // q's prefix vs the window's common prefix: -1 / 0 / +1
 #pragma unroll
-    for (int c = 0; c < WinRow<W>::WS / 4; ++c) {
-        const uint4 x = p[c];
-        v[4 * c] = x.x, v[4 * c + 1] = x.y, v[4 * c + 2] = x.z, v[4 * c + 3] = x.w;
+    for (int i = W - S - 1; i >= 0; --i) {
+        const uint32_t v = win[i];
+        if (q.w[i] != v) c = (q.w[i] < v) ? -1 : 1;
     }
-}
-
-template <int W>
-__device__ __forceinline__ bool win_row_less(const uint32_t* row, const Key<W>& k) {
-    uint32_t v[WinRow<W>::WS];
-    win_load_row<W>(row, v);
-    bool lt = false;
+    if (c != 0) {  // q sorts before / after every row of the window
+        lo_out = c < 0 ? 0u : cnt;
+        eq_out = false;
+        return;
+    }
+    uint32_t lo = 0, len = cnt;
+    while (len > 0) {
+        const uint32_t half = len >> 1;
+        const uint32_t mid = lo + half;
+        const uint32_t* r = win + mid * W + (W - S);
+        bool lt = false;
 #pragma unroll
-    for (int i = W - 1; i >= 0; --i) lt = (v[i] < k.w[i]) || (v[i] == k.w[i] && lt);
-    return lt;
-}
-
-template <int W>
-__device__ __forceinline__ bool win_row_equal(const uint32_t* row, const Key<W>& k) {
-    uint32_t v[WinRow<W>::WS];
-    win_load_row<W>(row, v);
-    bool eq = true;
+        for (int j = S - 1; j >= 0; --j) {
+            const uint32_t v = r[j], qq = q.w[W - S + j];
+            lt = (v < qq) || (v == qq && lt);
+        }
+        lo = lt ? mid + 1 : lo;
+        len = lt ? len - half - 1 : half;
+    }
+    bool eq = lo < cnt;
+    if (eq) {
+        const uint32_t* r = win + lo * W + (W - S);
 #pragma unroll
-    for (int i = 0; i < W; ++i) eq = eq && (v[i] == k.w[i]);
-    return eq;
+        for (int j = 0; j < S; ++j) eq = eq && (r[j] == q.w[W - S + j]);
+    }
+    lo_out = lo;
+    eq_out = eq;
 }
 
 /// Lower bound of k in table[0, n) by one warp: every round probes 32 rows, so a search from scratch takes
@@ -116,7 +133,6 @@ template <int W>
 __device__ __forceinline__ void warp_window_find(const uint32_t* __restrict__ table, uint32_t n, uint32_t* win,
                                                  uint32_t& cursor, const Key<W>& q, bool valid, uint32_t& pos,
                                                  bool& found) {
-    constexpr int WS = WinRow<W>::WS;
     const uint32_t lane = threadIdx.x & 31;
     const unsigned need = __ballot_sync(FULL, valid);
     pos = n;
@@ -129,23 +145,33 @@ __device__ __forceinline__ void warp_window_find(const uint32_t* __restrict__ ta
     for (;;) {
         const uint32_t cnt = min(uint32_t(WIN_ROWS), n - c);
         const uint32_t* src = table + size_t(c) * W;
-        for (uint32_t w = lane; w < cnt * W; w += 32) {
-            const uint32_t row = w / W;
-            win[row * WS + (w - row * W)] = __ldg(src + w);
-        }
+        for (uint32_t w = lane; w < cnt * W; w += 32) cp_async_u32(win + w, src + w);
+        cp_async_wait_all();
         __syncwarp();
+        // words that differ between the first and the last row of the window: only the suffix from the first
+        // such word on can differ between ANY two rows of it (the rows are sorted)
+        uint32_t differs = 0;
+        if (cnt > 1) {
+            const bool ne = (lane < uint32_t(W)) && (win[lane] != win[(cnt - 1) * W + lane]);
+            differs = __ballot_sync(FULL, ne);
+        }
+        const int suffix = differs ? W - (__ffs(differs) - 1) : 1;  // words the search has to look at (>= 1)
         if (open) {
-            uint32_t lo = 0, len = cnt;
-            while (len > 0) {
-                const uint32_t half = len >> 1;
-                const uint32_t mid = lo + half;
-                const bool lt = win_row_less<W>(win + mid * WS, q);
-                lo = lt ? mid + 1 : lo;
-                len = lt ? len - half - 1 : half;
-            }
+            uint32_t lo;
+            bool eq;
+            if (suffix <= 1)
+                win_search<W, 1>(win, cnt, q, lo, eq);
+            else if (W >= 2 && suffix <= 2)
+                win_search<W, (W >= 2 ? 2 : 1)>(win, cnt, q, lo, eq);
+            else if (W >= 3 && suffix <= 3)
+                win_search<W, (W >= 3 ? 3 : 1)>(win, cnt, q, lo, eq);
+            else if (W >= 4 && suffix <= 4)
+                win_search<W, (W >= 4 ? 4 : 1)>(win, cnt, q, lo, eq);
+            else
+                win_search<W, W>(win, cnt, q, lo, eq);
             if (lo < cnt || c + cnt >= n) {
                 pos = c + lo;
-                found = lo < cnt && win_row_equal<W>(win + lo * WS, q);
+                found = eq;
                 open = false;
             }
         }
@@ -221,7 +247,7 @@ __global__ void __launch_bounds__(NT) expand_window_kernel(ModelDev m, const uin
                                                            uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
                                                            uint32_t* __restrict__ gap_count, GrowCounters* ctr,
                                                            int count_emitted) {
-    __shared__ __align__(16) uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
+    __shared__ uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
     __shared__ uint32_t cur_all[NT / 32][N_MOVES];
     uint32_t* win = win_all + (threadIdx.x >> 5) * WinRow<W>::WORDS;
     uint32_t* cur = cur_all[threadIdx.x >> 5];
@@ -301,7 +327,7 @@ __global__ void __launch_bounds__(NT) assemble_window_kernel(ModelDev m, const u
                                                              uint32_t chunk, int width, uint32_t* __restrict__ tmp_col,
                                                              double* __restrict__ tmp_val,
                                                              uint32_t* __restrict__ row_len) {
-    __shared__ __align__(16) uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
+    __shared__ uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
     __shared__ uint32_t cur_all[NT / 32][N_MOVES];
     uint32_t* win = win_all + (threadIdx.x >> 5) * WinRow<W>::WORDS;
     uint32_t* cur = cur_all[threadIdx.x >> 5];
@@ -379,7 +405,7 @@ __global__ void __launch_bounds__(NT) remap_window_kernel(const uint32_t* __rest
                                                           uint32_t chunk, double2* __restrict__ dst_c,
                                                           double* __restrict__ partials, unsigned* ticket,
                                                           double* __restrict__ out) {
-    __shared__ __align__(16) uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
+    __shared__ uint32_t win_all[(NT / 32) * WinRow<W>::WORDS];
     __shared__ double smem[NT / 32];
     uint32_t* win = win_all + (threadIdx.x >> 5) * WinRow<W>::WORDS;
     const uint32_t lane = threadIdx.x & 31;
