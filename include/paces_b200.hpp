@@ -250,6 +250,29 @@ inline std::vector<double> phonon_numbers(const Device& dev, const SparseState& 
     return n;
 }
 
+/// weight_histogram (observables.hpp:123-176): the GPU sorts the weights, the serial sums are replayed on the host,
+/// so every field equals the reference's.
+inline WeightHistogram weight_histogram(const Device& dev, const SparseState& state, std::size_t bins = 0) {
+    const std::size_t cap = (bins == 0) ? state.coeff.size() : std::min<std::size_t>(bins, state.coeff.size());
+    std::vector<std::uint64_t> rank(std::max<std::size_t>(cap, 1));
+    std::vector<double> weight(std::max<std::size_t>(cap, 1));
+    pb200_weight_hist h{};
+    std::uint64_t npts = 0;
+    dev.check(pb200_weight_histogram(dev.get(), detail::reim(state.coeff), state.coeff.size(), bins, &h, rank.data(),
+                                     weight.data(), cap, &npts));
+    WeightHistogram out;
+    out.support = h.support;
+    out.q50 = h.q50;
+    out.q90 = h.q90;
+    out.q99 = h.q99;
+    out.q9999 = h.q9999;
+    out.tail_exponent = h.tail_exponent;
+    const std::size_t k = std::min<std::size_t>(npts, cap);
+    out.rank.assign(rank.begin(), rank.begin() + k);
+    out.weight.assign(weight.begin(), weight.begin() + k);
+    return out;
+}
+
 // ---- initialize / step / run -------------------------------------------------------------------------------------
 
 inline std::pair<SparseState, EffectiveSpace> initialize(const Device& dev, const RunConfig& config,
@@ -306,9 +329,27 @@ inline RunResult run(const RunConfig& config, const HamiltonianTermSet& terms, i
         return row;
     };
     auto histogram = [&]() {
-        // weight_histogram (observables.hpp:123-176) stays host post-processing of a downloaded state
-        auto [st, sp] = detail::download(dev, terms, config.m, config.q_nom);
-        result.histograms.emplace_back(st.t, weight_histogram(st, config.histogram_bins));
+        // weight_histogram (observables.hpp:123-176) of the resident state: sorted on the GPU, no state download
+        std::uint64_t rows = 0, npts = 0;
+        double t_now = 0;
+        dev.check(pb200_run_info(dev.get(), &rows, nullptr, &t_now, nullptr));
+        const std::size_t bins = config.histogram_bins;
+        const std::size_t cap = (bins == 0) ? rows : std::min<std::size_t>(bins, rows);
+        std::vector<std::uint64_t> rank(std::max<std::size_t>(cap, 1));
+        std::vector<double> weight(std::max<std::size_t>(cap, 1));
+        pb200_weight_hist h{};
+        dev.check(pb200_run_weight_histogram(dev.get(), bins, &h, rank.data(), weight.data(), cap, &npts));
+        WeightHistogram wh;
+        wh.support = h.support;
+        wh.q50 = h.q50;
+        wh.q90 = h.q90;
+        wh.q99 = h.q99;
+        wh.q9999 = h.q9999;
+        wh.tail_exponent = h.tail_exponent;
+        const std::size_t k = std::min<std::size_t>(npts, cap);
+        wh.rank.assign(rank.begin(), rank.begin() + k);
+        wh.weight.assign(weight.begin(), weight.begin() + k);
+        result.histograms.emplace_back(t_now, std::move(wh));
     };
     result.trajectory.push_back(observe());
     if (config.emit_histograms) histogram();

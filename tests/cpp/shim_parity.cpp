@@ -77,6 +77,14 @@ static void compare_runs(const char* name, const RunConfig& cfg) {
         for (std::size_t k = 0; k < std::min(x.density.size(), y.density.size()); ++k)
             CHECK(close(x.density[k], y.density[k], 1e-10, 1e-18), "%s: density %zu/%zu", name, i, k);
     }
+    CHECK(a.histograms.size() == b.histograms.size(), "%s: histogram count", name);
+    for (std::size_t i = 0; i < std::min(a.histograms.size(), b.histograms.size()); ++i) {
+        const auto &x = a.histograms[i].second, &y = b.histograms[i].second;
+        CHECK(close(a.histograms[i].first, b.histograms[i].first, 1e-14) && x.support == y.support && x.q50 == y.q50 &&
+                  x.q90 == y.q90 && x.q99 == y.q99 && x.q9999 == y.q9999 && x.tail_exponent == y.tail_exponent &&
+                  x.rank == y.rank && x.weight == y.weight,
+              "%s: weight histogram %zu", name, i);
+    }
     CHECK(same_bits(a.final_state.table->words, b.final_state.table->words), "%s: final table", name);
     CHECK(same_bits(a.final_state.coeff, b.final_state.coeff), "%s: final coefficients not bit-identical", name);
     CHECK(a.final_state.t == b.final_state.t, "%s: final t", name);
@@ -136,6 +144,13 @@ static void compare_functions() {
     CHECK(std::abs(dipole_amplitude(psi, terms) - b200::dipole_amplitude(dev, psi, terms)) <= 1e-12, "dipole");
     auto pn = phonon_numbers(psi, terms), gpn = b200::phonon_numbers(dev, psi, terms);
     for (std::size_t k = 0; k < pn.size(); ++k) CHECK(close(pn[k], gpn[k], 1e-10, 1e-18), "phonon numbers %zu", k);
+    {  // weight_histogram (observables.hpp:123-176; test_observables.cpp:170-220): every field identical
+        const WeightHistogram wh = weight_histogram(psi, 16), gwh = b200::weight_histogram(dev, psi, 16);
+        CHECK(wh.support == gwh.support && wh.q50 == gwh.q50 && wh.q90 == gwh.q90 && wh.q99 == gwh.q99 &&
+                  wh.q9999 == gwh.q9999 && wh.tail_exponent == gwh.tail_exponent && wh.rank == gwh.rank &&
+                  wh.weight == gwh.weight,
+              "weight_histogram");
+    }
     // error text parity (test_propagator.cpp:157-169, test_subspace.cpp preconditions)
     PropagatorConfig bad = cfg.propagator;
     bad.dt = 50.0;
@@ -165,6 +180,8 @@ int main() {
         compare_runs("cadence 3 + substeps 2", [] {
             RunConfig c = holstein({4}, 4, 1.3, 0.8, 60, 1.0, InitialStateSpec::Kind::localized);
             c.cadence = 3;
+            c.emit_histograms = true;  // RunResult.histograms from the resident state (engine.hpp:329-330, 365-366)
+            c.histogram_bins = 32;
             c.propagator.substeps = 2;
             c.propagator.dt = 0.1;
             c.m_init = 3;
