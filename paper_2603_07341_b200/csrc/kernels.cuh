@@ -145,18 +145,37 @@ constexpr int MAX_ROW = 2 * 3 + 3;  // hops (<= 6) + 2 ladder + diagonal
 
 // Pass 1 (assemble_window_kernel) lives in window.cuh.
 
-/// Pass 2: compact the fixed-width scratch into CSR (row_ptr from the scan of row_len).
+/// Pass 2: compact the fixed-width scratch into CSR (row_ptr from the scan of row_len).  A warp takes 32
+/// consecutive rows: their entries form ONE contiguous run of the CSR arrays, so the lanes write it with
+/// coalesced stores; the source row of an entry is found by a 5-step search over the 32 row offsets held in
+/// registers (shuffles).
 __global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int width, const uint32_t* __restrict__ tmp_col,
                                                               const double* __restrict__ tmp_val,
                                                               const uint32_t* __restrict__ row_ptr,
                                                               int32_t* __restrict__ col, double* __restrict__ val) {
-    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
-        const uint32_t b = row_ptr[i], e = row_ptr[i + 1];
-        const uint32_t* tc = tmp_col + size_t(i) * width;
-        const double* tv = tmp_val + size_t(i) * width;
-        for (uint32_t k = b; k < e; ++k) {
-            col[k] = int32_t(tc[k - b]);
-            val[k] = tv[k - b];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    for (uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        const uint32_t rp = __ldg(row_ptr + (i < n ? i : n));  // rows past the end are empty
+        const uint32_t rp0 = __shfl_sync(0xffffffffu, rp, 0);
+        const uint32_t end = __ldg(row_ptr + (base + 32 < n ? base + 32 : n));
+        const uint32_t total = end - rp0;
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint32_t target = rp0 + (k < total ? k : total - 1);
+            uint32_t r = 0;  // last row whose offset is <= target
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, rp, (r + step) & 31);
+                if (v <= target) r += step;
+            }
+            const uint32_t off = target - __shfl_sync(0xffffffffu, rp, r);
+            if (k < total) {
+                const size_t src = size_t(base + r) * width + off;
+                col[target] = int32_t(__ldg(tmp_col + src));
+                val[target] = __ldg(tmp_val + src);
+            }
         }
     }
 }
