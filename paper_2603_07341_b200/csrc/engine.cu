@@ -552,18 +552,27 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
             const int end = std::min(max_order, order + batch - 1);
             for (; order <= end; ++order) {
                 const double b = -dt_sub / double(order);
-                if (fuse_expectation && s == 0 && order == 1)
+                if (fuse_expectation && s == 0 && order == 1) {
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
-                    // (Ctl::out[1..3], read with the final read-back)
-                    taylor_order_kernel_t<true><<<g, NT, 0, stream>>>(
+                    // (Ctl::out[1..3], read with the final read-back).  This variant needs more registers: size
+                    // its grid to what is resident so the launch is a single wave.
+                    static int per_sm = 0;
+                    if (per_sm == 0 &&
+                        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taylor_order_kernel_t<true>, NT, 0) !=
+                             cudaSuccess ||
+                         per_sm < 1))
+                        per_sm = 4;
+                    const int g1 = std::min(g, sm_count * per_sm);
+                    taylor_order_kernel_t<true><<<g1, NT, 0, stream>>>(
                         n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
                         term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
                         partials.as<double>(), &c->taylor, 0, nullptr, c->out + 1);
-                else
+                } else {
                     taylor_order_kernel_t<false><<<g, NT, 0, stream>>>(
                         n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
                         term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
                         partials.as<double>(), &c->taylor, 0, nullptr, nullptr);
+                }
                 check_launch();
             }
             last_ctl = read_back<Ctl>(c);  // one read-back carries the stop flag AND the step's deferred scalars
