@@ -306,6 +306,9 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
         GrowCounters gc{};
         const uint32_t n_new = merge_level(out, n, cand_cap, fcur, true, &gc);
         if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
+        if (std::getenv("PB200_DEBUG_GROW"))
+            std::fprintf(stderr, "[grow] level %d: n=%u nf=%u candidates=%u new=%u longest gap segment=%u\n", k, n, nf,
+                         gc.n_cand, n_new, gc.max_seg);
         emitted_total += gc.emitted;
         identity_frontier = false;
         n += n_new;

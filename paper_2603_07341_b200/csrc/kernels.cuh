@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __res
         const uint32_t s0 = seg_start[g], s1 = seg_start[g + 1];
         const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
         bool dup = false;
-        for (uint32_t t = s0; t < s && !dup; ++t)
-            dup = key_equal<W>(load_key<W>(cand_keys + size_t(perm[t]) * W), k);
+        // early-exit compares: two different candidates of one gap usually differ within the first words read
+        for (uint32_t t = s0; t < s && !dup; ++t) dup = row_cmp<W>(cand_keys + size_t(perm[t]) * W, k) == 0;
         seg_rank[s] = dup ? SEG_DUP : 0u;
         if (!dup) atomicAdd(gap_kept + g, 1u);
         if (s == s0 && s1 - s0 > 32) atomicMax(&ctr->max_seg, s1 - s0);
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __rest
         uint32_t rank = 0;
         for (uint32_t t = s0; t < s1; ++t) {
             if (t == s || seg_rank[t] == SEG_DUP) continue;
-            if (key_cmp<W>(load_key<W>(cand_keys + size_t(perm[t]) * W), k) < 0) ++rank;
+            if (row_cmp<W>(cand_keys + size_t(perm[t]) * W, k) < 0) ++rank;
         }
         seg_rank[s] = rank;
     }

@@ -5,9 +5,18 @@ import paper_2603_07341_b200 as pb
 q = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1000000
 spin = int(sys.argv[2]) if len(sys.argv) > 2 else 9
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-model = dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16)
+name = sys.argv[4] if len(sys.argv) > 4 else "c2"
+MODELS = {
+    "c2": (dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+           dict(init="localized", site=-1, m_init=10)),
+    "c3": (dict(kind=1, extents=(6, 6), eps=(0.0,), hop=(-0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+           dict(init="optical", m_init=10)),
+    "c4": (dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+           dict(init="localized", site=-1, m_init=6)),
+}
+model, init_kw = MODELS[name]
 ctx = pb.Context(pb.ModelDef(**model))
-run = ctx.run(init="localized", site=-1, m_init=10, m=2, q_nom=q, dt=0.05, rtol=1e-15, t_max=50.0, seed=7)
+run = ctx.run(m=2, q_nom=q, dt=0.05, rtol=1e-15, t_max=50.0, seed=7, **init_kw)
 import torch
 for s in range(spin):
     run.step()
