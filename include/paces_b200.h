@@ -221,6 +221,13 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
 int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd, double* xbar,
                       double* amp, double* density);
 int pb200_run_times(const pb200_ctx* ctx, pb200_phase_times* out);
+/* How the resident steps grew their subspace: steps taken by the incremental adapt path (old-index-space BFS over
+ * the previous H_eff, incremental.cuh), steps that fell back to the full expansion, and how much key-based work the
+ * incremental steps still needed (old rows re-expanded, keys that entered from outside the previous table). */
+typedef struct {
+    uint64_t incremental_steps, fallbacks, expanded_rows, side_keys;
+} pb200_adapt_stats;
+int pb200_run_adapt_stats(const pb200_ctx* ctx, pb200_adapt_stats* out);
 int pb200_run_reset_times(pb200_ctx* ctx);
 
 /* ---- measurement helpers (bench.py) -----------------------------------------------------------

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_weight_histogram", "pb200_run_weight_histogram", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
-    "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_step_io", "pb200_run_observe", "pb200_run_times",
+    "pb200_run_state", "pb200_run_global", "pb200_run_csr", "pb200_run_load_state", "pb200_step", "pb200_step_io", "pb200_run_observe", "pb200_run_times", "pb200_run_adapt_stats",
     "pb200_run_reset_times", "pb200_bench_taylor", "pb200_bench_spmv",
 ]
 
@@ -68,6 +68,11 @@ class WeightHist(C.Structure):
     """WeightHistogram scalars (observables.hpp:115-121)."""
     _fields_ = [("support", C.c_uint64), ("q50", C.c_uint64), ("q90", C.c_uint64), ("q99", C.c_uint64),
                 ("q9999", C.c_uint64), ("tail_exponent", C.c_double)]
+
+
+class AdaptStats(C.Structure):
+    _fields_ = [("incremental_steps", C.c_uint64), ("fallbacks", C.c_uint64), ("expanded_rows", C.c_uint64),
+                ("side_keys", C.c_uint64)]
 
 
 class PhaseTimes(C.Structure):
@@ -159,6 +164,7 @@ def load_library():
                                 C.c_uint64, C.POINTER(Diag), u64p, u64p]
     L.pb200_run_observe.argtypes = [vp, f64p, f64p, f64p, f64p, f64p, f64p]
     L.pb200_run_times.argtypes = [vp, C.POINTER(PhaseTimes)]
+    L.pb200_run_adapt_stats.argtypes = [vp, C.POINTER(AdaptStats)]
     L.pb200_run_reset_times.argtypes = [vp]
     L.pb200_bench_taylor.argtypes = [vp, C.c_int, C.c_int, C.c_double, f64p, u64p, u64p]
     L.pb200_bench_spmv.argtypes = [vp, C.c_int, C.c_int, f64p]
@@ -508,6 +514,12 @@ class Run:
         t = PhaseTimes()
         self.ctx.lib.pb200_run_times(self.ctx.h, C.byref(t))
         return t.as_dict()
+
+    def adapt_stats(self):
+        """How the resident steps grew their subspace (pb200_run_adapt_stats)."""
+        st = AdaptStats()
+        self.ctx._ck(self.ctx.lib.pb200_run_adapt_stats(self.ctx.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in st._fields_}
 
     def reset_times(self):
         self.ctx.lib.pb200_run_reset_times(self.ctx.h)

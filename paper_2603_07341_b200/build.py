@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpaces_b200.so")
 SOURCES = ["paces_b200.cu"]
-DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "keys.cuh",
+DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "incremental.cu", "keys.cuh",
         "primitives.cuh",
         "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",

@@ -217,6 +217,7 @@ int pb200_grow(pb200_ctx* ctx, const uint32_t* seeds, uint64_t rows, int order, 
         e.has_state = false;  // the resident state no longer matches the current space
         Space& sp = e.space[e.cur];
         sp.has_h = false;
+        sp.has_full = false;
         e.grow(e.aux_words.as<uint32_t>(), uint32_t(rows), order, sp);
         e.sync();
         if (q_true) *q_true = sp.n;
@@ -494,6 +495,7 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
         sp.n = uint32_t(rows);
         sp.nnz = 0;
         sp.has_h = false;
+        sp.has_full = false;
         // engine.hpp:110: the caller's table must be sorted -- checked on the device copy (one streaming kernel)
         if (!e.rows_sorted_on_device(sp.words.as<uint32_t>(), sp.n))
             throw PacesError("truncate_select: state table must be sorted");
@@ -540,6 +542,7 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         sp.n = uint32_t(rows);
         sp.nnz = 0;
         sp.has_h = false;
+        sp.has_full = false;
         e.t = t;
         e.steps_done = step_index - 1;
         e.has_state = true;
@@ -627,6 +630,16 @@ int pb200_run_observe(pb200_ctx* ctx, double* norm, double* energy, double* rmsd
 int pb200_run_times(const pb200_ctx* ctx, pb200_phase_times* out) {
     if (!ctx || !out) return PB200_ERR_ARG;
     *out = ctx->eng.times;
+    return PB200_OK;
+}
+
+int pb200_run_adapt_stats(const pb200_ctx* ctx, pb200_adapt_stats* out) {
+    if (!ctx || !out) return PB200_ERR_ARG;
+    const Engine& e = ctx->eng;
+    out->incremental_steps = e.inc_steps;
+    out->fallbacks = e.inc_fallbacks;
+    out->expanded_rows = e.inc_expanded_total;
+    out->side_keys = e.inc_side_keys_total;
     return PB200_OK;
 }
 

@@ -192,6 +192,7 @@ void Engine::set_model(const HostModel& m) {
     has_cfg = false;
     space[0].n = space[1].n = 0;
     space[0].has_h = space[1].has_h = false;
+    space[0].has_full = space[1].has_full = false;
     if (m.W > 16) throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build");
 }
 
@@ -200,8 +201,9 @@ void Engine::set_model(const HostModel& m) {
 // scatter that writes the merged sorted table plus the next (sorted) frontier.  Expects gap[] (n+2 counters)
 // filled by the expansion kernel; the new frontier ends up in frontier[fcur] (fcur is flipped).
 // ------------------------------------------------------------------------------------------------
-uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcur, bool deferred,
-                             GrowCounters* counters) {
+/// Counting sort of the candidates by insertion gap, exact dedup + rank inside each gap segment, and the scan of
+/// the survivor counts: afterwards row_len[g] = unique new keys in gaps < g, row_len[n+1] = their total.
+void Engine::dedup_candidates_async(uint32_t n, uint32_t nc_bound) {
     const int W = md.W;
     Ctl* c = dctl();
     const uint32_t* nc_ptr = &c->grow.n_cand;  // exact candidate count, on the device
@@ -227,6 +229,20 @@ uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcu
     check_launch();
     // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
     exclusive_scan(row_len.as<uint32_t>(), uint64_t(n) + 2);
+}
+
+uint32_t Engine::dedup_candidates(uint32_t n, uint32_t nc_bound) {
+    dedup_candidates_async(n, nc_bound);
+    return read_back<uint32_t>(row_len.as<uint32_t>() + (size_t(n) + 1));
+}
+
+uint32_t Engine::merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcur, bool deferred,
+                             GrowCounters* counters) {
+    const int W = md.W;
+    Ctl* c = dctl();
+    const uint32_t* nc_ptr = &c->grow.n_cand;  // exact candidate count, on the device
+    const int gc_grid = grid_for(nc_bound);
+    dedup_candidates_async(n, nc_bound);
     uint32_t n_new = 0;
     uint64_t rows_bound;
     if (deferred) {
@@ -283,7 +299,8 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
     uint64_t emitted_total = 0;
     Ctl* c = dctl();
 
-    for (int k = 0; k < order && nf > 0; ++k) {
+    int levels_done = 0;
+    for (int k = 0; k < order && nf > 0; ++k, ++levels_done) {
         const uint64_t cand_cap64 = uint64_t(nf) * uint64_t(nmoves);
         if (cand_cap64 == 0) {
             nf = 0;
@@ -318,6 +335,14 @@ void Engine::grow(const uint32_t* d_seeds, uint32_t ns, int order, Space& out) {
     out.n = n;
     out.q_nom = ns;
     out.order = order;
+    // which rows had their neighbourhood generated: all but the last frontier (incremental.cuh needs it next step)
+    out.full.ensure(size_t(n) + 1);
+    PB_CUDA(cudaMemsetAsync(out.full.p, order == 0 ? 0 : 1, n, stream));
+    if (order > 0 && levels_done == order && nf > 0 && !identity_frontier) {
+        inc_clear_full_kernel<<<grid_for(nf), NT, 0, stream>>>(frontier[fcur].as<uint32_t>(), nf, out.full.as<uint8_t>());
+        check_launch();
+    }
+    out.has_full = true;
     PB_CUDA(cudaEventRecord(ev[2], stream));
     assemble(out);
 }
@@ -364,7 +389,7 @@ void Engine::assemble(Space& sp) {
 // truncate_select (engine.hpp:107-156)
 // ------------------------------------------------------------------------------------------------
 uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
-                        double* norm2_out) {
+                        double* norm2_out, bool compact) {
     require_model();
     if (q_nom < 1) throw PacesError("truncate_select: q_nom must be >= 1");
     const int W = md.W;
@@ -444,6 +469,15 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
             sync();  // `ties` must outlive the copy
         }
     }
+    const uint32_t kept = uint32_t(kept64);  // = popcount of keep[]: support when nothing is cut, else q_nom
+    if (compact) compact_kept(d_words, n, kept);
+    return kept;
+}
+
+void Engine::compact_kept(const uint32_t* d_words, uint32_t n, uint32_t kept) {
+    const int W = md.W;
+    const int g = grid_for(n);
+    uint32_t* keep = flag_keep.as<uint32_t>();
     pos_a.ensure((size_t(n) + 1) * 4);
     PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
     exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
@@ -453,13 +487,11 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         pending_words = false;
         if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
     }
-    const uint32_t kept = uint32_t(kept64);  // = popcount of keep[]: support when nothing is cut, else q_nom
     seeds.ensure(size_t(kept) * W * 4 + 4);
     PB_DISPATCH_W(W, compact_rows_kernel<W><<<g, NT, 0, stream>>>(d_words, keep, pos_a.as<uint32_t>(), n,
                                                                   seeds.as<uint32_t>()));
     check_launch();
     n_seeds = kept;
-    return kept;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -854,16 +886,29 @@ void Engine::run_step(pb200_diag* out) {
             ~DeferGuard() { flag = false; }
         } defer_guard{defer_reads};
         defer_reads = (world == 1);
+        // incremental adapt (incremental.cuh): needs the previous H_eff with its expansion flags; the full path
+        // remains for the first step after a load, m = 0, a memory cap (its transcript accounting) and overflows
+        bool incremental = world == 1 && !io && old.has_h && old.has_full && cfg.m >= 1 && memory_cap_bytes() == 0 &&
+                           std::getenv("PB200_NO_INCREMENTAL") == nullptr;
         const uint32_t kept = world > 1
                                   ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
-                                  : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre);
+                                  : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
+                                           !incremental);
         rec.norm_pre = std::sqrt(n2_pre);
         PB_CUDA(cudaEventRecord(ev[1], stream));
-        // grow() = expansion + assembly; split the timer inside via ev[2]
-        if (world > 1)
+        if (incremental && !grow_incremental(old, c_old, kept, cfg.m, next, coeff[ccur ^ 1])) {
+            incremental = false;
+            ++inc_fallbacks;
+            compact_kept(old.words.as<uint32_t>(), old.n, kept);
+        }
+        if (incremental) {
+            PB_CUDA(cudaEventRecord(ev[2], stream));
+        } else if (world > 1) {
+            // grow() = expansion + assembly; split the timer inside via ev[2]
             grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
-        else
+        } else {
             grow(seeds.as<uint32_t>(), kept, cfg.m, next);
+        }
         PB_CUDA(cudaEventRecord(ev[3], stream));
         if (io) {
             // the new table is final: ship it to the host beside remap + <H> + expmv
@@ -879,7 +924,9 @@ void Engine::run_step(pb200_diag* out) {
         double2* psi = coeff[ccur ^ 1].as<double2>();
         double e = 0, n2 = 0;
         if (defer_reads) {
-            remap_async(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+            // the incremental path already produced psi and the discarded weight (Ctl::out[0])
+            if (!incremental)
+                remap_async(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
             PB_CUDA(cudaEventRecord(ev[4], stream));
             PB_CUDA(cudaEventRecord(ev[5], stream));  // <H> is produced by the first Taylor order
         } else {

@@ -14,6 +14,7 @@
 #include "host_model.hpp"
 #include "kernels.cuh"
 #include "window.cuh"
+#include "incremental.cuh"
 #include "sharded.cuh"
 
 namespace pb {
@@ -111,6 +112,8 @@ struct Space {
     uint64_t q_nom = 0;
     int order = 0;
     bool has_h = false;
+    DevBuf full;  // uint8[n]: 1 = the row's whole neighbourhood is in the table (it was expanded), 0 = final frontier
+    bool has_full = false;
     // sharded runs: columns >= n index the halo (values received from other ranks every SpMV)
     uint32_t halo_n = 0;
     uint32_t send_total = 0;
@@ -272,10 +275,21 @@ struct Engine {
     /// the scatter is queued; the counters of the expansion come back through *counters.
     uint32_t merge_level(Space& out, uint32_t n, uint32_t nc_bound, int& fcur, bool deferred = false,
                          GrowCounters* counters = nullptr);
+    void dedup_candidates_async(uint32_t n, uint32_t nc_bound);
+    uint32_t dedup_candidates(uint32_t n, uint32_t nc_bound);  // returns the number of unique new keys
     void assemble(Space& sp);
     /// returns kept count; result in this->seeds
     uint32_t select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
-                    double* norm2_out);
+                    double* norm2_out, bool compact = true);
+    /// gathers the rows flagged in flag_keep into this->seeds (second half of select)
+    void compact_kept(const uint32_t* d_words, uint32_t n, uint32_t kept);
+    /// Incremental adapt (incremental.cuh): grows `next` from the previous space and the keep flags of select(),
+    /// remaps the coefficients into c_new (discarded weight -> Ctl::out[0]).  Returns false when it had to bail out
+    /// (a buffer bound was hit): the caller then runs the full path.
+    bool grow_incremental(const Space& old, const double2* c_old, uint32_t kept, int m, Space& next, DevBuf& c_new);
+    DevBuf inc_dist, inc_elist, inc_side_keys[2], inc_side_gap[2], inc_side_dist[2], inc_new_keys, inc_new_gap,
+        inc_newidx, inc_side_newidx, inc_s_col, inc_s_val, inc_s_len, inc_xcnt, inc_ctr;
+    uint64_t inc_steps = 0, inc_fallbacks = 0, inc_side_keys_total = 0, inc_expanded_total = 0;
     double remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
                  uint32_t nd, double2* dst_c);
     /// launches only: the discarded weight lands in Ctl::out[0]

@@ -368,6 +368,48 @@ def test_scale_beyond_reduction_grid(gpu):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,model,run_kw,steps", [
+    ("1d_L16", dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+     dict(init="localized", site=-1, m_init=8, m=2, q_nom=30000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 25),
+    ("2d_4x3_disordered_m3", dict(kind=1, extents=(4, 3), eps=tuple(0.05 * i - 0.2 for i in range(12)), hop=(0.55,),
+                                 omega=tuple(1.0 + 0.01 * i for i in range(12)), g=(0.71,), d_pho=7),
+     dict(init="optical", m_init=4, m=3, q_nom=3000, dt=0.05, rtol=1e-15, t_max=5.0, seed=3), 20),
+    ("3d_4x4x4_m1", dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+     dict(init="localized", site=-1, m_init=5, m=1, q_nom=8000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 15),
+    ("tb_chain", dict(kind=0, extents=(61,), eps=(0.0,), hop=(1.0,)),
+     dict(init="localized", site=-1, m_init=3, m=2, q_nom=9, dt=0.05, rtol=1e-15, t_max=5.0, seed=1), 30),
+])
+def test_incremental_adapt_equals_full_expansion(gpu, monkeypatch, name, model, run_kw, steps):
+    """The incremental adapt phase (BFS over the previous H_eff in old index space, incremental.cuh) against the full
+    expansion (PB200_NO_INCREMENTAL=1), step by step: tables, CSR and coefficients bit-identical, same diagnostics.
+    The incremental run must really have taken the incremental path, including steps that needed key-based
+    re-expansion of previous-frontier rows and keys from outside the previous table."""
+    monkeypatch.delenv("PB200_NO_INCREMENTAL", raising=False)
+    ri = _ctx(gpu, model).run(**run_kw)
+    monkeypatch.setenv("PB200_NO_INCREMENTAL", "1")
+    rf = _ctx(gpu, model).run(**run_kw)
+    for s in range(1, steps + 1):
+        monkeypatch.delenv("PB200_NO_INCREMENTAL", raising=False)
+        di = ri.step()
+        monkeypatch.setenv("PB200_NO_INCREMENTAL", "1")
+        df = rf.step()
+        assert di["q_true"] == df["q_true"] and di["taylor_order"] == df["taylor_order"], (name, s, di, df)
+        for k in ("norm_pre", "norm_post", "energy", "discarded_weight"):
+            assert _close(di[k], df[k], 1e-12, 1e-30), (name, s, k, di[k], df[k])
+        wi, ci = ri.state()
+        wf, cf = rf.state()
+        assert np.array_equal(wi, wf), (name, s)
+        assert ci.tobytes() == cf.tobytes(), (name, s)
+        if s % 5 == 0 or s == steps:
+            assert all(a.tobytes() == b.tobytes() for a, b in zip(ri.csr(), rf.csr())), (name, s)
+    si, sf = ri.adapt_stats(), rf.adapt_stats()
+    assert sf["incremental_steps"] == 0
+    # step 1 only evolves; while the space is still exploding (more new keys than old rows) a step may fall back
+    assert si["incremental_steps"] + si["fallbacks"] == steps - 1 and si["incremental_steps"] >= (steps - 1) // 2, si
+    if name != "tb_chain":
+        assert si["expanded_rows"] > 0 and si["side_keys"] > 0, si
+
+
 def test_weight_histogram_against_oracle(gpu, port):
     """SURVEY 8f rank 1 (observables.hpp:123-176, test_observables.cpp:170-220): the GPU sorts, the host replays the
     reference's serial sums -> every field bit-identical, on host vectors and on the resident state."""
