@@ -56,40 +56,41 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     for (auto& b : inc_side_gap) b.ensure(64);
     for (auto& b : inc_side_dist) b.ensure(64);
 
+    // candidate capacity: what the buffers already hold (the full path sized them for whole BFS levels), at least a
+    // quarter of the table's moves; running out of it only sends this step to the full path
+    {
+        const uint64_t want = std::max<uint64_t>(uint64_t(n / 4 + 1024) * uint64_t(nmoves), 1u << 16);
+        cand_keys.ensure(size_t(want) * W * 4);
+        cand_gap.ensure(size_t(want) * 4);
+    }
+    const uint32_t cand_cap =
+        uint32_t(std::min<uint64_t>({cand_keys.cap / (size_t(W) * 4), cand_gap.cap / 4, 0x7ffffff0ull}));
+    gap.ensure((size_t(n) + 2) * 4);
     for (int k = 0; k < m; ++k) {
         PB_CUDA(cudaMemsetAsync(&ictr->n_expand, 0, 4, stream));
         inc_mark_level_kernel<<<grid_for(n), NT, 0, stream>>>(n, k, old.full.as<uint8_t>(), old.row_ptr.as<uint32_t>(),
                                                                old.col.as<int32_t>(), dist, inc_elist.as<uint32_t>(),
                                                                ictr);
         check_launch();
-        const IncCounters ic = read_back<IncCounters>(ictr);
-        const uint64_t total = uint64_t(ic.n_expand) + side_n;
-        inc_expanded_total += ic.n_expand;
-        if (total == 0) continue;
-        const uint64_t cand_cap64 = total * uint64_t(nmoves);
-        if (cand_cap64 == 0) continue;
-        if (cand_cap64 > 0x7ffffff0ull) return false;
-        const uint32_t cand_cap = uint32_t(cand_cap64);
-        cand_keys.ensure(size_t(cand_cap) * W * 4);
-        cand_gap.ensure(size_t(cand_cap) * 4);
-        gap.ensure((size_t(n) + 2) * 4);
+        if (nmoves == 0) continue;
         PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
         PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
-        PB_DISPATCH_WI(W, inc_expand_kernel<W><<<grid_for(total), NT, 0, stream>>>(
-                              md, old.words.as<uint32_t>(), n, inc_elist.as<uint32_t>(), ic.n_expand,
+        PB_DISPATCH_WI(W, inc_expand_kernel<W><<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
+                              md, old.words.as<uint32_t>(), n, inc_elist.as<uint32_t>(), &ictr->n_expand,
                               inc_side_keys[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), side_n, k, dist,
                               cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow,
                               ictr));
         check_launch();
-        const GrowCounters gc = read_back<GrowCounters>(&c->grow);
-        if (gc.n_cand == 0) continue;
-        // unique new keys of this level, canonical order (the dedup machinery of the full path)
-        const uint32_t n_new = dedup_candidates(n, gc.n_cand);
+        inc_clamp_kernel<<<1, 1, 0, stream>>>(&c->grow.n_cand, cand_cap);
+        check_launch();
+        // unique new keys of this level, canonical order (the dedup machinery of the full path, on the device-side
+        // candidate count); ONE read-back per level
+        const uint32_t n_new = dedup_candidates(n, cand_cap);
         if (n_new == 0) continue;
         if (uint64_t(side_n) + n_new > side_cap) return false;
         inc_new_keys.ensure(size_t(n_new) * W * 4 + 4);
         inc_new_gap.ensure(size_t(n_new) * 4 + 4);
-        PB_DISPATCH_WI(W, inc_emit_unique_kernel<W><<<grid_for(gc.n_cand), NT, 0, stream>>>(
+        PB_DISPATCH_WI(W, inc_emit_unique_kernel<W><<<grid_for(cand_cap), NT, 0, stream>>>(
                               cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
                               seg_rank.as<uint32_t>(), &c->grow.n_cand, row_len.as<uint32_t>(),
                               inc_new_keys.as<uint32_t>(), inc_new_gap.as<uint32_t>()));
@@ -107,10 +108,6 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         scur ^= 1;
         side_n = merged;
     }
-    {
-        const IncCounters ic = read_back<IncCounters>(ictr);
-        if (ic.overflow) return false;
-    }
 
     // ---- index maps: pk = kept old rows before i, nb = side keys before row i
     pos_a.ensure((size_t(n) + 2) * 4);
@@ -125,7 +122,12 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         check_launch();
     }
     exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
-    const uint32_t n_keep = read_back<uint32_t>(pos_a.as<uint32_t>() + n);
+    // one read-back: overflow flag, statistics and the number of surviving old rows
+    PB_CUDA(cudaMemcpyAsync(&ictr->n_keep, pos_a.as<uint32_t>() + n, 4, cudaMemcpyDeviceToDevice, stream));
+    const IncCounters fin = read_back<IncCounters>(ictr);
+    if (fin.overflow) return false;
+    inc_expanded_total += fin.expanded_total;
+    const uint32_t n_keep = fin.n_keep;
     const uint64_t n_new64 = uint64_t(n_keep) + side_n;
     if (n_new64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     const uint32_t n_new = uint32_t(n_new64);

@@ -23,9 +23,10 @@ constexpr uint8_t DIST_INF = 255;
 constexpr uint32_t IDX_NONE = 0xffffffffu;
 
 struct IncCounters {
-    uint32_t n_expand;   // old rows at the current distance whose neighbourhood must be generated
-    uint32_t overflow;   // a side / candidate buffer was too small: the step falls back to the full path
-    uint32_t pad[2];
+    uint32_t n_expand;        // old rows at the current distance whose neighbourhood must be generated
+    uint32_t overflow;        // a side / candidate buffer was too small: the step falls back to the full path
+    uint32_t expanded_total;  // sum of n_expand over the levels of this step (statistics)
+    uint32_t n_keep;          // old rows that survive (copied from the prefix sum for the final read-back)
 };
 
 /// dist[i] = 0 for kept rows, INF otherwise.
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(NT) inc_mark_level_kernel(uint32_t n, int k, c
             }
         } else {
             elist[append_slot(&ctr->n_expand)] = i;
+            atomicAdd(&ctr->expanded_total, 1u);
         }
     }
 }
@@ -66,13 +68,15 @@ __device__ __forceinline__ bool side_find(const uint32_t* __restrict__ side_keys
 /// anything else becomes a candidate with its insertion gap in the OLD table (gap_count feeds the dedup machinery).
 template <int W>
 __global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
-                                                        const uint32_t* __restrict__ elist, uint32_t n_elist,
+                                                        const uint32_t* __restrict__ elist,
+                                                        const uint32_t* __restrict__ n_elist_ptr,
                                                         const uint32_t* __restrict__ side_keys,
                                                         const uint8_t* __restrict__ side_dist, uint32_t side_n, int k,
                                                         uint8_t* dist, uint32_t* __restrict__ cand_keys,
                                                         uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
                                                         uint32_t* __restrict__ gap_count, GrowCounters* gctr,
                                                         IncCounters* ictr) {
+    const uint32_t n_elist = *n_elist_ptr;  // stays on the device: no host round trip between mark and expand
     const uint32_t total = n_elist + side_n;
     for (uint32_t t = blockIdx.x * NT + threadIdx.x; t < total; t += gridDim.x * NT) {
         Key<W> key;
@@ -99,6 +103,12 @@ __global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const uint32
             }
         });
     }
+}
+
+/// After an overflowing expansion the candidate counter exceeds the buffer: clamp it so the dedup kernels stay in
+/// bounds (the step is discarded anyway -- IncCounters::overflow is set).
+__global__ void inc_clamp_kernel(uint32_t* n_cand, uint32_t cap) {
+    if (*n_cand > cap) *n_cand = cap;
 }
 
 /// Unique candidates of one level in canonical order: survivor of gap g with rank r -> index kept_before[g] + r.
