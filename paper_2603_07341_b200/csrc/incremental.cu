@@ -170,9 +170,11 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         check_launch();
     }
     next.row_ptr.ensure((size_t(n_new) + 1) * 4);
+    inc_simple.ensure(size_t(n) + 4);
     inc_row_len_kernel<<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
         n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), inc_xcnt.as<uint32_t>(),
-        inc_side_newidx.as<uint32_t>(), inc_s_len.as<uint32_t>(), side_n, next.row_ptr.as<uint32_t>());
+        inc_side_newidx.as<uint32_t>(), inc_s_len.as<uint32_t>(), side_n, next.row_ptr.as<uint32_t>(),
+        inc_simple.as<uint8_t>());
     check_launch();
     PB_CUDA(cudaMemsetAsync(next.row_ptr.as<uint32_t>() + n_new, 0, 4, stream));
     exclusive_scan(next.row_ptr.as<uint32_t>(), uint64_t(n_new) + 1);
@@ -183,7 +185,11 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), old.val.as<double>(), width,
         tmp_col.as<uint32_t>(), tmp_val.as<double>(), inc_xcnt.as<uint32_t>(), inc_side_newidx.as<uint32_t>(),
         inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), inc_s_len.as<uint32_t>(), side_n,
-        next.row_ptr.as<uint32_t>(), next.col.as<int32_t>(), next.val.as<double>());
+        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>());
+    check_launch();
+    inc_fill_simple_kernel<<<grid_for(n), NT, 0, stream>>>(
+        n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), old.val.as<double>(),
+        inc_simple.as<uint8_t>(), next.row_ptr.as<uint32_t>(), next.col.as<int32_t>(), next.val.as<double>());
     check_launch();
     next.n = n_new;
     next.nnz = 0;  // arrives with the step's final read-back (Ctl::nnz)

@@ -274,15 +274,21 @@ __global__ void __launch_bounds__(NT) inc_row_len_kernel(uint32_t n, const uint3
                                                          const uint32_t* __restrict__ x_cnt,
                                                          const uint32_t* __restrict__ side_newidx,
                                                          const uint32_t* __restrict__ s_len, uint32_t side_n,
-                                                         uint32_t* __restrict__ len_new) {
+                                                         uint32_t* __restrict__ len_new, uint8_t* __restrict__ simple) {
     for (uint32_t t = blockIdx.x * NT + threadIdx.x; t < n + side_n; t += gridDim.x * NT) {
         if (t < n) {
             const uint32_t o = newidx[t];
-            if (o == IDX_NONE) continue;
-            uint32_t len = x_cnt[t];
+            if (o == IDX_NONE) {
+                simple[t] = 0;
+                continue;
+            }
+            const uint32_t nx = x_cnt[t];
+            uint32_t len = nx;
             const uint32_t kb = __ldg(row_ptr + t), ke = __ldg(row_ptr + t + 1);
             for (uint32_t e = kb; e < ke; ++e) len += (newidx[uint32_t(__ldg(col + e))] != IDX_NONE) ? 1u : 0u;
             len_new[o] = len;
+            // simple: the row keeps every entry and gains none -> its entries are a straight copy with renumbering
+            simple[t] = (nx == 0 && len == ke - kb) ? 1 : 0;
         } else {
             len_new[side_newidx[t - n]] = s_len[t - n];
         }
@@ -302,8 +308,10 @@ __global__ void __launch_bounds__(NT) inc_fill_kernel(uint32_t n, const uint32_t
                                                       const double* __restrict__ s_val,
                                                       const uint32_t* __restrict__ s_len, uint32_t side_n,
                                                       const uint32_t* __restrict__ row_ptr_new,
+                                                      const uint8_t* __restrict__ simple,
                                                       int32_t* __restrict__ col_new, double* __restrict__ val_new) {
     for (uint32_t t = blockIdx.x * NT + threadIdx.x; t < n + side_n; t += gridDim.x * NT) {
+        if (t < n && simple[t]) continue;  // copied by inc_fill_simple_kernel
         if (t >= n) {
             const uint32_t j = t - n;
             uint32_t w = row_ptr_new[side_newidx[j]];
@@ -360,6 +368,50 @@ __global__ void __launch_bounds__(NT) inc_fill_kernel(uint32_t n, const uint32_t
         for (; xi < nx; ++xi, ++w) {
             col_new[w] = int32_t(xc[xi]);
             val_new[w] = xv[xi];
+        }
+    }
+}
+
+/// The common case of inc_fill -- rows that keep all their entries and gain none -- as a coalesced copy: a warp
+/// takes 32 consecutive OLD rows, whose entries are one contiguous run of CSR_old; every lane moves entries of that
+/// run (the source row of an entry is found by a 5-step search over the 32 row offsets, as in
+/// assemble_compact_kernel), renumbering the column through the index map.
+__global__ void __launch_bounds__(NT) inc_fill_simple_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
+                                                             const uint32_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const double* __restrict__ val,
+                                                             const uint8_t* __restrict__ simple,
+                                                             const uint32_t* __restrict__ row_ptr_new,
+                                                             int32_t* __restrict__ col_new,
+                                                             double* __restrict__ val_new) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    for (uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        const bool in = i < n;
+        const uint32_t rp = __ldg(row_ptr + (in ? i : n));
+        const bool smp = in && simple[i];
+        const uint32_t dst0 = smp ? row_ptr_new[newidx[i]] : 0u;  // new offset of the row's first entry
+        const unsigned smask = __ballot_sync(0xffffffffu, smp);
+        const uint32_t rp0 = __shfl_sync(0xffffffffu, rp, 0);
+        const uint32_t end = __ldg(row_ptr + (base + 32 < n ? base + 32 : n));
+        const uint32_t total = end - rp0;
+        if (smask == 0) continue;
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint32_t e = rp0 + (k < total ? k : total - 1);
+            uint32_t r = 0;  // last row whose offset is <= e
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, rp, (r + step) & 31);
+                if (v <= e) r += step;
+            }
+            const uint32_t off = e - __shfl_sync(0xffffffffu, rp, r);
+            const uint32_t d0 = __shfl_sync(0xffffffffu, dst0, r);
+            if (k < total && ((smask >> r) & 1u)) {
+                col_new[d0 + off] = int32_t(newidx[uint32_t(__ldg(col + e))]);
+                val_new[d0 + off] = __ldg(val + e);
+            }
         }
     }
 }
