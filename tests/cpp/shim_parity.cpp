@@ -8,6 +8,7 @@
 #include <string>
 
 #include "paces/engine.hpp"
+#include "paces/spectra.hpp"
 
 #include "paces_b200.hpp"
 
@@ -162,9 +163,42 @@ static void compare_functions() {
     std::printf("functions                    fails so far=%d\n", g_fail);
 }
 
+// BASELINE config 3 end to end at a size the CPU finishes quickly: 2D aggregate, optical start, the autocorrelation
+// <mu(t) mu(0)> (ObservablesRow.amp) of the GPU trajectory goes through the reference's own damp_signal + transform
+// (spectra.hpp:42-88, as tools/paces.cpp:106-109 does) and must give the reference's absorption spectrum.
+static void compare_spectrum() {
+    RunConfig cfg = holstein({4, 4}, 6, 0.71, -0.55, 1500, 6.0, InitialStateSpec::Kind::optical);
+    cfg.m_init = 4;
+    const HamiltonianTermSet terms = build_model(cfg.model);
+    const RunResult a = run(cfg, terms), b = b200::run(cfg, terms);
+    CHECK(a.error.empty() && b.error.empty() && a.trajectory.size() == b.trajectory.size(), "spectrum: runs");
+    SpectrumConfig sc;
+    sc.tau = 1.0 / 0.0577;
+    sc.pad_factor = 4;
+    sc.omega_min = -5.0;
+    sc.omega_max = 5.0;
+    std::vector<SignalSample> sa, sb;
+    for (const auto& r : a.trajectory) sa.push_back({r.t, r.amp});
+    for (const auto& r : b.trajectory) sb.push_back({r.t, r.amp});
+    damp_signal(sa, sc.tau);
+    damp_signal(sb, sc.tau);
+    const auto pa = transform(sa, sc), pb = transform(sb, sc);
+    CHECK(pa.size() == pb.size() && pa.size() > 10, "spectrum: bins");
+    double amax = 0, dmax = 0;
+    for (std::size_t k = 0; k < std::min(pa.size(), pb.size()); ++k) {
+        amax = std::max(amax, std::fabs(pa[k].a));
+        dmax = std::max(dmax, std::fabs(pa[k].a - pb[k].a));
+        CHECK(pa[k].omega == pb[k].omega, "spectrum: grid %zu", k);
+    }
+    CHECK(dmax <= 1e-10 * amax, "spectrum: max |dA| = %.3e of peak %.3e", dmax, amax);
+    std::printf("absorption spectrum (cfg 3)  bins=%zu peak=%.6f max|dA|=%.2e fails so far=%d\n", pa.size(), amax, dmax,
+                g_fail);
+}
+
 int main() {
     try {
         compare_functions();
+        compare_spectrum();
         compare_runs("holstein 1D L=4 d=8 (cfg 1)", [] {
             RunConfig c = holstein({4}, 8, 1.0, 1.0, 2000, 2.0, InitialStateSpec::Kind::localized);
             c.m_init = 6;

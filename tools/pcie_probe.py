@@ -27,3 +27,28 @@ for _ in range(10):
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 print("duplex GB/s per direction", 10 * n / dt / 1e9)
+# two concurrent H2D copies on two streams: does the aggregate beat one stream?
+for nstreams in (1, 2, 4):
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    hs = [torch.empty(n // nstreams, dtype=torch.uint8).pin_memory() for _ in range(nstreams)]
+    ds = [torch.empty(n // nstreams, dtype=torch.uint8, device="cuda") for _ in range(nstreams)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        for s, hh, dd in zip(streams, hs, ds):
+            with torch.cuda.stream(s):
+                dd.copy_(hh, non_blocking=True)
+    torch.cuda.synchronize()
+    print("h2d", nstreams, "streams GB/s", 10 * n / (time.perf_counter() - t0) / 1e9)
+for nstreams in (1, 2):
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    hs = [torch.empty(n // nstreams, dtype=torch.uint8).pin_memory() for _ in range(nstreams)]
+    ds = [torch.empty(n // nstreams, dtype=torch.uint8, device="cuda") for _ in range(nstreams)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        for s, hh, dd in zip(streams, hs, ds):
+            with torch.cuda.stream(s):
+                hh.copy_(dd, non_blocking=True)
+    torch.cuda.synchronize()
+    print("d2h", nstreams, "streams GB/s", 10 * n / (time.perf_counter() - t0) / 1e9)
