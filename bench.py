@@ -271,6 +271,7 @@ def main():
         wall = time.perf_counter() - t0
         dev_ms = ev0.elapsed_time(ev1)
         times = run.times()
+        adapt = run.adapt_stats() if world == 1 else None
         launches = ctx.kernel_launches - launches0
         t_ms = torch.tensor([dev_ms], dtype=torch.float64)  # CPU tensor: gloo carries the scalar reductions
         if world > 1:
@@ -396,7 +397,8 @@ def main():
                        "parallelism": "single GPU" if world == 1 else
                        f"state and subspace sharded over {world} GPUs by hash of the basis key (phonon part); "
                        "NCCL all-to-all of candidate keys / look-ups / halos",
-                       "l2": "per-step working set (~150 B/row x q_true ~ 0.5 GB) exceeds the 126 MB L2; no flush"},
+                       "l2": "per-step working set (~150 B/row x q_true ~ 0.5 GB) exceeds the 126 MB L2; no flush",
+                       "adapt": adapt},
             "spmv_nnz_per_sec": spmv_rate,
             "wall_ms_per_step": 1e3 * wall / args.steps,
             "phase_ms_per_step": {k: times[k] / args.steps for k in
