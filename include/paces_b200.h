@@ -212,7 +212,12 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
 /* Same operator with the transfers overlapped with the step: the key upload runs beside the weight/selection
  * kernels (which only need the coefficients), the download of the new table runs beside remap + <H> + expmv, and only
  * the new coefficients cross PCIe after the last Taylor order.  out_words/out_coeff must hold out_cap_rows rows
- * (pinned host memory for full PCIe speed); fails with PB200_ERR_ARG if the new state has more rows. */
+ * (pinned host memory for full PCIe speed); fails with PB200_ERR_ARG if the new state has more rows.
+ * The context keeps its last result resident.  When a call is the next step of that result (same step index, time
+ * and run parameters), the uploaded coefficients and keys are compared on the device with the resident ones -- on
+ * their own stream, beside the step -- and, when they are bit-identical, the step works on the resident table and
+ * H_eff (the caller's EffectiveSpace, engine.hpp:268) and takes the incremental adapt path; nothing is committed
+ * before both comparisons agree.  Any difference, and the step is redone from the caller's buffers. */
 int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
                   const double* coeff, uint64_t rows, double t, uint32_t* out_words, double* out_coeff,
                   uint64_t out_cap_rows, pb200_diag* out, uint64_t* rows_out, uint64_t* nnz_out);

@@ -434,6 +434,12 @@ class Context:
         self._ck(self.lib.pb200_run_state(self.h, _p(ow, u32p), _p(oc.view(np.float64), f64p)))
         return ow, oc, d.as_dict()
 
+    def adapt_stats(self):
+        """How the steps of this context grew their subspace (pb200_run_adapt_stats)."""
+        st = AdaptStats()
+        self._ck(self.lib.pb200_run_adapt_stats(self.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in st._fields_}
+
     # ---- resident trajectory -------------------------------------------------------------------
     def run(self, **kw) -> "Run":
         """initialize() (engine.hpp:235-251); returns the resident run."""

@@ -523,11 +523,79 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         c.n_entries = 0;
         c.entry_occ = nullptr;
         c.entry_amp = nullptr;
+        const size_t W = e.hm.W;
+        Engine::StepIO io;
+        io.out_words = out_words;
+        io.out_coeff = out_coeff;
+        io.out_cap_rows = out_cap_rows;
+        struct Guard {
+            Engine& e;
+            ~Guard() {
+                e.io = nullptr;
+                e.pending_words = false;
+                cudaStreamSynchronize(e.copy_stream);  // never leave a transfer into caller memory in flight
+                cudaStreamSynchronize(e.io_stream);
+            }
+        } guard{e};
+
+        // ---- Is this the state the context produced last?  Same step, same time, same run parameters and (checked on
+        // the device, bit for bit) the same coefficients and keys: then the resident table, H_eff and expansion flags
+        // are exactly the caller's EffectiveSpace and the step takes the incremental adapt path.  Everything is still
+        // uploaded -- the comparison needs it -- but the keys no longer sit on the critical path: their upload and
+        // comparison run on the copy stream beside the step and are checked before anything is committed.
+        const Space& res = e.space[e.cur];
+        const bool candidate = e.world == 1 && e.has_state && e.has_cfg && res.has_h && res.has_full && res.n == rows &&
+                               e.steps_done + 1 == step_index && e.t == t && e.cfg.m == c.m && e.cfg.q_nom == c.q_nom &&
+                               e.cfg.dt == c.dt && e.cfg.rtol == c.rtol && e.cfg.max_order == c.max_order &&
+                               e.cfg.substeps == c.substeps && e.cfg.seed == c.seed &&
+                               std::getenv("PB200_NO_STEP_CACHE") == nullptr;
+        if (candidate) {
+            e.io_flags.ensure(16);
+            uint32_t* flags = e.io_flags.as<uint32_t>();
+            e.aux_coeff.ensure(rows * 16 + 16);
+            e.aux_words.ensure(rows * W * 4 + 16);
+            // both uploads and comparisons on their own stream: the step itself starts at once on the resident data
+            e.sync();  // the resident buffers they read are final
+            PB_CUDA(cudaMemsetAsync(flags, 0, 8, e.io_stream));
+            PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
+            words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(
+                e.aux_coeff.as<uint32_t>(), e.coeff[e.ccur].as<uint32_t>(), rows * 4, flags);
+            e.check_launch();
+            PB_CUDA(cudaMemcpyAsync(e.aux_words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.io_stream));
+            words_differ_kernel<<<e.grid_for(rows * W), NT, 0, e.io_stream>>>(
+                e.aux_words.as<uint32_t>(), res.words.as<uint32_t>(), rows * W, flags + 1);
+            e.check_launch();
+            {
+                const pb200_run_cfg saved = e.cfg;
+                e.cfg = c;
+                io.cached = true;
+                io.mismatch = flags;
+                e.io = &io;
+                try {
+                    e.run_step(out);
+                    const Space& nsp = e.space[e.cur];
+                    if (rows_out) *rows_out = nsp.n;
+                    if (nnz_out) *nnz_out = nsp.nnz;
+                    return;
+                } catch (const Engine::CacheMiss&) {
+                    // not the resident state after all: redo the step from the caller's buffers
+                } catch (...) {
+                    cudaStreamSynchronize(e.io_stream);
+                    throw;
+                }
+                e.cfg = saved;
+                e.io = nullptr;
+                io.cached = false;
+                io.mismatch = nullptr;
+            }
+            PB_CUDA(cudaStreamSynchronize(e.io_stream));
+            PB_CUDA(cudaStreamSynchronize(e.copy_stream));
+        }
+
         e.cfg = c;
         e.has_cfg = true;
         e.has_state = false;
         Space& sp = e.space[e.cur];
-        const size_t W = e.hm.W;
         sp.words.ensure(rows * W * 4 + 4);
         e.coeff[e.ccur].ensure(rows * 16 + 16);
         // coefficients first on the compute stream (the weight / selection kernels need only them); the keys travel
@@ -546,18 +614,6 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         e.t = t;
         e.steps_done = step_index - 1;
         e.has_state = true;
-        Engine::StepIO io;
-        io.out_words = out_words;
-        io.out_coeff = out_coeff;
-        io.out_cap_rows = out_cap_rows;
-        struct Guard {
-            Engine& e;
-            ~Guard() {
-                e.io = nullptr;
-                e.pending_words = false;
-                cudaStreamSynchronize(e.copy_stream);  // never leave a transfer into caller memory in flight
-            }
-        } guard{e};
         e.io = &io;
         e.run_step(out);
         const Space& nsp = e.space[e.cur];

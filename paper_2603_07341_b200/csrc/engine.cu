@@ -55,6 +55,7 @@ Engine::Engine(int dev) : device(dev) {
     PB_CUDA(cudaMallocHost(&pinned, 4096));
     for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
     PB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    PB_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
     PB_CUDA(cudaEventCreateWithFlags(&ev_words, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_table, cudaEventDisableTiming));
     ctl.ensure(sizeof(Ctl));
@@ -73,6 +74,10 @@ Engine::~Engine() {
     if (copy_stream) {
         cudaStreamSynchronize(copy_stream);
         cudaStreamDestroy(copy_stream);
+    }
+    if (io_stream) {
+        cudaStreamSynchronize(io_stream);
+        cudaStreamDestroy(io_stream);
     }
     if (ev_words) cudaEventDestroy(ev_words);
     if (ev_table) cudaEventDestroy(ev_table);
@@ -888,7 +893,8 @@ void Engine::run_step(pb200_diag* out) {
         defer_reads = (world == 1);
         // incremental adapt (incremental.cuh): needs the previous H_eff with its expansion flags; the full path
         // remains for the first step after a load, m = 0, a memory cap (its transcript accounting) and overflows
-        bool incremental = world == 1 && !io && old.has_h && old.has_full && cfg.m >= 1 && memory_cap_bytes() == 0 &&
+        bool incremental = world == 1 && (!io || io->cached) && old.has_h && old.has_full && cfg.m >= 1 &&
+                           memory_cap_bytes() == 0 &&
                            std::getenv("PB200_NO_INCREMENTAL") == nullptr;
         const uint32_t kept = world > 1
                                   ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
@@ -965,6 +971,15 @@ void Engine::run_step(pb200_diag* out) {
             PB_CUDA(cudaMemcpyAsync(io->out_coeff, psi, size_t(next.n) * 16, cudaMemcpyDeviceToHost, stream));
         sync();
         if (io) PB_CUDA(cudaStreamSynchronize(copy_stream));
+        if (io && io->cached) {
+            // the uploads and their comparisons ran beside the step; nothing is committed before they agree
+            PB_CUDA(cudaStreamSynchronize(io_stream));
+            struct F {
+                uint32_t v[2];
+            };
+            const F f = read_back<F>(io->mismatch);
+            if (f.v[0] != 0 || f.v[1] != 0) throw CacheMiss{};
+        }
         rec.taylor_order = order;
         rec.delta_norm_expmv = lcn - rec.norm_post;
         cur ^= 1;

@@ -164,13 +164,22 @@ struct Engine {
     cudaEvent_t ev[10]{};
     // host-buffer step with overlapped transfers (pb200_step_io)
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t io_stream = nullptr;  // uploads + comparisons of a cached host-buffer step (beside everything else)
     cudaEvent_t ev_words = nullptr, ev_table = nullptr;
     bool pending_words = false;   // the key upload of the current step is still in flight on copy_stream
     struct StepIO {
         uint32_t* out_words = nullptr;
         double* out_coeff = nullptr;
         uint64_t out_cap_rows = 0;
+        // The caller handed in the very state this context produced last (verified on the device, bit for bit):
+        // the resident table, H_eff and expansion flags are used, so the step can take the incremental adapt path.
+        // The comparison of the keys runs beside the step on the copy stream and is checked before the commit.
+        bool cached = false;
+        const uint32_t* mismatch = nullptr;  // two device flags written by the comparisons (coefficients, keys)
     };
+    /// thrown by run_step when the deferred key comparison of a cached host-buffer step fails
+    struct CacheMiss {};
+    DevBuf io_flags;  // [0] coefficients differ, [1] keys differ
     const StepIO* io = nullptr;
 
     // multi-GPU (one context per rank); world == 1 is the single-GPU path

@@ -732,6 +732,16 @@ __global__ void __launch_bounds__(NT) check_sorted_kernel(const uint32_t* __rest
     }
 }
 
+/// flag[0] = 1 unless the two word arrays are bitwise identical (host-buffer step: is the state the caller hands
+/// in the one this context produced last?).
+__global__ void __launch_bounds__(NT) words_differ_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                                          uint64_t n_words, uint32_t* __restrict__ flag) {
+    bool diff = false;
+    for (uint64_t i = uint64_t(blockIdx.x) * NT + threadIdx.x; i < n_words; i += uint64_t(gridDim.x) * NT)
+        diff |= (a[i] != b[i]);
+    if (diff) flag[0] = 1u;
+}
+
 /// L2 flush for benchmarking: streams a buffer larger than L2.
 __global__ void flush_kernel(double* __restrict__ buf, size_t n) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)

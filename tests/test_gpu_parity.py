@@ -485,3 +485,68 @@ def test_host_step_operator(gpu, port):
         ctx.step(w, c, t, 12, out_words=ow[: 10 * ctx.words], out_coeff=oc[:10], **kw)
     # the context is still usable after the failures
     assert np.array_equal(ctx.step(w, c, t, 12, **kw)[0], ctx.step(w, c, t, 12, out_words=ow, out_coeff=oc, **kw)[0])
+
+
+def test_host_step_reuses_resident_space_only_when_input_matches(gpu, port):
+    """pb200_step_io keeps its last result resident.  When the caller hands that very state back (verified on the
+    device, bit for bit) the step reuses the resident H_eff and takes the incremental adapt path; any difference in
+    the coefficients or the keys must be honoured -- the step is redone from the caller's buffers.  Every result is
+    compared with the oracle stepping from exactly the state that was passed in."""
+    from oracle.pyoracle import ModelDef
+
+    case = CASES["cfg2_layout_L16_d16_small"]
+    ctx = _ctx(gpu, case["model"])
+    om = port.model(ModelDef(**case["model"]))
+    ro = om.run(**case["run"])
+    for _ in range(5):
+        ro.step()
+    kw = {k: v for k, v in case["run"].items() if k not in ("init", "site")}
+    cap = 400000
+    bufs = [(np.zeros(cap * ctx.words, np.uint32), np.zeros(cap, np.complex128)) for _ in range(2)]
+    w, c = ro.state()
+    t = ro.info()[2]
+    # chain: feed the result back in, six times
+    inc0 = ctx.adapt_stats()["incremental_steps"]
+    for k, s in enumerate(range(6, 12)):
+        ow, oc, d = ctx.step(w, c, t, s, out_words=bufs[k & 1][0], out_coeff=bufs[k & 1][1], **kw)
+        do = ro.step()
+        wo, co = ro.state()
+        assert np.array_equal(ow, wo) and oc.tobytes() == co.tobytes(), s
+        _check_diag(d, do, "step_io chain", s)
+        w, c, t = ow, oc, d["t"]
+    assert ctx.adapt_stats()["incremental_steps"] - inc0 >= 4  # all but the first call reuse the resident space
+    w, c = np.array(w, copy=True), np.array(c, copy=True)  # the results above live in the output buffers
+
+    def oracle_step(words, coeff, tt, s):
+        kept = om.truncate_select(words, coeff, kw["q_nom"], port.mix_seed(kw["seed"] + s))
+        tw, rp, col, val = om.grow(kept, kw["m"])
+        psi, disc = om.remap(words, coeff, tw)
+        from oracle.pyoracle import expmv
+
+        psi2, order, _ = expmv(port, rp, col, val, psi, dt=kw["dt"], rtol=kw["rtol"], max_order=200, substeps=1)
+        return tw, psi2, order
+
+    # (a) same shape, one coefficient changed: the resident copy must NOT be used
+    c_mod = np.array(c, copy=True)
+    c_mod[len(c_mod) // 3] *= 0.5
+    ow, oc, d = ctx.step(w, c_mod, t, 12, out_words=bufs[0][0], out_coeff=bufs[0][1], **kw)
+    tw, psi, order = oracle_step(w, c_mod, t, 12)
+    assert np.array_equal(ow, tw) and oc.tobytes() == psi.tobytes() and d["taylor_order"] == order
+    # (b) the unmodified state again right after: the resident state is now the result of (a), so this is a miss too
+    ow, oc, d = ctx.step(w, c, t, 12, out_words=bufs[1][0], out_coeff=bufs[1][1], **kw)
+    tw, psi, order = oracle_step(w, c, t, 12)
+    assert np.array_equal(ow, tw) and oc.tobytes() == psi.tobytes() and d["taylor_order"] == order
+    # (c) feed (b)'s result back (a hit), then the same call with ONE key replaced by another sorted, valid key
+    w1, c1, t1 = np.array(ow, copy=True), np.array(oc, copy=True), d["t"]
+    ow, oc, d = ctx.step(w1, c1, t1, 13, out_words=bufs[0][0], out_coeff=bufs[0][1], **kw)
+    tw, psi, order = oracle_step(w1, c1, t1, 13)
+    assert np.array_equal(ow, tw) and oc.tobytes() == psi.tobytes()
+    w2, c2, t2 = np.array(ow, copy=True), np.array(oc, copy=True), d["t"]
+    w_bad = np.array(w2, copy=True)
+    L, d_pho = case["model"]["extents"][0], case["model"]["d_pho"]
+    cand = ctx.pack([L - 1] + [d_pho - 1] * L)  # the largest key of the layout: the table stays sorted and unique
+    assert tuple(cand) > tuple(w_bad[-1])
+    w_bad[-1] = cand
+    ow, oc, d = ctx.step(w_bad, c2, t2, 14, out_words=bufs[1][0], out_coeff=bufs[1][1], **kw)
+    tw, psi, order = oracle_step(w_bad, c2, t2, 14)
+    assert np.array_equal(ow, tw) and oc.tobytes() == psi.tobytes() and d["taylor_order"] == order
