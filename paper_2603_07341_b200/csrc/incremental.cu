@@ -140,10 +140,13 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     PB_CUDA(cudaMemsetAsync(c_new.p, 0, size_t(n_new) * 16, stream));
     inc_newidx.ensure(size_t(n) * 4 + 4);
     inc_side_newidx.ensure(size_t(side_n) * 4 + 4);
-    PB_DISPATCH_WI(W, inc_scatter_old_kernel<W><<<grid_for(n), NT, 0, stream>>>(
-                          old.words.as<uint32_t>(), c_old, n, m, dist, pos_a.as<uint32_t>(), gap.as<uint32_t>(),
-                          inc_newidx.as<uint32_t>(), next.words.as<uint32_t>(), next.full.as<uint8_t>(),
-                          c_new.as<double2>(), partials.as<double>(), &c->ticket, c->out));
+    inc_scatter_old_kernel<<<grid_for(n), NT, 0, stream>>>(c_old, n, m, dist, pos_a.as<uint32_t>(), gap.as<uint32_t>(),
+                                                           inc_newidx.as<uint32_t>(), next.full.as<uint8_t>(),
+                                                           c_new.as<double2>(), partials.as<double>(), &c->ticket,
+                                                           c->out);
+    check_launch();
+    PB_DISPATCH_WI(W, inc_copy_rows_kernel<W><<<grid_for(uint64_t(n) * W), NT, 0, stream>>>(
+                          old.words.as<uint32_t>(), n, inc_newidx.as<uint32_t>(), next.words.as<uint32_t>()));
     check_launch();
     if (side_n) {
         PB_DISPATCH_WI(W, inc_scatter_side_kernel<W><<<grid_for(side_n), NT, 0, stream>>>(

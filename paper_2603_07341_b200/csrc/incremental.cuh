@@ -177,17 +177,14 @@ __global__ void __launch_bounds__(NT) inc_count_gaps_kernel(const uint32_t* __re
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < side_n; j += gridDim.x * NT) atomicAdd(cntgap + side_gap[j], 1u);
 }
 
-/// New index of every old row (IDX_NONE when dropped), new table rows, `full` flags of the new space, and the
-/// coefficient remap fused in: kept rows carry their coefficient, dropped rows add |c|^2 to the discarded weight.
+/// New index of every old row (IDX_NONE when dropped), `full` flags of the new space, and the coefficient remap
+/// fused in: kept rows carry their coefficient, dropped rows add |c|^2 to the discarded weight.
 /// pk = exclusive scan of keepflag, nb = exclusive scan of cntgap (side keys with gap <= i precede row i).
-template <int W>
-__global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const uint32_t* __restrict__ table,
-                                                             const double2* __restrict__ c_old, uint32_t n, int m,
+__global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const double2* __restrict__ c_old, uint32_t n, int m,
                                                              const uint8_t* __restrict__ dist,
                                                              const uint32_t* __restrict__ pk,
                                                              const uint32_t* __restrict__ nb,
                                                              uint32_t* __restrict__ newidx,
-                                                             uint32_t* __restrict__ out_table,
                                                              uint8_t* __restrict__ out_full,
                                                              double2* __restrict__ c_new, double* __restrict__ partials,
                                                              unsigned* ticket, double* __restrict__ out) {
@@ -198,7 +195,6 @@ __global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const uint32_t* __r
         if (dist[i] <= uint8_t(m)) {
             const uint32_t o = pk[i] + nb[i + 1];
             newidx[i] = o;
-            store_key<W>(out_table + size_t(o) * W, load_key<W>(table + size_t(i) * W));
             out_full[o] = dist[i] < uint8_t(m) ? 1 : 0;
             c_new[o] = x;
         } else {
@@ -208,6 +204,20 @@ __global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const uint32_t* __r
     }
     double tot[1];
     if (grid_sum<1>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) out[0] = tot[0];
+}
+
+/// The surviving old rows into the new table, one thread per WORD: surviving rows come in long runs, so both the
+/// reads and the writes are coalesced whatever the key width (a thread per row moves 4W bytes at a 4W-byte stride).
+template <int W>
+__global__ void __launch_bounds__(NT) inc_copy_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
+                                                           const uint32_t* __restrict__ newidx,
+                                                           uint32_t* __restrict__ out_table) {
+    const uint64_t total = uint64_t(n) * W;
+    for (uint64_t w = uint64_t(blockIdx.x) * NT + threadIdx.x; w < total; w += uint64_t(gridDim.x) * NT) {
+        const uint32_t i = uint32_t(w / W);
+        const uint32_t o = __ldg(newidx + i);
+        if (o != IDX_NONE) out_table[uint64_t(o) * W + (w - uint64_t(i) * W)] = __ldg(table + w);
+    }
 }
 
 /// Side keys into the new table (c_new was zeroed: they start with zero amplitude).
