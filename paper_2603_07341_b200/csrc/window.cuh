@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(NT) expand_window_kernel(ModelDev m, const uin
             [&](int move, const Key<W>& kk, double, bool valid) {
                 uint32_t c = cur[move], pos;
                 bool found;
+                __syncwarp();  // all lanes hold the cursor before lane 0 rewrites it (no other barrier if no lane is valid)
                 warp_window_find<W>(table, n, win, c, kk, valid, pos, found);
                 if (lane == 0) cur[move] = c;
                 if (valid) {
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(NT) assemble_window_kernel(ModelDev m, const u
             [&](int move, const Key<W>& kk, double amp, bool valid) {
                 uint32_t c = cur[move], pos;
                 bool found;
+                __syncwarp();  // all lanes hold the cursor before lane 0 rewrites it (no other barrier if no lane is valid)
                 warp_window_find<W>(table, n, win, c, kk, valid, pos, found);
                 if (lane == 0) cur[move] = c;
                 if (valid && found) {
