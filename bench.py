@@ -292,7 +292,9 @@ def main():
         peak, peak_src = measured_peak()
         orders = max(1, times["taylor_orders"])
         avg_launch_ms = times["expmv_ms"] / orders
-        bytes_per_launch = 12.0 * (times["spmv_nnz"] / orders) + 72.0 * rows
+        # a deferred order (kernels.cuh TAYLOR_DEFER) neither reads nor writes c: 12z + 40n instead of 12z + 72n
+        deferred = times.get("taylor_deferred", 0)
+        bytes_per_launch = 12.0 * (times["spmv_nnz"] / orders) + (72.0 - 32.0 * deferred / orders) * rows
         achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
         traffic, traffic_src = measured_traffic(bytes_per_launch)
         iso_ms, _, _ = run.bench_taylor(orders=20, flush_l2=True, dt=RUN["dt"])
@@ -303,7 +305,9 @@ def main():
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
-            "launches_timed": int(orders),
+            "launches_timed": int(orders), "launches_deferred": int(deferred),
+            "bytes_formula": "12*nnz + 72*rows per order (SURVEY 8d); 12*nnz + 40*rows for an order that leaves c "
+                             "alone (paired orders: c crosses HBM once per two orders)",
             "isolated_l2_flushed": {"ms": iso_ms, "GB/s": (12.0 * nnz + 72.0 * rows) / (iso_ms * 1e-3) / 1e9},
             "plain_spmv_l2_flushed": {"ms": spmv_ms, "GB/s": (12.0 * nnz + 40.0 * rows) / (spmv_ms * 1e-3) / 1e9,
                                       "nnz_per_s": nnz / (spmv_ms * 1e-3)},

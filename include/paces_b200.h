@@ -78,6 +78,7 @@ typedef struct pb200_phase_times {
     uint64_t taylor_orders; /* number of fused Taylor-order launches */
     uint64_t kernel_launches;
     uint64_t steps;
+    uint64_t taylor_deferred; /* of taylor_orders: launches that ran deferred (c untouched: 12z + 40n bytes) */
 } pb200_phase_times;
 
 /* ---- context ------------------------------------------------------------------------------- */

@@ -586,12 +586,24 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
         }
         int order = 1;
         bool converged = false;
+        // Paired orders (kernels.cuh): DEFER/CATCHUP pairs from order k0 on, placed so that the order the previous
+        // expmv stopped at is the second of a pair; a DEFER launch that meets streak != 0 raises `bail` instead.
+        bool singles = !taylor_defer;
+        const int k0 = (last_order > 2 && (last_order & 1) == 0) ? 3 : 2;
+        static int catchup_per_sm = 0;
+        if (catchup_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&catchup_per_sm, taylor_catchup_kernel,
+                                                                                  NT, 0) != cudaSuccess ||
+                                    catchup_per_sm < 1))
+            catchup_per_sm = 4;
+        const int gc = std::min(g, sm_count * catchup_per_sm);  // single wave
         // launch in batches; the stop rule runs on the device and turns the tail of a batch into no-ops
         int batch = last_order > 2 ? last_order : 8;
         while (order <= max_order) {
             const int end = std::min(max_order, order + batch - 1);
             for (; order <= end; ++order) {
                 const double b = -dt_sub / double(order);
+                const double2* tin = term[(order - 1) & 1].as<double2>();
+                double2* tout = term[order & 1].as<double2>();
                 if (fuse_expectation && s == 0 && order == 1) {
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
                     // (Ctl::out[1..3], read with the final read-back).  This variant needs more registers: size
@@ -604,14 +616,20 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                         per_sm = 4;
                     const int g1 = std::min(g, sm_count * per_sm);
                     taylor_order_kernel_t<true><<<g1, NT, 0, stream>>>(
-                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
-                        term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
-                        partials.as<double>(), &c->taylor, 0, nullptr, c->out + 1);
+                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(), tin, tout, c_vec, b,
+                        order, rtol, partials.as<double>(), &c->taylor, 0, nullptr, c->out + 1);
+                } else if (!singles && order >= k0 && ((order - k0) & 1)) {
+                    taylor_catchup_kernel<<<gc, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                                 sp.val.as<double>(), tin, tout, c_vec, b, order, rtol,
+                                                                 partials.as<double>(), &c->taylor);
+                } else if (!singles && order >= k0 && order < max_order) {
+                    taylor_defer_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                                              sp.val.as<double>(), tin, tout, b, order,
+                                                              partials.as<double>(), &c->taylor);
                 } else {
                     taylor_order_kernel_t<false><<<g, NT, 0, stream>>>(
-                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(),
-                        term[(order - 1) & 1].as<double2>(), term[order & 1].as<double2>(), c_vec, b, order, rtol,
-                        partials.as<double>(), &c->taylor, 0, nullptr, nullptr);
+                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(), tin, tout, c_vec, b,
+                        order, rtol, partials.as<double>(), &c->taylor, 0, nullptr, nullptr);
                 }
                 check_launch();
             }
@@ -621,6 +639,12 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                 converged = true;
                 break;
             }
+            if (tc.bail) {  // order tc.bail has to run SINGLE (everything launched after it returned at once)
+                order = tc.bail;
+                singles = true;
+                tc.bail = 0;
+                PB_CUDA(cudaMemsetAsync(&c->taylor.bail, 0, sizeof(int), stream));
+            }
             batch = 2;
         }
         times.taylor_orders += uint64_t(tc.last_order);
@@ -628,6 +652,7 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
             throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
                              "; reduce dt or increase substeps");
     }
+    times.taylor_deferred += uint64_t(tc.deferred);
     last_order = tc.order_used;
     if (order_used) *order_used = tc.order_used;
     if (last_term_norm) *last_term_norm = tc.last_term_norm;

@@ -271,6 +271,8 @@ struct Engine {
     /// Snapshot of the control block taken by the last read-back of expmv(): the step's deferred scalars
     /// (discarded weight, <H>, norm, nnz) ride along instead of costing a stream synchronisation each.
     Ctl last_ctl{};
+    // paired Taylor orders (kernels.cuh, TAYLOR_DEFER / TAYLOR_CATCHUP); PB200_NO_TAYLOR_DEFER=1 runs every order SINGLE
+    bool taylor_defer = std::getenv("PB200_NO_TAYLOR_DEFER") == nullptr;
     bool defer_reads = false;  // run_step on one GPU: leave scalars on the device until the final read-back
     Ctl* dctl() const { return ctl.as<Ctl>(); }
 

@@ -410,6 +410,49 @@ def test_incremental_adapt_equals_full_expansion(gpu, monkeypatch, name, model, 
         assert si["expanded_rows"] > 0 and si["side_keys"] > 0, si
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("rtol,substeps,max_order", [(1e-15, 1, 200), (1e-6, 1, 200), (1e-3, 2, 200), (0.5, 1, 200),
+                                                     (1e-15, 3, 200), (1e-15, 1, 9)])
+def test_paired_taylor_orders_equal_single_orders(gpu, port, monkeypatch, rtol, substeps, max_order):
+    """expmv with paired orders (an order whose predecessor did not meet the stop rule leaves c alone, the next one
+    adds both terms in the reference's order; kernels.cuh TAYLOR_DEFER / TAYLOR_CATCHUP) against one order per launch
+    (PB200_NO_TAYLOR_DEFER=1) and against the oracle: coefficients bit-identical, same order and norms, for stop
+    orders of either parity, substeps, and a series that runs into max_order (same error, propagator.hpp:87-89)."""
+    from oracle import pyoracle
+
+    model = dict(kind=1, extents=(5,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=6)
+    run_kw = dict(init="localized", site=-1, m_init=5, m=2, q_nom=700, dt=0.05, rtol=rtol, max_order=max_order,
+                  substeps=substeps, t_max=5.0, seed=7)
+    monkeypatch.delenv("PB200_NO_TAYLOR_DEFER", raising=False)
+    rp = _ctx(gpu, model).run(**run_kw)
+    monkeypatch.setenv("PB200_NO_TAYLOR_DEFER", "1")
+    rs = _ctx(gpu, model).run(**run_kw)
+    monkeypatch.delenv("PB200_NO_TAYLOR_DEFER", raising=False)
+    ro = port.model(pyoracle.ModelDef(**model)).run(**run_kw)
+    if max_order == 9:  # rtol 1e-15 needs ~11 orders: every implementation must refuse with the reference's text
+        for r in (rp, rs):
+            with pytest.raises(gpu.PacesError, match="reduce dt"):
+                r.step()
+        with pytest.raises(Exception, match="reduce dt"):
+            ro.step()
+        return
+    orders = set()
+    for s in range(1, 13):
+        dp, ds, do = rp.step(), rs.step(), ro.step()
+        orders.add(dp["taylor_order"])
+        assert dp["taylor_order"] == ds["taylor_order"] == do["taylor_order"], (s, dp, ds, do)
+        for k in ("norm_pre", "norm_post", "energy", "discarded_weight", "delta_norm_expmv"):
+            assert _close(dp[k], ds[k], 1e-13, 1e-14), (s, k, dp[k], ds[k])  # reduction shapes differ (grid sizes)
+            assert _close(dp[k], do[k], 1e-10, 1e-13), (s, k, dp[k], do[k])
+        (wp, cp), (ws, cs), (wo, co) = rp.state(), rs.state(), ro.state()
+        assert np.array_equal(wp, ws) and np.array_equal(wp, wo), s
+        assert cp.tobytes() == cs.tobytes() == co.tobytes(), s
+    tp, ts = rp.times(), rs.times()
+    assert ts["taylor_deferred"] == 0 and tp["taylor_orders"] == ts["taylor_orders"]
+    if min(orders) >= 4:
+        assert tp["taylor_deferred"] >= (tp["taylor_orders"] - 3 * 12 * substeps) // 2, (tp, orders)
+
+
 def test_weight_histogram_against_oracle(gpu, port):
     """SURVEY 8f rank 1 (observables.hpp:123-176, test_observables.cpp:170-220): the GPU sorts, the host replays the
     reference's serial sums -> every field bit-identical, on host vectors and on the resident state."""
