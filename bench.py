@@ -300,8 +300,9 @@ def main():
         iso_ms, _, _ = run.bench_taylor(orders=20, flush_l2=True, dt=RUN["dt"])
         spmv_ms = run.bench_spmv(reps=20, flush_l2=True)
         roofline = {
-            "kernel": "taylor_order_kernel_t (y=H_eff x fused with term'=(0,-dt/n) y, c+=term', |term'|^2, |c|^2; the "
-                      "first order also yields <x|H|x>)",
+            "kernel": "fused Taylor order (taylor_order_kernel_t / taylor_defer_kernel / taylor_catchup_kernel): y=H_eff x, "
+                      "term'=(0,-dt/n) y, |term'|^2; c+=term' and |c|^2 once per PAIR of orders; the first order also "
+                      "yields <x|H|x>",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,

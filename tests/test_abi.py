@@ -64,3 +64,28 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".hpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in text.replace("dense oracle", ""), os.path.join(dirpath, f)
+
+
+def test_taylor_kernels_keep_their_register_budget(lib):
+    """The Taylor-order kernels are latency-bound: SINGLE and DEFER need 32 registers (8 resident CTAs of 256 threads
+    per SM), CATCHUP and the first-order variant 40 (6 CTAs), none may spill.  ptxas once gave the DEFER kernel 40
+    registers in the full build and 32 stand-alone; the launch bounds pin them, this test watches the binary."""
+    import shutil
+    import subprocess
+
+    from paper_2603_07341_b200 import build
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", build.LIB], capture_output=True, text=True).stdout
+    usage = {}
+    for name, regs, stack in re.findall(r"Function (\S+?):\s*\n\s*REG:(\d+) STACK:(\d+)", out):
+        usage[name] = (int(regs), int(stack))
+    budget = {"taylor_order_kernel_tILb0E": 32, "taylor_order_kernel_tILb1E": 40, "taylor_defer_kernel": 32,
+              "taylor_catchup_kernel": 40}
+    for key, cap in budget.items():
+        hits = [v for k, v in usage.items() if key in k]
+        assert hits, (key, sorted(usage)[:5])
+        for regs, stack in hits:
+            assert regs <= cap and stack == 0, (key, regs, stack)
