@@ -15,7 +15,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpaces_b200.so")
 SOURCES = ["paces_b200.cu"]
-DEPS = ["paces_b200.cu", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "incremental.cu", "keys.cuh",
+# compiled on their own and WITHOUT -split-compile: ptxas under -split-compile gives the Taylor kernels a different
+# register allocation from one run to the next (spills or not, same source), and those kernels need exact budgets
+SERIAL_SOURCES = ["taylor.cu"]
+DEPS = ["paces_b200.cu", "taylor.cu", "taylor.cuh", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "incremental.cu", "keys.cuh",
         "primitives.cuh",
         "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
@@ -39,12 +42,27 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    objs = []
+    serial_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-split-compile", "0")]
+    for src in SERIAL_SOURCES:
+        obj = os.path.join(HERE, "_" + os.path.splitext(src)[0] + ".o")
+        c = [_nvcc(), *serial_flags, "-c", "-o", obj, os.path.join(CSRC, src)] + (["-Xptxas", "-v"] if verbose else [])
+        r = subprocess.run(c, cwd=CSRC, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed compiling " + src)
+        if verbose:
+            sys.stderr.write(r.stderr)
+        objs.append(obj)
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + objs
     if os.environ.get("PB200_ONLY_W"):  # development / profiling build restricted to one key width
         cmd += ["-DPB_ONLY_W=" + str(int(os.environ["PB200_ONLY_W"]))]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    for obj in objs:
+        if os.path.exists(obj):
+            os.remove(obj)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libpaces_b200.so")

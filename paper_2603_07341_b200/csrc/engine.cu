@@ -1,4 +1,5 @@
 // engine.cu -- implementation of the device-resident paces step (see engine.cuh, kernels.cuh).
+#include <atomic>
 #include "engine.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -53,6 +54,11 @@ Engine::Engine(int dev) : device(dev) {
     sm_count = prop.multiProcessorCount;
     PB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PB_CUDA(cudaMallocHost(&pinned, 4096));
+    if (std::getenv("PB200_READBACK_MEMCPY") == nullptr) {
+        PB_CUDA(cudaHostAlloc(&mapped, 4096, cudaHostAllocMapped));
+        std::memset(mapped, 0, 4096);
+        PB_CUDA(cudaHostGetDevicePointer(&mapped_dev, mapped, 0));
+    }
     for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
     PB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PB_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
@@ -82,7 +88,36 @@ Engine::~Engine() {
     if (ev_words) cudaEventDestroy(ev_words);
     if (ev_table) cudaEventDestroy(ev_table);
     if (pinned) cudaFreeHost(pinned);
+    if (mapped) cudaFreeHost(mapped);
     if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+/// read_back's device side: payload words into mapped host memory, then the sequence flag.
+__global__ void publish_kernel(const uint32_t* __restrict__ src, uint32_t* dst, uint32_t nwords, uint32_t* flag,
+                               uint32_t seq) {
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *(volatile uint32_t*)flag = seq;
+}
+
+void Engine::publish(const void* dptr, uint32_t nwords) {
+    const uint32_t want = ++rb_seq;
+    uint32_t* base = static_cast<uint32_t*>(mapped_dev);
+    publish_kernel<<<1, 128, 0, stream>>>(static_cast<const uint32_t*>(dptr), base + 16, nwords, base, want);
+    check_launch();
+    volatile uint32_t* flag = static_cast<volatile uint32_t*>(mapped);
+    for (uint64_t spins = 1; *flag != want; ++spins) {
+        if ((spins & 0x3fff) == 0) {  // a failed kernel never raises the flag: look at the stream now and then
+            const cudaError_t q = cudaStreamQuery(stream);
+            if (q == cudaSuccess) {
+                if (*flag == want) break;
+                throw CudaFail("internal error: read-back flag missing after the stream drained");
+            }
+            if (q != cudaErrorNotReady) PB_CUDA(q);
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 void Engine::exclusive_scan(uint32_t* data, uint64_t n) {
@@ -590,12 +625,6 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
         // expmv stopped at is the second of a pair; a DEFER launch that meets streak != 0 raises `bail` instead.
         bool singles = !taylor_defer;
         const int k0 = (last_order > 2 && (last_order & 1) == 0) ? 3 : 2;
-        static int catchup_per_sm = 0;
-        if (catchup_per_sm == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&catchup_per_sm, taylor_catchup_kernel,
-                                                                                  NT, 0) != cudaSuccess ||
-                                    catchup_per_sm < 1))
-            catchup_per_sm = 4;
-        const int gc = std::min(g, sm_count * catchup_per_sm);  // single wave
         // launch in batches; the stop rule runs on the device and turns the tail of a batch into no-ops
         int batch = last_order > 2 ? last_order : 8;
         while (order <= max_order) {
@@ -604,32 +633,23 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                 const double b = -dt_sub / double(order);
                 const double2* tin = term[(order - 1) & 1].as<double2>();
                 double2* tout = term[order & 1].as<double2>();
+                const uint32_t* rp = sp.row_ptr.as<uint32_t>();
+                const int32_t* cl = sp.col.as<int32_t>();
+                const double* vl = sp.val.as<double>();
+                double* pt = partials.as<double>();
                 if (fuse_expectation && s == 0 && order == 1) {
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
-                    // (Ctl::out[1..3], read with the final read-back).  This variant needs more registers: size
-                    // its grid to what is resident so the launch is a single wave.
-                    static int per_sm = 0;
-                    if (per_sm == 0 &&
-                        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taylor_order_kernel_t<true>, NT, 0) !=
-                             cudaSuccess ||
-                         per_sm < 1))
-                        per_sm = 4;
-                    const int g1 = std::min(g, sm_count * per_sm);
-                    taylor_order_kernel_t<true><<<g1, NT, 0, stream>>>(
-                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(), tin, tout, c_vec, b,
-                        order, rtol, partials.as<double>(), &c->taylor, 0, nullptr, c->out + 1);
+                    // (Ctl::out[1..3], read with the final read-back)
+                    taylor_launch_single(true, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
+                                         &c->taylor, 0, nullptr, c->out + 1);
                 } else if (!singles && order >= k0 && ((order - k0) & 1)) {
-                    taylor_catchup_kernel<<<gc, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                                                 sp.val.as<double>(), tin, tout, c_vec, b, order, rtol,
-                                                                 partials.as<double>(), &c->taylor);
+                    taylor_launch_catchup(g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
+                                          &c->taylor);
                 } else if (!singles && order >= k0 && order < max_order) {
-                    taylor_defer_kernel<<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                                              sp.val.as<double>(), tin, tout, b, order,
-                                                              partials.as<double>(), &c->taylor);
+                    taylor_launch_defer(g, stream, n, rp, cl, vl, tin, tout, b, order, pt, &c->taylor);
                 } else {
-                    taylor_order_kernel_t<false><<<g, NT, 0, stream>>>(
-                        n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), sp.val.as<double>(), tin, tout, c_vec, b,
-                        order, rtol, partials.as<double>(), &c->taylor, 0, nullptr, nullptr);
+                    taylor_launch_single(false, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
+                                         &c->taylor, 0, nullptr, nullptr);
                 }
                 check_launch();
             }

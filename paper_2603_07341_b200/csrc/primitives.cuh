@@ -98,7 +98,7 @@ constexpr int LB_IPT = 16;
 constexpr int LB_TILE = NT * LB_IPT;
 constexpr unsigned long long LB_AGG = 1ull << 62, LB_PREFIX = 2ull << 62, LB_FLAGS = 3ull << 62;
 
-__global__ void __launch_bounds__(NT) scan_lookback_kernel(const uint32_t* in, uint64_t n, uint32_t* out,
+static __global__ void __launch_bounds__(NT) scan_lookback_kernel(const uint32_t* in, uint64_t n, uint32_t* out,
                                                            unsigned long long* status, unsigned* ticket) {
     __shared__ uint32_t smem[NT / 32];
     __shared__ uint32_t s_tile, s_prefix;

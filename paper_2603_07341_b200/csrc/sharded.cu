@@ -447,10 +447,10 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
             for (; order <= end; ++order) {
                 const double b = -dt_sub / double(order);
                 halo_exchange(sp, term[(order - 1) & 1].as<double2>());
-                taylor_order_kernel_t<false><<<g, NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                                          sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
-                                                          term[order & 1].as<double2>(), c_vec, b, order, rtol,
-                                                          partials.as<double>(), &c->taylor, 0, c->out, nullptr);
+                taylor_launch_single(false, g, sm_count, stream, n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+                                     sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
+                                     term[order & 1].as<double2>(), c_vec, b, order, rtol, partials.as<double>(),
+                                     &c->taylor, 0, c->out, nullptr);
                 check_launch();
                 comm_check(ops.allreduce_f64_dev(ops.user, c->out, 2, stream), "allreduce_f64_dev");
                 taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);

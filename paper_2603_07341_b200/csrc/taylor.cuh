@@ -1,0 +1,40 @@
+// taylor.cuh -- K4, the fused Taylor-order kernels of expmv (propagator.hpp:52-92): control block and launchers.
+// The kernels live in their own translation unit (taylor.cu): they are latency-bound and need exact register budgets
+// (32 / 40), and inside the large unity module (-split-compile) ptxas was seen to give the same source 40 registers or
+// spills depending on unrelated code.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pb {
+
+struct TaylorCtl {
+    int done;        // stop rule satisfied: later launches of this substep return immediately
+    int streak;      // consecutive small terms (propagator.hpp:80)
+    int order_used;  // max over substeps (propagator.hpp:78)
+    int last_order;  // order of the most recent launch that did work
+    double last_term_norm;
+    double last_c_norm;
+    unsigned ticket;
+    int pending;         // the previous order ran deferred: its term is not in c yet, its stop rule not applied
+    double pending_tn2;  // |term|^2 of that order
+    int bail;            // a deferred launch found streak != 0 at this order and did nothing: the host relaunches it SINGLE
+    unsigned deferred;   // launches that ran deferred (statistics)
+};
+
+/// Launch modes (see taylor.cu).  `grid` is the caller's row grid (8 CTAs per SM); the first-order and catch-up
+/// kernels clamp it to one resident wave.  All launches are asynchronous on `stream`; errors surface in the caller's
+/// cudaGetLastError check.
+void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                          const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
+                          double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
+                          double* tot_out, double* expect_out);
+void taylor_launch_defer(int grid, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
+                         const double* val, const double2* term_in, double2* term_out, double b, int order,
+                         double* partials, TaylorCtl* ctl);
+void taylor_launch_catchup(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
+                           double b, int order, double rtol, double* partials, TaylorCtl* ctl);
+
+}  // namespace pb

@@ -68,8 +68,9 @@ def test_product_never_imports_oracle():
 
 def test_taylor_kernels_keep_their_register_budget(lib):
     """The Taylor-order kernels are latency-bound: SINGLE and DEFER need 32 registers (8 resident CTAs of 256 threads
-    per SM), CATCHUP and the first-order variant 40 (6 CTAs), none may spill.  ptxas once gave the DEFER kernel 40
-    registers in the full build and 32 stand-alone; the launch bounds pin them, this test watches the binary."""
+    per SM), CATCHUP and the first-order variant 40 (6 CTAs), none may spill (the first-order variant parks one double).
+    Under -split-compile ptxas gave the same source 32 or 40 registers, spills or none, from one build to the next:
+    the launch bounds pin the budgets, taylor.cu is compiled without that flag, and this test watches the binary."""
     import shutil
     import subprocess
 
@@ -88,4 +89,4 @@ def test_taylor_kernels_keep_their_register_budget(lib):
         hits = [v for k, v in usage.items() if key in k]
         assert hits, (key, sorted(usage)[:5])
         for regs, stack in hits:
-            assert regs <= cap and stack == 0, (key, regs, stack)
+            assert regs <= cap and stack <= (8 if "ILb1E" in key else 0), (key, regs, stack)
