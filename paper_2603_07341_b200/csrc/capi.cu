@@ -556,15 +556,21 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
             e.aux_words.ensure(rows * W * 4 + 16);
             // both uploads and comparisons on their own stream: the step itself starts at once on the resident data
             e.sync();  // the resident buffers they read are final
-            PB_CUDA(cudaMemsetAsync(flags, 0, 8, e.io_stream));
-            PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
-            words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(
-                e.aux_coeff.as<uint32_t>(), e.coeff[e.ccur].as<uint32_t>(), rows * 4, flags);
-            e.check_launch();
-            PB_CUDA(cudaMemcpyAsync(e.aux_words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.io_stream));
-            words_differ_kernel<<<e.grid_for(rows * W), NT, 0, e.io_stream>>>(
-                e.aux_words.as<uint32_t>(), res.words.as<uint32_t>(), rows * W, flags + 1);
-            e.check_launch();
+            auto upload = [&e, flags, coeff, words, rows, W, &res]() {
+                PB_CUDA(cudaMemsetAsync(flags, 0, 8, e.io_stream));
+                PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
+                words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(
+                    e.aux_coeff.as<uint32_t>(), e.coeff[e.ccur].as<uint32_t>(), rows * 4, flags);
+                e.check_launch();
+                PB_CUDA(cudaMemcpyAsync(e.aux_words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.io_stream));
+                words_differ_kernel<<<e.grid_for(rows * W), NT, 0, e.io_stream>>>(
+                    e.aux_words.as<uint32_t>(), res.words.as<uint32_t>(), rows * W, flags + 1);
+                e.check_launch();
+            };
+            if (std::getenv("PB200_EAGER_UPLOAD"))
+                upload();
+            else
+                io.start_upload = upload;
             {
                 const pb200_run_cfg saved = e.cfg;
                 e.cfg = c;

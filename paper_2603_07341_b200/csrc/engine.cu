@@ -961,6 +961,10 @@ void Engine::run_step(pb200_diag* out) {
             grow(seeds.as<uint32_t>(), kept, cfg.m, next);
         }
         PB_CUDA(cudaEventRecord(ev[3], stream));
+        if (io && io->start_upload) {
+            io->start_upload();
+            io->start_upload = nullptr;
+        }
         if (io) {
             // the new table is final: ship it to the host beside remap + <H> + expmv
             if (next.n > io->out_cap_rows) throw ArgError("step_io: output buffers too small for the new state");

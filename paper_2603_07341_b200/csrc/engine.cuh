@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <random>
 #include <string>
 #include <vector>
@@ -179,6 +180,10 @@ struct Engine {
         // The comparison of the keys runs beside the step on the copy stream and is checked before the commit.
         bool cached = false;
         const uint32_t* mismatch = nullptr;  // two device flags written by the comparisons (coefficients, keys)
+        // Enqueues the verification uploads + comparisons.  run_step calls it once the adapt phase is enqueued: that
+        // phase is ~40 short kernels whose launches (command fetches over PCIe) crawl while 100 MB of upload
+        // saturate the same link direction; the Taylor kernels behind it are long and enqueued ahead.
+        mutable std::function<void()> start_upload;
     };
     /// thrown by run_step when the deferred key comparison of a cached host-buffer step fails
     struct CacheMiss {};
