@@ -15,14 +15,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpaces_b200.so")
 SOURCES = ["paces_b200.cu"]
-# compiled on their own and WITHOUT -split-compile: ptxas under -split-compile gives the Taylor kernels a different
-# register allocation from one run to the next (spills or not, same source), and those kernels need exact budgets
+# No -split-compile anywhere: with it ptxas gave the same source different register allocations from one build to the
+# next (the Taylor kernels: 32 or 40 registers, spills or none) -- up to 10 % of a step.  The latency-critical Taylor
+# kernels are also their own translation unit so that their budgets do not depend on the rest of the module.
 SERIAL_SOURCES = ["taylor.cu"]
 DEPS = ["paces_b200.cu", "taylor.cu", "taylor.cuh", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "incremental.cu", "keys.cuh",
         "primitives.cuh",
         "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
-              "-Xcompiler", "-fPIC,-O2", "-shared", "-split-compile", "0"]
+              "-Xcompiler", "-fPIC,-O2", "-shared"]
 
 
 def _nvcc() -> str:
@@ -43,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     objs = []
-    serial_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-split-compile", "0")]
+    serial_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     for src in SERIAL_SOURCES:
         obj = os.path.join(HERE, "_" + os.path.splitext(src)[0] + ".o")
         c = [_nvcc(), *serial_flags, "-c", "-o", obj, os.path.join(CSRC, src)] + (["-Xptxas", "-v"] if verbose else [])
