@@ -40,12 +40,14 @@ for q in qs:
     for _ in range(3):
         run.step()
     run.reset_times()
+    a0 = run.adapt_stats()
     k = 20 if q <= 3e6 else 5
     t0 = time.perf_counter()
     for _ in range(k):
         d = run.step()
     wall = (time.perf_counter() - t0) / k
     tm = run.times()
+    a1 = run.adapt_stats()
     rows, nnz, _, _ = run.info()
     t_ms, _, _ = run.bench_taylor(10, True)
     s_ms = run.bench_spmv(10, True)
@@ -55,6 +57,7 @@ for q in qs:
                taylor_ms=t_ms, taylor_GBs=(12 * nnz + 72 * rows) / t_ms / 1e6, taylor_frac=(12 * nnz + 72 * rows) / t_ms / 1e6 / PEAK,
                spmv_ms=s_ms, spmv_GBs=(12 * nnz + 40 * rows) / s_ms / 1e6, spmv_frac=(12 * nnz + 40 * rows) / s_ms / 1e6 / PEAK,
                spmv_nnz_per_s=nnz / (s_ms * 1e-3),
+               adapt_in_window={kk: a1[kk] - a0[kk] for kk in a1},
                in_step_taylor_GBs=(12 * tm["spmv_nnz"] / max(tm["taylor_orders"], 1) + 72 * rows) / (tm["expmv_ms"] / max(tm["taylor_orders"], 1)) / 1e6)
     print(json.dumps(rec), flush=True)
     ctx.close()
