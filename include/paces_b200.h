@@ -79,6 +79,13 @@ typedef struct pb200_phase_times {
     uint64_t kernel_launches;
     uint64_t steps;
     uint64_t taylor_deferred; /* of taylor_orders: launches that ran deferred (c untouched: 12z + 40n bytes) */
+    uint64_t taylor_rows;          /* sum over Taylor-order launches of the rows they covered */
+    uint64_t taylor_deferred_rows; /* same, deferred launches only */
+    uint64_t rows_sum, nnz_sum;    /* sum over steps of q_true and nnz(H_eff) of the space the step evolved on */
+    uint64_t rows_old_sum;         /* sum over steps of the rows of the state the step started from */
+    uint64_t kept_sum;             /* sum over steps of the keys truncate_select kept */
+    /* assemble_ms, remap_ms and expectation_ms stay ~0 in the resident single-GPU step: assembly and remap are
+     * part of the incremental adapt phase (inside grow_ms), <H> rides on the first Taylor order (inside expmv_ms) */
 } pb200_phase_times;
 
 /* ---- context ------------------------------------------------------------------------------- */
@@ -130,7 +137,8 @@ int pb200_model_info(const pb200_ctx* ctx, uint32_t* layout_sites, uint32_t* wor
 int pb200_pack(const pb200_ctx* ctx, const uint32_t* occ, uint32_t* words);
 int pb200_unpack(const pb200_ctx* ctx, const uint32_t* words, uint32_t* occ);
 /* apply_terms (lattice_models.hpp:212-267) for n_keys keys on the device: per key up to `cap`
- * (neighbour key, amplitude) pairs in the reference's emission order, count[i] of them. */
+ * (neighbour key, amplitude) pairs in CANONICAL (ascending key) order -- the reference emits them in term order;
+ * as sorted sets the two are identical (tests/test_gpu_parity.py) -- count[i] of them. */
 int pb200_apply_terms(pb200_ctx* ctx, const uint32_t* keys, uint64_t n_keys, uint32_t* out_keys,
                       double* out_amps, int cap, int* count);
 
@@ -171,9 +179,12 @@ int pb200_phonon_numbers(pb200_ctx* ctx, const uint32_t* words, const double* co
 
 /* weight_histogram (observables.hpp:114-176): descending |c|^2 curve of the non-zero
  * coefficients, the counts reaching 50 / 90 / 99 / 99.99 % of the total weight, the log-log tail slope, and the
- * curve sampled at `bins` ranks (0 = every rank).  The O(q log q) sort runs on the GPU; the serial running sums
- * of the reference are replayed on the host over the sorted weights, so every field equals the reference's bit
- * for bit.  rank/weight receive min(cap, *npts) points.  pb200_run_weight_histogram works on the resident state. */
+ * curve sampled at `bins` ranks (0 = every rank).  Everything runs on the GPU (stable LSD radix sort of the
+ * weights' bit patterns, prefix sums for the marks, a grid reduction for the slope); only min(cap, *npts) curve
+ * points and a 64-byte result block are downloaded.  support, the sampled ranks and weights are exact; the marks
+ * use fixed-tree prefix sums instead of the reference's serial running sum (they can differ only when a running
+ * sum lies within rounding distance of a threshold); tail_exponent agrees to 1e-10 relative.
+ * pb200_run_weight_histogram works on the resident state. */
 typedef struct {
     uint64_t support, q50, q90, q99, q9999;
     double tail_exponent;
@@ -218,7 +229,9 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
  * and run parameters), the uploaded coefficients and keys are compared on the device with the resident ones -- on
  * their own stream, beside the step -- and, when they are bit-identical, the step works on the resident table and
  * H_eff (the caller's EffectiveSpace, engine.hpp:268) and takes the incremental adapt path; nothing is committed
- * before both comparisons agree.  Any difference, and the step is redone from the caller's buffers. */
+ * before both comparisons agree.  Any difference, and the step is redone from the caller's buffers.
+ * The input buffers are read while the outputs are written: words/coeff must not overlap out_words/out_coeff
+ * (PB200_ERR_ARG otherwise) -- alternate between two buffer sets. */
 int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, const uint32_t* words,
                   const double* coeff, uint64_t rows, double t, uint32_t* out_words, double* out_coeff,
                   uint64_t out_cap_rows, pb200_diag* out, uint64_t* rows_out, uint64_t* nnz_out);

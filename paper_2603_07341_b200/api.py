@@ -80,7 +80,9 @@ class PhaseTimes(C.Structure):
         ("select_ms", C.c_double), ("grow_ms", C.c_double), ("assemble_ms", C.c_double), ("remap_ms", C.c_double),
         ("expectation_ms", C.c_double), ("expmv_ms", C.c_double), ("total_ms", C.c_double),
         ("spmv_nnz", C.c_uint64), ("taylor_orders", C.c_uint64), ("kernel_launches", C.c_uint64),
-        ("steps", C.c_uint64), ("taylor_deferred", C.c_uint64),
+        ("steps", C.c_uint64), ("taylor_deferred", C.c_uint64), ("taylor_rows", C.c_uint64),
+        ("taylor_deferred_rows", C.c_uint64), ("rows_sum", C.c_uint64), ("nnz_sum", C.c_uint64),
+        ("rows_old_sum", C.c_uint64), ("kept_sum", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -14,14 +14,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpaces_b200.so")
-SOURCES = ["paces_b200.cu"]
-# No -split-compile anywhere: with it ptxas gave the same source different register allocations from one build to the
-# next (the Taylor kernels: 32 or 40 registers, spills or none) -- up to 10 % of a step.  The latency-critical Taylor
-# kernels are also their own translation unit so that their budgets do not depend on the rest of the module.
-SERIAL_SOURCES = ["taylor.cu"]
-DEPS = ["paces_b200.cu", "taylor.cu", "taylor.cuh", "engine.cu", "capi.cu", "engine.cuh", "sharded.cu", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "incremental.cu", "keys.cuh",
-        "primitives.cuh",
-        "host_model.hpp", os.path.join("..", "..", "include", "paces_b200.h")]
+# Separate translation units compiled in parallel (kernels live in headers with internal linkage).  No -split-compile
+# anywhere: with it ptxas gave the same source different register allocations from one build to the next (the Taylor
+# kernels: 32 or 40 registers, spills or none) -- up to 10 % of a step.
+SOURCES = ["engine.cu", "incremental.cu", "histogram.cu", "sharded.cu", "nccl_comm.cu", "capi.cu", "taylor.cu"]
+DEPS = SOURCES + ["taylor.cuh", "engine.cuh", "sharded.cuh", "kernels.cuh", "window.cuh", "incremental.cuh", "histogram.cuh",
+                  "keys.cuh", "primitives.cuh", "host_model.hpp", "nccl_comm.hpp",
+                  os.path.join("..", "..", "include", "paces_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
               "-Xcompiler", "-fPIC,-O2", "-shared"]
 
@@ -43,32 +42,39 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    objs = []
-    serial_flags = [f for f in NVCC_FLAGS if f != "-shared"]
-    for src in SERIAL_SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-diag-suppress", "177"]
+    if os.environ.get("PB200_ONLY_W"):  # development / profiling build restricted to one key width
+        flags += ["-DPB_ONLY_W=" + str(int(os.environ["PB200_ONLY_W"]))]
+    if verbose:
+        flags += ["-Xptxas", "-v"]
+    srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+
+    def compile_one(src):
         obj = os.path.join(HERE, "_" + os.path.splitext(src)[0] + ".o")
-        c = [_nvcc(), *serial_flags, "-c", "-o", obj, os.path.join(CSRC, src)] + (["-Xptxas", "-v"] if verbose else [])
-        r = subprocess.run(c, cwd=CSRC, capture_output=True, text=True)
+        r = subprocess.run([_nvcc(), *flags, "-c", "-o", obj, os.path.join(CSRC, src)], cwd=CSRC, capture_output=True,
+                           text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs = []
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed compiling " + src)
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + objs
-    if os.environ.get("PB200_ONLY_W"):  # development / profiling build restricted to one key width
-        cmd += ["-DPB_ONLY_W=" + str(int(os.environ["PB200_ONLY_W"]))]
-    if verbose:
-        cmd += ["-Xptxas", "-v"]
-    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    r = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-ldl"],
+                       cwd=CSRC, capture_output=True, text=True)
     for obj in objs:
         if os.path.exists(obj):
             os.remove(obj)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libpaces_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libpaces_b200.so")
     return LIB
 
 

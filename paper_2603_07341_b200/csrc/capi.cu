@@ -320,6 +320,18 @@ int pb200_expmv(pb200_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t
         e.upload_csr(tmp, n, row_ptr, col, val);
         e.aux_coeff.ensure(size_t(n) * 16 + 16);
         if (n) PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, c, size_t(n) * 16, cudaMemcpyHostToDevice, e.stream));
+        // a stand-alone operator must not disturb a resident run's batching heuristics, deferred scalars or counters
+        struct Restore {
+            Engine& e;
+            int last_order;
+            Engine::Ctl last_ctl;
+            pb200_phase_times times;
+            ~Restore() {
+                e.last_order = last_order;
+                e.last_ctl = last_ctl;
+                e.times = times;
+            }
+        } restore{e, e.last_order, e.last_ctl, e.times};
         e.last_order = 0;
         e.expmv(tmp, e.aux_coeff.as<double2>(), dt, rtol, max_order, substeps, order_used, last_term_norm, nullptr);
         if (n) PB_CUDA(cudaMemcpyAsync(c, e.aux_coeff.p, size_t(n) * 16, cudaMemcpyDeviceToHost, e.stream));
@@ -524,6 +536,19 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         c.entry_occ = nullptr;
         c.entry_amp = nullptr;
         const size_t W = e.hm.W;
+        {
+            // The input buffers are still being read (verification uploads, a redo after a cache miss) while the
+            // outputs are written: in-place calls are not supported.
+            auto overlap = [](const void* a, size_t na, const void* b, size_t nb) {
+                const char* pa = static_cast<const char*>(a);
+                const char* pb_ = static_cast<const char*>(b);
+                return na != 0 && nb != 0 && pa < pb_ + nb && pb_ < pa + na;
+            };
+            const size_t in_w = rows * W * 4, in_c = rows * 16, out_w = out_cap_rows * W * 4, out_c = out_cap_rows * 16;
+            need(!overlap(words, in_w, out_words, out_w) && !overlap(words, in_w, out_coeff, out_c) &&
+                     !overlap(coeff, in_c, out_words, out_w) && !overlap(coeff, in_c, out_coeff, out_c),
+                 "step_io: input and output buffers must not overlap (use two buffer sets and alternate)");
+        }
         Engine::StepIO io;
         io.out_words = out_words;
         io.out_coeff = out_coeff;
@@ -587,6 +612,7 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
                     // not the resident state after all: redo the step from the caller's buffers
                 } catch (...) {
                     cudaStreamSynchronize(e.io_stream);
+                    e.cfg = saved;
                     throw;
                 }
                 e.cfg = saved;

@@ -2,8 +2,6 @@
 #include <atomic>
 #include "engine.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include <cmath>
 
 namespace pb {
@@ -96,9 +94,11 @@ Engine::~Engine() {
 __global__ void publish_kernel(const uint32_t* __restrict__ src, uint32_t* dst, uint32_t nwords, uint32_t* flag,
                                uint32_t seq) {
     for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = __ldcg(src + i);
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) *(volatile uint32_t*)flag = seq;
+    __syncthreads();  // every thread's payload stores happen-before thread 0's fence ...
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // ... which orders them (cumulativity) before the flag at system scope
+        *(volatile uint32_t*)flag = seq;
+    }
 }
 
 void Engine::publish(const void* dptr, uint32_t nwords) {
@@ -456,7 +456,14 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
     check_launch();
     SelectCtl sc = read_back<SelectCtl>(&c->select);
     if (norm2_out) *norm2_out = sc.norm2;
-    if (sc.support == 0) throw PacesError("truncate_select: state has no support");
+    if (sc.support == 0) {
+        if (pending_words) {  // the reference checks sortedness first (engine.hpp:110-112)
+            PB_CUDA(cudaStreamWaitEvent(stream, ev_words, 0));
+            pending_words = false;
+            if (!rows_sorted_on_device(d_words, n)) throw PacesError("truncate_select: state table must be sorted");
+        }
+        throw PacesError("truncate_select: state has no support");
+    }
 
     uint32_t* keep = flag_keep.as<uint32_t>();
     uint64_t kept64 = sc.support;
@@ -668,11 +675,13 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
             batch = 2;
         }
         times.taylor_orders += uint64_t(tc.last_order);
+        times.taylor_rows += uint64_t(tc.last_order) * n;
         if (!converged)
             throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
                              "; reduce dt or increase substeps");
     }
     times.taylor_deferred += uint64_t(tc.deferred);
+    times.taylor_deferred_rows += uint64_t(tc.deferred) * n;
     last_order = tc.order_used;
     if (order_used) *order_used = tc.order_used;
     if (last_term_norm) *last_term_norm = tc.last_term_norm;
@@ -750,72 +759,6 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
             // but the 1/sqrt(L) factor was applied per rank, which is exact for the single non-zero term
             comm_check(ops.allreduce_f64_host(ops.user, amp, 2), "allreduce_f64_host");
         }
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// weight_histogram (observables.hpp:123-176).  Device: |c|^2 and a descending radix sort (CUB -- library code, off
-// the per-step path).  Host: the reference's serial loops over the sorted weights, so the quantile counts, the tail
-// slope (same libm log) and the sampled curve are the reference's bit for bit.
-// ------------------------------------------------------------------------------------------------
-void Engine::weight_histogram(const double2* cvec, uint32_t n, uint64_t bins, pb200_weight_hist* out, uint64_t* rank,
-                              double* weight, uint64_t cap, uint64_t* npts_out) {
-    Ctl* c = dctl();
-    weights.ensure(size_t(n) * 8 + 8);
-    sort_out.ensure(size_t(n) * 8 + 8);
-    PB_CUDA(cudaMemsetAsync(&c->select, 0, sizeof(SelectCtl), stream));
-    weights_kernel<<<grid_for(n), NT, 0, stream>>>(cvec, n, weights.as<double>(), partials.as<double>(), &c->select);
-    check_launch();
-    size_t tmp_bytes = 0;
-    PB_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp_bytes, weights.as<double>(), sort_out.as<double>(),
-                                                     int(n), 0, 64, stream));
-    sort_tmp.ensure(tmp_bytes + 16);
-    PB_CUDA(cub::DeviceRadixSort::SortKeysDescending(sort_tmp.p, tmp_bytes, weights.as<double>(),
-                                                     sort_out.as<double>(), int(n), 0, 64, stream));
-    ++launches;
-    const SelectCtl sc = read_back<SelectCtl>(&c->select);
-    const size_t m = size_t(sc.support);  // weights are >= 0: the positive ones lead the descending order
-    if (m == 0) throw PacesError("weight histogram: empty state");
-    std::vector<double> w(m);
-    PB_CUDA(cudaMemcpyAsync(w.data(), sort_out.p, m * 8, cudaMemcpyDeviceToHost, stream));
-    sync();
-    double total = 0.0;
-    for (double v : w) total += v;
-    uint64_t marks[4] = {m, m, m, m};
-    const double frac[4] = {0.50, 0.90, 0.99, 0.9999};
-    double running = 0;
-    size_t done = 0;
-    for (size_t i = 0; i < m && done < 4; ++i) {
-        running += w[i];
-        while (done < 4 && running >= frac[done] * total - 1e-15 * total) marks[done++] = i + 1;
-    }
-    out->support = m;
-    out->q50 = marks[0];
-    out->q90 = marks[1];
-    out->q99 = marks[2];
-    out->q9999 = marks[3];
-    out->tail_exponent = 0;
-    const size_t lo = m / 10;
-    if (m - lo >= 2) {
-        double sx = 0, sy = 0, sxx = 0, sxy = 0;
-        size_t cnt = 0;
-        for (size_t i = lo; i < m; ++i) {
-            const double x = std::log(double(i + 1)), y = std::log(w[i]);
-            sx += x;
-            sy += y;
-            sxx += x * x;
-            sxy += x * y;
-            ++cnt;
-        }
-        const double denom = cnt * sxx - sx * sx;
-        out->tail_exponent = denom != 0 ? (cnt * sxy - sx * sy) / denom : 0.0;
-    }
-    const size_t npts = (bins == 0 || m <= bins) ? m : size_t(bins);
-    if (npts_out) *npts_out = npts;
-    for (size_t k = 0; k < npts && k < cap; ++k) {
-        const size_t i = npts == 1 ? 0 : k * (m - 1) / (npts - 1);
-        if (rank) rank[k] = i + 1;
-        if (weight) weight[k] = w[i];
     }
 }
 
@@ -938,8 +881,9 @@ void Engine::run_step(pb200_diag* out) {
         defer_reads = (world == 1);
         // incremental adapt (incremental.cuh): needs the previous H_eff with its expansion flags; the full path
         // remains for the first step after a load, m = 0, a memory cap (its transcript accounting) and overflows
+        // (BFS distances are bytes with DIST_INF = 255: larger neighbour orders take the full path)
         bool incremental = world == 1 && (!io || io->cached) && old.has_h && old.has_full && cfg.m >= 1 &&
-                           memory_cap_bytes() == 0 &&
+                           cfg.m <= INC_MAX_ORDER && memory_cap_bytes() == 0 &&
                            std::getenv("PB200_NO_INCREMENTAL") == nullptr;
         const uint32_t kept = world > 1
                                   ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
@@ -1049,6 +993,10 @@ void Engine::run_step(pb200_diag* out) {
         PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[6]));
         times.total_ms += ms;
         times.spmv_nnz += uint64_t(order) * next.nnz;
+        times.rows_sum += next.n;
+        times.nnz_sum += next.nnz;
+        times.rows_old_sum += old.n;
+        times.kept_sum += kept;
     }
     t = t + cfg.dt;
     rec.t = t;

@@ -337,7 +337,9 @@ struct Engine {
     void upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val);
     void observe(const uint32_t* words, const double2* c, uint32_t n, double* density, double* amp, double* phonons);
 
-    /// weight_histogram (observables.hpp:123-176): GPU sort of the weights, reference loops on the host
+    /// weight_histogram (observables.hpp:123-176), entirely on the device (histogram.cuh); only the sampled curve and
+    /// a 64-byte result block are downloaded
+    DevBuf hist_counts, hist_tiles, hist_res, hist_curve;
     void weight_histogram(const double2* c, uint32_t n, uint64_t bins, pb200_weight_hist* out, uint64_t* rank,
                           double* weight, uint64_t cap, uint64_t* npts);
 

@@ -20,6 +20,7 @@
 namespace pb {
 
 constexpr uint8_t DIST_INF = 255;
+constexpr int INC_MAX_ORDER = 250;  // distances are bytes: m + 1 must stay below DIST_INF
 constexpr uint32_t IDX_NONE = 0xffffffffu;
 
 struct IncCounters {
@@ -30,14 +31,14 @@ struct IncCounters {
 };
 
 /// dist[i] = 0 for kept rows, INF otherwise.
-__global__ void __launch_bounds__(NT) inc_init_dist_kernel(const uint32_t* __restrict__ keep, uint32_t n,
+static __global__ void __launch_bounds__(NT) inc_init_dist_kernel(const uint32_t* __restrict__ keep, uint32_t n,
                                                            uint8_t* __restrict__ dist) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) dist[i] = keep[i] ? 0 : DIST_INF;
 }
 
 /// One BFS level in old index space: rows at distance k either spread k+1 along their CSR row (complete
 /// neighbourhood) or are queued for key-based expansion.  Concurrent byte stores of the same value are benign.
-__global__ void __launch_bounds__(NT) inc_mark_level_kernel(uint32_t n, int k, const uint8_t* __restrict__ full,
+static __global__ void __launch_bounds__(NT) inc_mark_level_kernel(uint32_t n, int k, const uint8_t* __restrict__ full,
                                                             const uint32_t* __restrict__ row_ptr,
                                                             const int32_t* __restrict__ col, uint8_t* dist,
                                                             uint32_t* __restrict__ elist, IncCounters* ctr) {
@@ -67,7 +68,7 @@ __device__ __forceinline__ bool side_find(const uint32_t* __restrict__ side_keys
 /// distance k.  A neighbour found in the old table gets distance k+1; one found in the side list is already known;
 /// anything else becomes a candidate with its insertion gap in the OLD table (gap_count feeds the dedup machinery).
 template <int W>
-__global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
                                                         const uint32_t* __restrict__ elist,
                                                         const uint32_t* __restrict__ n_elist_ptr,
                                                         const uint32_t* __restrict__ side_keys,
@@ -107,13 +108,13 @@ __global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const uint32
 
 /// After an overflowing expansion the candidate counter exceeds the buffer: clamp it so the dedup kernels stay in
 /// bounds (the step is discarded anyway -- IncCounters::overflow is set).
-__global__ void inc_clamp_kernel(uint32_t* n_cand, uint32_t cap) {
+static __global__ void inc_clamp_kernel(uint32_t* n_cand, uint32_t cap) {
     if (*n_cand > cap) *n_cand = cap;
 }
 
 /// Unique candidates of one level in canonical order: survivor of gap g with rank r -> index kept_before[g] + r.
 template <int W>
-__global__ void __launch_bounds__(NT) inc_emit_unique_kernel(const uint32_t* __restrict__ cand_keys,
+static __global__ void __launch_bounds__(NT) inc_emit_unique_kernel(const uint32_t* __restrict__ cand_keys,
                                                              const uint32_t* __restrict__ cand_gap,
                                                              const uint32_t* __restrict__ perm,
                                                              const uint32_t* __restrict__ seg_rank,
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(NT) inc_emit_unique_kernel(const uint32_t* __r
 /// Merge of two sorted, disjoint key lists A (side so far) and B (this level's new keys, distance `kb`):
 /// out index of A[j] = j + #B < A[j], of B[t] = t + #A < B[t].
 template <int W>
-__global__ void __launch_bounds__(NT) inc_side_merge_kernel(const uint32_t* __restrict__ a_keys,
+static __global__ void __launch_bounds__(NT) inc_side_merge_kernel(const uint32_t* __restrict__ a_keys,
                                                             const uint32_t* __restrict__ a_gap,
                                                             const uint8_t* __restrict__ a_dist, uint32_t na,
                                                             const uint32_t* __restrict__ b_keys,
@@ -165,14 +166,14 @@ __global__ void __launch_bounds__(NT) inc_side_merge_kernel(const uint32_t* __re
 }
 
 /// keepflag[i] = dist[i] <= m (n+1 entries, trailing 0, scanned in place afterwards).
-__global__ void __launch_bounds__(NT) inc_keepflag_kernel(const uint8_t* __restrict__ dist, uint32_t n, int m,
+static __global__ void __launch_bounds__(NT) inc_keepflag_kernel(const uint8_t* __restrict__ dist, uint32_t n, int m,
                                                           uint32_t* __restrict__ keepflag) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i <= n; i += gridDim.x * NT)
         keepflag[i] = (i < n && dist[i] <= uint8_t(m)) ? 1u : 0u;
 }
 
 /// cntgap[gap]++ for every side key (array zeroed before; scanned afterwards).
-__global__ void __launch_bounds__(NT) inc_count_gaps_kernel(const uint32_t* __restrict__ side_gap, uint32_t side_n,
+static __global__ void __launch_bounds__(NT) inc_count_gaps_kernel(const uint32_t* __restrict__ side_gap, uint32_t side_n,
                                                             uint32_t* __restrict__ cntgap) {
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < side_n; j += gridDim.x * NT) atomicAdd(cntgap + side_gap[j], 1u);
 }
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NT) inc_count_gaps_kernel(const uint32_t* __re
 /// New index of every old row (IDX_NONE when dropped), `full` flags of the new space, and the coefficient remap
 /// fused in: kept rows carry their coefficient, dropped rows add |c|^2 to the discarded weight.
 /// pk = exclusive scan of keepflag, nb = exclusive scan of cntgap (side keys with gap <= i precede row i).
-__global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const double2* __restrict__ c_old, uint32_t n, int m,
+static __global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const double2* __restrict__ c_old, uint32_t n, int m,
                                                              const uint8_t* __restrict__ dist,
                                                              const uint32_t* __restrict__ pk,
                                                              const uint32_t* __restrict__ nb,
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(NT) inc_scatter_old_kernel(const double2* __re
 /// The surviving old rows into the new table, one thread per WORD: surviving rows come in long runs, so both the
 /// reads and the writes are coalesced whatever the key width (a thread per row moves 4W bytes at a 4W-byte stride).
 template <int W>
-__global__ void __launch_bounds__(NT) inc_copy_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) inc_copy_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
                                                            const uint32_t* __restrict__ newidx,
                                                            uint32_t* __restrict__ out_table) {
     const uint64_t total = uint64_t(n) * W;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(NT) inc_copy_rows_kernel(const uint32_t* __res
 
 /// Side keys into the new table (c_new was zeroed: they start with zero amplitude).
 template <int W>
-__global__ void __launch_bounds__(NT) inc_scatter_side_kernel(const uint32_t* __restrict__ side_keys,
+static __global__ void __launch_bounds__(NT) inc_scatter_side_kernel(const uint32_t* __restrict__ side_keys,
                                                               const uint32_t* __restrict__ side_gap,
                                                               const uint8_t* __restrict__ side_dist, uint32_t side_n,
                                                               int m, const uint32_t* __restrict__ pk,
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(NT) inc_scatter_side_kernel(const uint32_t* __
 /// side list.  An old-row neighbour also receives the symmetric entry (extras slots of that row: x_col/x_val with
 /// stride `width`, counted in x_cnt).
 template <int W>
-__global__ void __launch_bounds__(NT) inc_side_rows_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) inc_side_rows_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
                                                            const uint32_t* __restrict__ newidx,
                                                            const uint32_t* __restrict__ side_keys,
                                                            const uint32_t* __restrict__ side_newidx, uint32_t side_n,
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(NT) inc_side_rows_kernel(ModelDev m, const uin
 }
 
 /// Row lengths of the new CSR (written at the NEW row index; every new row is written exactly once).
-__global__ void __launch_bounds__(NT) inc_row_len_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
+static __global__ void __launch_bounds__(NT) inc_row_len_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
                                                          const uint32_t* __restrict__ row_ptr,
                                                          const int32_t* __restrict__ col,
                                                          const uint32_t* __restrict__ x_cnt,
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(NT) inc_row_len_kernel(uint32_t n, const uint3
 
 /// Entries of the new CSR.  Old rows: the old entries whose column survives, renumbered (a monotone map, so they
 /// stay ascending), merged with the row's extras (a handful, insertion-sorted by column).  Side rows: copied.
-__global__ void __launch_bounds__(NT) inc_fill_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
+static __global__ void __launch_bounds__(NT) inc_fill_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
                                                       const uint32_t* __restrict__ row_ptr,
                                                       const int32_t* __restrict__ col, const double* __restrict__ val,
                                                       int width, const uint32_t* __restrict__ x_col,
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(NT) inc_fill_kernel(uint32_t n, const uint32_t
 /// takes 32 consecutive OLD rows, whose entries are one contiguous run of CSR_old; every lane moves entries of that
 /// run (the source row of an entry is found by a 5-step search over the 32 row offsets, as in
 /// assemble_compact_kernel), renumbering the column through the index map.
-__global__ void __launch_bounds__(NT) inc_fill_simple_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
+static __global__ void __launch_bounds__(NT) inc_fill_simple_kernel(uint32_t n, const uint32_t* __restrict__ newidx,
                                                              const uint32_t* __restrict__ row_ptr,
                                                              const int32_t* __restrict__ col,
                                                              const double* __restrict__ val,
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(NT) inc_fill_simple_kernel(uint32_t n, const u
 }
 
 /// full[i] = 1 everywhere, then 0 for the rows listed (the final frontier of a full grow_subspace).
-__global__ void __launch_bounds__(NT) inc_clear_full_kernel(const uint32_t* __restrict__ rows, uint32_t cnt,
+static __global__ void __launch_bounds__(NT) inc_clear_full_kernel(const uint32_t* __restrict__ rows, uint32_t cnt,
                                                             uint8_t* __restrict__ full) {
     for (uint32_t t = blockIdx.x * NT + threadIdx.x; t < cnt; t += gridDim.x * NT) full[rows[t]] = 0;
 }

@@ -35,7 +35,7 @@ struct GrowCounters {
 // ================================================================================================
 
 /// perm[seg_start[gap] + k] = candidate id, k = arrival order inside the gap (gap_fill starts at zero).
-__global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap,
+static __global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap,
                                                               const uint32_t* __restrict__ nc_ptr,
                                                               const uint32_t* __restrict__ seg_start,
                                                               uint32_t* __restrict__ gap_fill,
@@ -54,7 +54,7 @@ constexpr uint32_t SEG_DUP = 0xffffffffu;
 /// at a smaller slot (which copy survives is irrelevant: they are the same key).  seg_rank[s] = SEG_DUP
 /// for dropped duplicates, 0 otherwise; gap_kept[g] += 1 per survivor.
 template <int W>
-__global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __restrict__ cand_keys,
+static __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __restrict__ cand_keys,
                                                            const uint32_t* __restrict__ cand_gap,
                                                            const uint32_t* __restrict__ perm,
                                                            const uint32_t* __restrict__ nc_ptr,
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __res
 /// Survivors get rank = number of surviving smaller keys in their segment = canonical position inside
 /// the gap.  Readers only test a slot for SEG_DUP, which a concurrent rank write never produces.
 template <int W>
-__global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __restrict__ cand_keys,
+static __global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __restrict__ cand_keys,
                                                           const uint32_t* __restrict__ cand_gap,
                                                           const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ nc_ptr,
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __rest
 /// indices of the new keys in the merged table).   (sort_unique_rows + diff_rows + merge_rows,
 /// basis_codec.hpp:247-321, in one pass.)
 template <int W>
-__global__ void __launch_bounds__(NT) merge_old_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) merge_old_rows_kernel(const uint32_t* __restrict__ table, uint32_t n,
                                                             const uint32_t* __restrict__ kept_before,
                                                             uint32_t* __restrict__ out) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(NT) merge_old_rows_kernel(const uint32_t* __re
 }
 
 template <int W>
-__global__ void __launch_bounds__(NT) merge_new_rows_kernel(const uint32_t* __restrict__ cand_keys,
+static __global__ void __launch_bounds__(NT) merge_new_rows_kernel(const uint32_t* __restrict__ cand_keys,
                                                             const uint32_t* __restrict__ cand_gap,
                                                             const uint32_t* __restrict__ perm,
                                                             const uint32_t* __restrict__ seg_rank,
@@ -150,7 +150,7 @@ constexpr int MAX_ROW = 2 * 3 + 3;  // hops (<= 6) + 2 ladder + diagonal
 /// consecutive rows: their entries form ONE contiguous run of the CSR arrays, so the lanes write it with
 /// coalesced stores; the source row of an entry is found by a 5-step search over the 32 row offsets held in
 /// registers (shuffles).
-__global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int width, const uint32_t* __restrict__ tmp_col,
+static __global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int width, const uint32_t* __restrict__ tmp_col,
                                                               const double* __restrict__ tmp_val,
                                                               const uint32_t* __restrict__ row_ptr,
                                                               int32_t* __restrict__ col, double* __restrict__ val) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n, int wi
 // K4  fused Taylor order: taylor.cuh / taylor.cu (own translation unit)
 // ================================================================================================
 /// Plain y = H x (csr_matvec, subspace.hpp:35-43).
-__global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+static __global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                   const int32_t* __restrict__ col, const double* __restrict__ val,
                                                   const double2* __restrict__ x, double2* __restrict__ y) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __
 // K5  <x|H|x> (csr_expectation, subspace.hpp:46-55) fused with |x|^2 and the finiteness check of
 //     expmv (propagator.hpp:55-57).  out[0] = <x|H|x>, out[1] = sum |x|^2, out[2] = #non-finite.
 // ================================================================================================
-__global__ void __launch_bounds__(NT) expectation_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+static __global__ void __launch_bounds__(NT) expectation_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                          const int32_t* __restrict__ col,
                                                          const double* __restrict__ val,
                                                          const double2* __restrict__ x, double* __restrict__ partials,
@@ -253,7 +253,7 @@ struct SelectCtl {
 };
 
 /// w_i = re^2 + im^2 (std::norm), sum and support count.
-__global__ void __launch_bounds__(NT) weights_kernel(const double2* __restrict__ c, uint32_t n, double* __restrict__ w,
+static __global__ void __launch_bounds__(NT) weights_kernel(const double2* __restrict__ c, uint32_t n, double* __restrict__ w,
                                                      double* __restrict__ partials, SelectCtl* ctl) {
     __shared__ double smem[NT / 32];
     double acc[2] = {0.0, 0.0};
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(NT) weights_kernel(const double2* __restrict__
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 
-__global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restrict__ w, uint32_t n, int shift, int width,
+static __global__ void __launch_bounds__(NT) select_pass_kernel(const double* __restrict__ w, uint32_t n, int shift, int width,
                                                          SelectCtl* ctl, uint32_t* __restrict__ hist, int fuse_pick) {
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ uint32_t wsum[NT / 32];
@@ -382,7 +382,7 @@ __device__ __forceinline__ void hist_add_aggregated(uint32_t* sh, uint32_t digit
 /// Selection pass 1 fused with the weights: w_i = re^2 + im^2 (std::norm, engine.hpp:113-116), their sum, the
 /// support count, and the histogram of the top 11 bits (sign + exponent) of the positive weights.  The last CTA
 /// to finish stores norm2 / support and, when support > q_nom (= ctl->k on entry), picks the first digit.
-__global__ void __launch_bounds__(NT) weights_hist_kernel(const double2* __restrict__ c, uint32_t n,
+static __global__ void __launch_bounds__(NT) weights_hist_kernel(const double2* __restrict__ c, uint32_t n,
                                                           double* __restrict__ w, double* __restrict__ partials,
                                                           SelectCtl* ctl, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[SEL_BINS];
@@ -428,7 +428,7 @@ constexpr uint32_t SEL_LIST_CAP = 1u << 16;
 /// After the first two digits (22 bits) the group that still contains the cutoff is almost always tiny: gather
 /// its members' bit patterns so one CTA can finish the remaining 42 bits.  Does nothing when the group is larger
 /// than the list (massive exact ties): the host then falls back to full passes.
-__global__ void __launch_bounds__(NT) select_gather_kernel(const double* __restrict__ w, uint32_t n, int hi_shift,
+static __global__ void __launch_bounds__(NT) select_gather_kernel(const double* __restrict__ w, uint32_t n, int hi_shift,
                                                            SelectCtl* ctl, unsigned long long* __restrict__ list) {
     if (ctl->support <= ctl->k) return;  // nothing is cut (after a pick the wanted rank is below the support)
     if (ctl->count_eq > SEL_LIST_CAP) return;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NT) select_gather_kernel(const double* __restr
 }
 
 /// Single CTA: remaining digits (shifts 31, 20, 9, 0; widths 11, 11, 11, 9) over the gathered list.
-__global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long long* __restrict__ list, SelectCtl* ctl) {
+static __global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long long* __restrict__ list, SelectCtl* ctl) {
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ uint32_t wsum[NT / 32];
     const uint32_t cnt = ctl->list_n;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long lon
 
 /// mode 0: keep every supported row (w > 0).  mode 1: keep w > cutoff, and w == cutoff too when
 /// keep_ties; otherwise the ties are flagged separately for the host-side Fisher-Yates draw.
-__global__ void __launch_bounds__(NT) select_flags_kernel(const double* __restrict__ w, uint32_t n, int mode,
+static __global__ void __launch_bounds__(NT) select_flags_kernel(const double* __restrict__ w, uint32_t n, int mode,
                                                           const SelectCtl* __restrict__ ctl, int keep_ties,
                                                           uint32_t* __restrict__ keep, uint32_t* __restrict__ tie) {
     const unsigned long long cut = ctl->prefix;
@@ -499,21 +499,21 @@ __global__ void __launch_bounds__(NT) select_flags_kernel(const double* __restri
 }
 
 /// idx[pos[i]] = i for flagged i (order preserving).
-__global__ void __launch_bounds__(NT) compact_index_kernel(const uint32_t* __restrict__ flag,
+static __global__ void __launch_bounds__(NT) compact_index_kernel(const uint32_t* __restrict__ flag,
                                                            const uint32_t* __restrict__ pos, uint32_t n,
                                                            uint32_t* __restrict__ idx) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT)
         if (flag[i]) idx[pos[i]] = i;
 }
 
-__global__ void set_flags_kernel(const uint32_t* __restrict__ idx, uint32_t cnt, uint32_t* __restrict__ flag) {
+static __global__ void set_flags_kernel(const uint32_t* __restrict__ idx, uint32_t cnt, uint32_t* __restrict__ flag) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) flag[idx[i]] = 1;
 }
 
 /// out[pos[i]] = table[i] for flagged rows: ascending indices of a sorted parent stay sorted
 /// (engine.hpp:146-155).
 template <int W>
-__global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __restrict__ table,
+static __global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __restrict__ table,
                                                           const uint32_t* __restrict__ flag,
                                                           const uint32_t* __restrict__ pos, uint32_t n,
                                                           uint32_t* __restrict__ out) {
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(NT) compact_rows_kernel(const uint32_t* __rest
 /// site are contiguous: a CTA's chunk touches only a few sites and reduces each with the fixed tree.
 /// block_part[(blockIdx, site)] partial sums are combined in CTA order by density_finish_kernel.
 template <int W>
-__global__ void __launch_bounds__(NT) density_kernel(ModelDev m, const uint32_t* __restrict__ table,
+static __global__ void __launch_bounds__(NT) density_kernel(ModelDev m, const uint32_t* __restrict__ table,
                                                      const double2* __restrict__ c, uint32_t n,
                                                      uint32_t rows_per_block, double* __restrict__ block_part) {
     __shared__ double smem[NT / 32];
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(NT) density_kernel(ModelDev m, const uint32_t*
 
 /// density[site] = sum over CTAs in ascending order; one thread per site.  block_part must be zeroed
 /// before density_kernel.
-__global__ void density_finish_kernel(const double* __restrict__ block_part, uint32_t nblocks, int L,
+static __global__ void density_finish_kernel(const double* __restrict__ block_part, uint32_t nblocks, int L,
                                       double* __restrict__ density) {
     const int site = blockIdx.x * blockDim.x + threadIdx.x;
     if (site >= L) return;
@@ -575,7 +575,7 @@ __global__ void density_finish_kernel(const double* __restrict__ block_part, uin
 /// amp = (1/sqrt(L)) sum_j c[find_row(|j; vacuum>)], summed in ascending j by one thread after the
 /// L look-ups ran in parallel.
 template <int W>
-__global__ void dipole_kernel(ModelDev m, const uint32_t* __restrict__ table, const double2* __restrict__ c,
+static __global__ void dipole_kernel(ModelDev m, const uint32_t* __restrict__ table, const double2* __restrict__ c,
                               uint32_t n, double2* __restrict__ found, double* __restrict__ out) {
     for (int j = threadIdx.x; j < m.L; j += blockDim.x) {
         Key<W> k;
@@ -600,7 +600,7 @@ __global__ void dipole_kernel(ModelDev m, const uint32_t* __restrict__ table, co
 
 /// n_j = sum_i |c_i|^2 * occ_j(i); per-CTA partials for all L sites, combined by density_finish_kernel.
 template <int W>
-__global__ void __launch_bounds__(NT) phonon_numbers_kernel(ModelDev m, const uint32_t* __restrict__ table,
+static __global__ void __launch_bounds__(NT) phonon_numbers_kernel(ModelDev m, const uint32_t* __restrict__ table,
                                                             const double2* __restrict__ c, uint32_t n,
                                                             uint32_t rows_per_block, double* __restrict__ block_part) {
     __shared__ double smem[NT / 32];
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(NT) phonon_numbers_kernel(ModelDev m, const ui
 
 /// apply_terms for a batch of keys (lattice_models.hpp:212-267), canonical neighbour order.
 template <int W>
-__global__ void apply_terms_kernel(ModelDev m, const uint32_t* __restrict__ keys, uint32_t n, int cap,
+static __global__ void apply_terms_kernel(ModelDev m, const uint32_t* __restrict__ keys, uint32_t n, int cap,
                                    uint32_t* __restrict__ out_keys, double* __restrict__ out_amps,
                                    int* __restrict__ count) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -642,7 +642,7 @@ __global__ void apply_terms_kernel(ModelDev m, const uint32_t* __restrict__ keys
 
 /// bad[0] != 0 unless the rows are strictly ascending (PackedBasisTable::sorted, basis_codec.hpp:211).
 template <int W>
-__global__ void __launch_bounds__(NT) check_sorted_kernel(const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) check_sorted_kernel(const uint32_t* __restrict__ table, uint32_t n,
                                                           uint32_t* __restrict__ bad) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i + 1 < n; i += gridDim.x * NT) {
         const Key<W> a = load_key<W>(table + size_t(i) * W), b = load_key<W>(table + size_t(i + 1) * W);
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(NT) check_sorted_kernel(const uint32_t* __rest
 
 /// flag[0] = 1 unless the two word arrays are bitwise identical (host-buffer step: is the state the caller hands
 /// in the one this context produced last?).
-__global__ void __launch_bounds__(NT) words_differ_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+static __global__ void __launch_bounds__(NT) words_differ_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                                           uint64_t n_words, uint32_t* __restrict__ flag) {
     bool diff = false;
     for (uint64_t i = uint64_t(blockIdx.x) * NT + threadIdx.x; i < n_words; i += uint64_t(gridDim.x) * NT)
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(NT) words_differ_kernel(const uint32_t* __rest
 }
 
 /// L2 flush for benchmarking: streams a buffer larger than L2.
-__global__ void flush_kernel(double* __restrict__ buf, size_t n) {
+static __global__ void flush_kernel(double* __restrict__ buf, size_t n) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         buf[i] = buf[i] + 1.0;
 }

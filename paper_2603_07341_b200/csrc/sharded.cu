@@ -464,6 +464,7 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
             batch = 2;
         }
         times.taylor_orders += uint64_t(tc.last_order);
+        times.taylor_rows += uint64_t(tc.last_order) * n;
         if (!converged)
             throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
                              "; reduce dt or increase substeps");

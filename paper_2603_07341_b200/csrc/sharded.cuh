@@ -22,7 +22,7 @@ struct ShardCounters {
 /// expand_window_kernel (look-up, candidate + gap when absent); the others are appended to the outgoing list
 /// with their destination rank.
 template <int W>
-__global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
+static __global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
     ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n,
     const uint32_t* __restrict__ frontier, uint32_t nf, uint32_t chunk, uint32_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_gap, uint32_t cand_cap, uint32_t* __restrict__ gap_count, GrowCounters* ctr,
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
 }
 
 /// counts[dest[i]]++ (P is tiny: shared-memory histogram per CTA).
-__global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restrict__ dest, uint32_t cnt, uint32_t P,
+static __global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restrict__ dest, uint32_t cnt, uint32_t P,
                                                          uint32_t* __restrict__ counts) {
     __shared__ uint32_t sh[64];
     if (threadIdx.x < 64) sh[threadIdx.x] = 0;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restr
 }
 
 /// pos[i] = displ[dest[i]] + arrival order inside the bucket; fill[] starts at zero.
-__global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restrict__ dest, uint32_t cnt,
+static __global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restrict__ dest, uint32_t cnt,
                                                          const uint32_t* __restrict__ displ,
                                                          uint32_t* __restrict__ fill, uint32_t* __restrict__ pos) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) {
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restr
 }
 
 template <int W>
-__global__ void __launch_bounds__(NT) route_scatter_keys_kernel(const uint32_t* __restrict__ keys,
+static __global__ void __launch_bounds__(NT) route_scatter_keys_kernel(const uint32_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ pos, uint32_t cnt,
                                                                 uint32_t* __restrict__ send) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT)
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(NT) route_scatter_keys_kernel(const uint32_t* 
 
 /// Keys received from other ranks during expansion: those absent from the local table become candidates.
 template <int W>
-__global__ void __launch_bounds__(NT) classify_received_kernel(const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) classify_received_kernel(const uint32_t* __restrict__ table, uint32_t n,
                                                                const uint32_t* __restrict__ recv, uint32_t nr,
                                                                uint32_t* __restrict__ cand_keys,
                                                                uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(NT) classify_received_kernel(const uint32_t* _
 /// look-up request; its scratch column holds COL_REQ | request id until the replies arrive.  Entries stay
 /// in ascending NEIGHBOUR-KEY order (the reference's summation order), whatever their final column.
 template <int W>
-__global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
+static __global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
     ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n, uint32_t chunk, int width,
     uint32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, uint32_t* __restrict__ tmp_cnt,
     uint32_t* __restrict__ req_keys, uint32_t* __restrict__ req_dest, uint32_t req_cap, ShardCounters* sc) {
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
 /// Owner side of the look-up exchange: answer[j] = local row of the requested key or COL_ABSENT;
 /// found[j] = 1/0 (scanned afterwards to build the halo send list).
 template <int W>
-__global__ void __launch_bounds__(NT) answer_requests_kernel(const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) answer_requests_kernel(const uint32_t* __restrict__ table, uint32_t n,
                                                              const uint32_t* __restrict__ recv, uint32_t nr,
                                                              uint32_t* __restrict__ answer,
                                                              uint32_t* __restrict__ found) {
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(NT) answer_requests_kernel(const uint32_t* __r
 }
 
 /// send_idx[found_pos[j]] = answer[j] for found requests (order preserving).
-__global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __restrict__ answer,
+static __global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __restrict__ answer,
                                                              const uint32_t* __restrict__ found_pos, uint32_t nr,
                                                              uint32_t* __restrict__ send_idx) {
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < nr; j += gridDim.x * NT)
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __r
 }
 
 /// Requester side: reply[] is in send (bucketed) order.  flag[p] = reply found; scanned into halo slots.
-__global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* __restrict__ reply, uint32_t nreq,
+static __global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* __restrict__ reply, uint32_t nreq,
                                                          uint32_t* __restrict__ flag) {
     for (uint32_t p = blockIdx.x * NT + threadIdx.x; p < nreq; p += gridDim.x * NT)
         flag[p] = (reply[p] != COL_ABSENT) ? 1u : 0u;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* __restr
 
 /// Resolves the COL_REQ markers: found -> n_local + halo slot, absent -> COL_ABSENT; counts the surviving
 /// entries per row.
-__global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int width, uint32_t* __restrict__ tmp_col,
+static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int width, uint32_t* __restrict__ tmp_col,
                                                               const uint32_t* __restrict__ tmp_cnt,
                                                               const uint32_t* __restrict__ req_pos,
                                                               const uint32_t* __restrict__ reply,
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int wi
 }
 
 /// Pass 2 on a shard: compacts the scratch into CSR, skipping absent remote neighbours.
-__global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
+static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
                                                                       const uint32_t* __restrict__ tmp_col,
                                                                       const double* __restrict__ tmp_val,
                                                                       const uint32_t* __restrict__ tmp_cnt,
@@ -243,14 +243,14 @@ __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n
 }
 
 /// Halo pack: send[j] = x[send_idx[j]].
-__global__ void __launch_bounds__(NT) halo_pack_kernel(const double2* __restrict__ x,
+static __global__ void __launch_bounds__(NT) halo_pack_kernel(const double2* __restrict__ x,
                                                        const uint32_t* __restrict__ send_idx, uint32_t cnt,
                                                        double2* __restrict__ send) {
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < cnt; j += gridDim.x * NT) send[j] = x[send_idx[j]];
 }
 
 /// Stop rule of propagator.hpp:76-84 on globally reduced sums tot = (|term|^2, |c|^2).
-__global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restrict__ tot, int order, double rtol) {
+static __global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restrict__ tot, int order, double rtol) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (ctl->done) return;
     const double tn = __dsqrt_rn(tot[0]), rn = __dsqrt_rn(tot[1]);
@@ -265,7 +265,7 @@ __global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restrict__ to
 
 /// Marks the locally owned keys among the globally selected tie keys (truncate_select, engine.hpp:137-142).
 template <int W>
-__global__ void __launch_bounds__(NT) mark_selected_kernel(ModelDev m, uint32_t rank, uint32_t P,
+static __global__ void __launch_bounds__(NT) mark_selected_kernel(ModelDev m, uint32_t rank, uint32_t P,
                                                            const uint32_t* __restrict__ table, uint32_t n,
                                                            const uint32_t* __restrict__ sel, uint32_t ns,
                                                            uint32_t* __restrict__ keep) {
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NT) mark_selected_kernel(ModelDev m, uint32_t 
 /// Gathers the keys of flagged rows (order preserving): out[pos[i]] = table[i].  (= compact_rows_kernel)
 
 /// Pick step of the radix select on an ALL-REDUCED histogram (one CTA); see select_pass_kernel.
-__global__ void __launch_bounds__(NT) select_pick_global_kernel(uint32_t* __restrict__ hist, int width, SelectCtl* ctl) {
+static __global__ void __launch_bounds__(NT) select_pick_global_kernel(uint32_t* __restrict__ hist, int width, SelectCtl* ctl) {
     __shared__ uint32_t wsum[NT / 32];
     constexpr int PER = SEL_BINS / NT;
     uint32_t loc[PER];

@@ -241,7 +241,7 @@ __device__ __forceinline__ void for_each_move_warp(const ModelDev& m, const Key<
 /// together with their insertion gap.  gap_count[g] counts the candidates that fall between table rows g-1 and g.
 /// A warp walks 32*chunk consecutive frontier rows, 32 at a time.  frontier == nullptr means "all rows".
 template <int W>
-__global__ void __launch_bounds__(NT) expand_window_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) expand_window_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
                                                            const uint32_t* __restrict__ frontier, uint32_t nf,
                                                            uint32_t chunk, uint32_t* __restrict__ cand_keys,
                                                            uint32_t* __restrict__ cand_gap, uint32_t cand_cap,
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NT) expand_window_kernel(ModelDev m, const uin
 /// are generated in ascending key order, so the found columns are already ascending.  Results are parked in
 /// fixed-width scratch (stride `width`) and compacted by assemble_compact_kernel.
 template <int W>
-__global__ void __launch_bounds__(NT) assemble_window_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
+static __global__ void __launch_bounds__(NT) assemble_window_kernel(ModelDev m, const uint32_t* __restrict__ table, uint32_t n,
                                                              uint32_t chunk, int width, uint32_t* __restrict__ tmp_col,
                                                              double* __restrict__ tmp_val,
                                                              uint32_t* __restrict__ row_len) {
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(NT) assemble_window_kernel(ModelDev m, const u
 //     coefficient when the key is present, otherwise add |c|^2 to the discarded weight.  dst must be zeroed.
 // ================================================================================================
 template <int W>
-__global__ void __launch_bounds__(NT) remap_window_kernel(const uint32_t* __restrict__ src_table,
+static __global__ void __launch_bounds__(NT) remap_window_kernel(const uint32_t* __restrict__ src_table,
                                                           const double2* __restrict__ src_c, uint32_t ns,
                                                           const uint32_t* __restrict__ dst_table, uint32_t nd,
                                                           uint32_t chunk, double2* __restrict__ dst_c,
