@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libpaces_b200.so")
+_LIB_PATH = os.environ.get("PB200_LIB") or os.path.join(HERE, "libpaces_b200.so")  # PB200_LIB: A/B builds
 
 u32p = C.POINTER(C.c_uint32)
 i32p = C.POINTER(C.c_int32)

@@ -13,7 +13,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libpaces_b200.so")
+LIB = os.environ.get("PB200_LIB_OUT") or os.path.join(HERE, "libpaces_b200.so")
 # Separate translation units compiled in parallel (kernels live in headers with internal linkage).  No -split-compile
 # anywhere: with it ptxas gave the same source different register allocations from one build to the next (the Taylor
 # kernels: 32 or 40 registers, spills or none) -- up to 10 % of a step.
@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-diag-suppress", "177"]
     if os.environ.get("PB200_ONLY_W"):  # development / profiling build restricted to one key width
         flags += ["-DPB_ONLY_W=" + str(int(os.environ["PB200_ONLY_W"]))]
+    flags += os.environ.get("PB200_EXTRA_NVCC_FLAGS", "").split()  # experiments (e.g. -DTILE_TR=128)
     if verbose:
         flags += ["-Xptxas", "-v"]
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]

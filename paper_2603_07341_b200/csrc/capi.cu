@@ -766,7 +766,7 @@ int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush, double dt, double*
             taylor_launch_single(false, e.grid_for(n), e.sm_count, e.stream, n, sp.row_ptr.as<uint32_t>(),
                                  sp.col.as<int32_t>(), sp.val.as<double>(), e.term[(o - 1) & 1].as<double2>(),
                                  e.term[o & 1].as<double2>(), e.aux_coeff.as<double2>(), -dt / double(o), o, 1e-15,
-                                 e.partials.as<double>(), &c->taylor, 1, nullptr, nullptr);
+                                 e.partials.as<double>(), &c->taylor, 1, nullptr, nullptr, sp.max_row);
             e.check_launch();
             PB_CUDA(cudaEventRecord(e.ev[9], e.stream));
             e.sync();

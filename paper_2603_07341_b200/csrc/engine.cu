@@ -396,7 +396,7 @@ void Engine::assemble(Space& sp) {
     const int width = row_width;
     tmp_col.ensure(size_t(n) * width * 4);
     tmp_val.ensure(size_t(n) * width * 8);
-    sp.row_ptr.ensure((size_t(n) + 1) * 4);
+    sp.row_ptr.ensure((size_t(n) + 1) * 4 + CSR_PAD);
     const uint32_t achunk = chunk_for(n);
     PB_DISPATCH_W(W, assemble_window_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
                          md, sp.words.as<uint32_t>(), n, achunk, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
@@ -408,20 +408,21 @@ void Engine::assemble(Space& sp) {
     if (defer_reads) {
         // resident step: size col/val by the row-width bound and pick nnz up with the step's final read-back
         PB_CUDA(cudaMemcpyAsync(&dctl()->nnz, sp.row_ptr.as<uint32_t>() + n, 4, cudaMemcpyDeviceToDevice, stream));
-        sp.col.ensure(size_t(n) * width * 4 + 4);
-        sp.val.ensure(size_t(n) * width * 8 + 8);
+        sp.col.ensure(size_t(n) * width * 4 + CSR_PAD);
+        sp.val.ensure(size_t(n) * width * 8 + CSR_PAD);
     } else {
         nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
         // the reference's assembly buffer check: 2 entries of 16 bytes per transcript element (subspace.hpp:152)
         require_memory(uint64_t(nnz) * 2 * 16, "matrix assembly buffer");
-        sp.col.ensure(size_t(nnz) * 4 + 4);
-        sp.val.ensure(size_t(nnz) * 8 + 8);
+        sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
+        sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
     }
     assemble_compact_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                                                             sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                             sp.val.as<double>());
     check_launch();
     sp.nnz = nnz;
+    sp.max_row = width;
     sp.has_h = true;
 }
 
@@ -648,15 +649,16 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
                     // (Ctl::out[1..3], read with the final read-back)
                     taylor_launch_single(true, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                         &c->taylor, 0, nullptr, c->out + 1);
+                                         &c->taylor, 0, nullptr, c->out + 1, sp.max_row);
                 } else if (!singles && order >= k0 && ((order - k0) & 1)) {
                     taylor_launch_catchup(g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                          &c->taylor);
+                                          &c->taylor, sp.max_row);
                 } else if (!singles && order >= k0 && order < max_order) {
-                    taylor_launch_defer(g, stream, n, rp, cl, vl, tin, tout, b, order, pt, &c->taylor);
+                    taylor_launch_defer(g, sm_count, stream, n, rp, cl, vl, tin, tout, b, order, pt, &c->taylor,
+                                        sp.max_row);
                 } else {
                     taylor_launch_single(false, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                         &c->taylor, 0, nullptr, nullptr);
+                                         &c->taylor, 0, nullptr, nullptr, sp.max_row);
                 }
                 check_launch();
             }
@@ -693,10 +695,15 @@ void Engine::upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int3
     const int64_t nnz = row_ptr[n];
     if (nnz < 0 || nnz > 0xfffffff0LL) throw ArgError("csr: nnz out of range");
     std::vector<uint32_t> rp(size_t(n) + 1);
-    for (int64_t i = 0; i <= n; ++i) rp[size_t(i)] = uint32_t(row_ptr[i]);
-    sp.row_ptr.ensure((size_t(n) + 1) * 4);
-    sp.col.ensure(size_t(nnz) * 4 + 4);
-    sp.val.ensure(size_t(nnz) * 8 + 8);
+    int64_t longest = 0;
+    for (int64_t i = 0; i <= n; ++i) {
+        rp[size_t(i)] = uint32_t(row_ptr[i]);
+        if (i > 0) longest = std::max<int64_t>(longest, row_ptr[i] - row_ptr[i - 1]);
+    }
+    sp.max_row = longest <= 15 ? int(std::max<int64_t>(longest, 1)) : 0;
+    sp.row_ptr.ensure((size_t(n) + 1) * 4 + CSR_PAD);
+    sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
+    sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
     PB_CUDA(cudaMemcpyAsync(sp.row_ptr.p, rp.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice, stream));
     if (nnz) {
         PB_CUDA(cudaMemcpyAsync(sp.col.p, col, size_t(nnz) * 4, cudaMemcpyHostToDevice, stream));

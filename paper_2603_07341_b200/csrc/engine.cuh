@@ -102,6 +102,10 @@ struct DevBuf {
     }
 };
 
+/// Slack behind row_ptr / col / val: the Taylor tile kernels fetch 16-byte-aligned slices with bulk copies, which may
+/// read up to 15 bytes past the last element.
+constexpr size_t CSR_PAD = 64;
+
 /// EffectiveSpace (subspace.hpp:76-82) on the device: sorted key table + CSR H_eff.
 struct Space {
     DevBuf words;  // n x W uint32, canonical order
@@ -110,6 +114,7 @@ struct Space {
     DevBuf col;      // int32[nnz] ascending per row
     DevBuf val;      // double[nnz]
     uint64_t nnz = 0;
+    int max_row = 0;  // upper bound on the entries of a row (0 = unknown): selects the Taylor tile kernels
     uint64_t q_nom = 0;
     int order = 0;
     bool has_h = false;

@@ -172,7 +172,7 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
                               tmp_col.as<uint32_t>(), tmp_val.as<double>(), inc_xcnt.as<uint32_t>()));
         check_launch();
     }
-    next.row_ptr.ensure((size_t(n_new) + 1) * 4);
+    next.row_ptr.ensure((size_t(n_new) + 1) * 4 + CSR_PAD);
     inc_simple.ensure(size_t(n) + 4);
     inc_row_len_kernel<<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
         n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), inc_xcnt.as<uint32_t>(),
@@ -182,8 +182,8 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     PB_CUDA(cudaMemsetAsync(next.row_ptr.as<uint32_t>() + n_new, 0, 4, stream));
     exclusive_scan(next.row_ptr.as<uint32_t>(), uint64_t(n_new) + 1);
     PB_CUDA(cudaMemcpyAsync(&c->nnz, next.row_ptr.as<uint32_t>() + n_new, 4, cudaMemcpyDeviceToDevice, stream));
-    next.col.ensure(size_t(n_new) * width * 4 + 4);
-    next.val.ensure(size_t(n_new) * width * 8 + 8);
+    next.col.ensure(size_t(n_new) * width * 4 + CSR_PAD);
+    next.val.ensure(size_t(n_new) * width * 8 + CSR_PAD);
     inc_fill_kernel<<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
         n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), old.val.as<double>(), width,
         tmp_col.as<uint32_t>(), tmp_val.as<double>(), inc_xcnt.as<uint32_t>(), inc_side_newidx.as<uint32_t>(),
@@ -198,6 +198,7 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     next.nnz = 0;  // arrives with the step's final read-back (Ctl::nnz)
     next.q_nom = kept;
     next.order = m;
+    next.max_row = width;
     next.has_h = true;
     next.has_full = true;
     ++inc_steps;

@@ -189,7 +189,7 @@ void Engine::assemble_sharded(Space& sp) {
     tmp_col.ensure(size_t(n) * width * 4 + 4);
     tmp_val.ensure(size_t(n) * width * 8 + 8);
     tmp_cnt.ensure(size_t(n) * 4 + 4);
-    sp.row_ptr.ensure((size_t(n) + 1) * 4);
+    sp.row_ptr.ensure((size_t(n) + 1) * 4 + CSR_PAD);
     const uint64_t req_cap64 = uint64_t(n) * uint64_t(width) + 1;
     if (req_cap64 > 0x7ffffff0ull) throw PacesError("assembly: request count exceeds 31-bit indexing");
     const uint32_t req_cap = uint32_t(req_cap64);
@@ -277,13 +277,14 @@ void Engine::assemble_sharded(Space& sp) {
     PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
     exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
     const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
-    sp.col.ensure(size_t(nnz) * 4 + 4);
-    sp.val.ensure(size_t(nnz) * 8 + 8);
+    sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
+    sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
     assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                                                                     tmp_cnt.as<uint32_t>(), sp.row_ptr.as<uint32_t>(),
                                                                     sp.col.as<int32_t>(), sp.val.as<double>());
     check_launch();
     sp.nnz = nnz;
+    sp.max_row = width;
     sp.has_h = true;
     uint64_t g[2] = {n, nnz};
     comm_check(ops.allreduce_u64_host(ops.user, g, 2), "allreduce_u64_host");
@@ -450,7 +451,7 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
                 taylor_launch_single(false, g, sm_count, stream, n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                      sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
                                      term[order & 1].as<double2>(), c_vec, b, order, rtol, partials.as<double>(),
-                                     &c->taylor, 0, c->out, nullptr);
+                                     &c->taylor, 0, c->out, nullptr, sp.max_row);
                 check_launch();
                 comm_check(ops.allreduce_f64_dev(ops.user, c->out, 2, stream), "allreduce_f64_dev");
                 taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);

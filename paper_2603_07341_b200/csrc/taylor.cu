@@ -2,6 +2,7 @@
 #include "taylor.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "primitives.cuh"
 
@@ -261,6 +262,350 @@ __global__ void __launch_bounds__(NT, 6) taylor_catchup_kernel(uint32_t n, const
 }
 
 
+
+// ================================================================================================
+// K4, tile form (sm_100: bulk-copy pipeline).  The row kernels above make every thread walk a chain of dependent global
+// loads -- row_ptr -> col/val -> x, and the x of entry k+1 only after the multiply-add of entry k -- about 5 exposed
+// DRAM latencies per row, and fetch col/val with 32 scattered 4/8-byte requests per warp instruction (the L1 wavefront
+// pipe is their co-bottleneck).  Here a CTA takes TR consecutive rows per tile.  What is CONTIGUOUS for a tile -- its
+// row_ptr slice and its run of col and val -- is fetched by a producer warp with 1-D bulk copies (cp.async.bulk,
+// completion on an mbarrier with expect_tx) into a shared-memory ring, a few tiles ahead.  A consumer thread still owns
+// one row, but reads its extent, columns and values from shared memory, so it can issue ALL x gathers of the row back to
+// back (they are the only scattered global loads left) and then add the products in ascending column order: ONE exposed
+// latency per row, the same multiplies and additions in the same order as the row kernels and the reference
+// (csr_matvec, subspace.hpp:35-43), hence bit-identical coefficients.  Consumer warps never meet at a CTA barrier: a
+// warp releases a stage with one mbarrier arrive.  Every mode runs on the same persistent grid, so SINGLE / DEFER /
+// CATCHUP / FIRST share one reduction shape.
+// ================================================================================================
+namespace tile {
+
+#ifndef TILE_TR
+#define TILE_TR 256
+#endif
+#ifndef TILE_STAGES
+#define TILE_STAGES 2
+#endif
+#ifndef TILE_MINB
+#define TILE_MINB 1
+#endif
+#ifndef TILE_EVICT_FIRST
+#define TILE_EVICT_FIRST 0
+#endif
+constexpr int TR = TILE_TR;        // rows per tile = consumer threads per CTA
+constexpr int STAGES = TILE_STAGES;
+constexpr int NTHREADS = TR + 32;  // + one producer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {  // try_wait suspends the thread in hardware for a bounded time; loop until the phase has completed
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+/// 1-D bulk copy global -> shared; src, dst and bytes are multiples of 16.  The matrix streams through once per
+/// launch: with TILE_EVICT_FIRST it is marked evict-first in L2 so that it does not push out the vector being gathered.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#if TILE_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+#else
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+#endif
+}
+
+enum Mode { SINGLE = 0, FIRST = 1, DEFER = 2, CATCHUP = 3 };
+
+struct Layout {  // byte offsets inside the dynamic shared memory of one CTA
+    uint32_t ecap;   // entries a stage holds (TR * max_row + 8)
+    uint32_t rp, col, val, stage_bytes, bars, total;
+};
+__host__ __device__ inline Layout make_layout(int max_row) {
+    Layout L;
+    L.ecap = uint32_t(TR) * uint32_t(max_row) + 8;
+    uint32_t o = 0;
+    L.rp = o;
+    o += (TR + 4) * 4;
+    L.col = o;
+    o += L.ecap * 4;
+    o = (o + 15) & ~15u;
+    L.val = o;
+    o += L.ecap * 8;
+    L.stage_bytes = (o + 127) & ~127u;
+    L.bars = L.stage_bytes * STAGES;  // full[STAGES], empty[STAGES]
+    L.total = L.bars + 2 * STAGES * 8 + 128;  // + reduction scratch
+    return L;
+}
+
+template <int MODE, int MAXR>
+__global__ void __launch_bounds__(NTHREADS, TILE_MINB) taylor_tile_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                               const int32_t* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double2* __restrict__ term_in,
+                                                               double2* __restrict__ term_out, double2* __restrict__ c,
+                                                               double b, int order, double rtol, int max_row,
+                                                               double* __restrict__ partials, TaylorCtl* ctl,
+                                                               int ignore_stop, double* __restrict__ tot_out,
+                                                               double* __restrict__ expect_out) {
+    constexpr bool HAS_C = MODE != DEFER;
+    constexpr int K = MODE == FIRST ? 5 : (MODE == CATCHUP ? 3 : (MODE == DEFER ? 1 : 2));
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
+    if (MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
+        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
+        return;
+    }
+    const Layout L = make_layout(max_row);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* empty = full + STAGES;
+    double* red = reinterpret_cast<double*>(smem + L.bars + 2 * STAGES * 8);
+    const uint32_t ntiles = (n + TR - 1) / TR;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, TR / 32);  // one arrive per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid >= TR) {
+        // ---------------- producer warp: one lane streams the tiles of this CTA into the ring ----------------
+        if (tid != TR) return;
+        uint32_t t = blockIdx.x;
+        // boundaries of the NEXT tile are requested one iteration ahead (two dependent global loads otherwise)
+        uint32_t e0n = 0, e1n = 0;
+        if (t < ntiles) {
+            e0n = __ldg(row_ptr + size_t(t) * TR);
+            e1n = __ldg(row_ptr + min(size_t(t + 1) * TR, size_t(n)));
+        }
+        for (uint32_t j = 0; t < ntiles; ++j, t += gridDim.x) {
+            const int s = int(j % STAGES);
+            const uint32_t e0 = e0n, e1 = e1n;
+            const uint32_t tn = t + gridDim.x;
+            if (tn < ntiles) {
+                e0n = __ldg(row_ptr + size_t(tn) * TR);
+                e1n = __ldg(row_ptr + min(size_t(tn + 1) * TR, size_t(n)));
+            }
+            if (j >= STAGES) mbar_wait(empty + s, ((j / STAGES) - 1) & 1);
+            unsigned char* st = smem + size_t(s) * L.stage_bytes;
+            const uint32_t r0 = t * TR;
+            const uint32_t rows = min(uint32_t(TR), n - r0);
+            const uint32_t rp_bytes = ((rows + 1 + 3) & ~3u) * 4;
+            const uint32_t a0 = e0 & ~3u;
+            const uint32_t cnt = (e1 - a0 + 3) & ~3u;
+            mbar_expect_tx(full + s, rp_bytes + cnt * 12);
+            bulk_load(st + L.rp, row_ptr + r0, rp_bytes, full + s);
+            if (cnt) {
+                bulk_load(st + L.col, col + a0, cnt * 4, full + s);
+                bulk_load(st + L.val, val + a0, cnt * 8, full + s);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: one row per thread and tile ----------------
+    double acc[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    uint32_t j = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; ++j, t += gridDim.x) {
+        const int s = int(j % STAGES);
+        unsigned char* st = smem + size_t(s) * L.stage_bytes;
+        const uint32_t* rp_s = reinterpret_cast<const uint32_t*>(st + L.rp);
+        const int32_t* col_s = reinterpret_cast<const int32_t*>(st + L.col);
+        const double* val_s = reinterpret_cast<const double*>(st + L.val);
+        const uint32_t i = t * TR + tid;
+        const bool live = i < n;
+        // independent of the ring: this row's slice of c and (catch-up / first order) of the previous term
+        double2 cc = make_double2(0.0, 0.0), tp = make_double2(0.0, 0.0);
+        if (HAS_C && live) cc = c[i];
+        if ((MODE == CATCHUP || MODE == FIRST) && live) tp = __ldg(term_in + i);
+        mbar_wait(full + s, (j / STAGES) & 1);
+        double ar = 0.0, ai = 0.0;
+        if (live) {
+            const uint32_t base = rp_s[0] & ~3u;  // the slices start at the 16-byte boundary below the first entry
+            const uint32_t kb = rp_s[tid] - base;
+            const uint32_t len = rp_s[tid + 1] - base - kb;
+            double2 x[MAXR];
+#pragma unroll
+            for (int u = 0; u < MAXR; ++u)
+                if (uint32_t(u) < len) x[u] = __ldg(term_in + col_s[kb + u]);
+#pragma unroll
+            for (int u = 0; u < MAXR; ++u)
+                if (uint32_t(u) < len) {
+                    const double v = val_s[kb + u];
+                    ar = __dadd_rn(ar, __dmul_rn(v, x[u].x));
+                    ai = __dadd_rn(ai, __dmul_rn(v, x[u].y));
+                }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(empty + s);  // this warp has read everything it needs from the stage
+        if (live) {
+            if (MODE == FIRST) {
+                // real(conj(x) * row) = xr*rr - (-xi)*ri
+                acc[2] = __dadd_rn(acc[2], __dsub_rn(__dmul_rn(tp.x, ar), __dmul_rn(-tp.y, ai)));
+                acc[3] = __dadd_rn(acc[3], __dadd_rn(__dmul_rn(tp.x, tp.x), __dmul_rn(tp.y, tp.y)));
+                if (!isfinite(tp.x) || !isfinite(tp.y)) acc[4] = acc[4] + 1.0;
+            }
+            // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
+            const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
+            const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
+            term_out[i] = make_double2(tr, ti);
+            acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti)));
+            if (HAS_C) {
+                if (MODE == CATCHUP) {
+                    cc.x = __dadd_rn(cc.x, tp.x);
+                    cc.y = __dadd_rn(cc.y, tp.y);
+                    acc[2] = __dadd_rn(acc[2], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+                }
+                cc.x = __dadd_rn(cc.x, tr);
+                cc.y = __dadd_rn(cc.y, ti);
+                c[i] = cc;
+                acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+            }
+        }
+    }
+
+    // ---------------- reduction: fixed tree inside the CTA, partials combined by the last CTA in CTA order ------
+    auto consumer_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(TR) : "memory"); };
+    const int lane = tid & 31, warp = tid >> 5;
+    double blk[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const double w = warp_sum(acc[q]);
+        consumer_sync();
+        if (lane == 0) red[warp] = w;
+        consumer_sync();
+        double tsum = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
+        blk[q] = tsum;
+    }
+    uint32_t* flag = reinterpret_cast<uint32_t*>(red + 12);
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) partials[size_t(q) * gridDim.x + blockIdx.x] = blk[q];
+        __threadfence();
+        *flag = (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    consumer_sync();
+    if (*flag == 0) return;
+    __threadfence();
+    double tot[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        double a = 0.0;
+        for (uint32_t g = tid; g < gridDim.x; g += TR) a = __dadd_rn(a, __ldcg(partials + size_t(q) * gridDim.x + g));
+        const double w = warp_sum(a);
+        consumer_sync();
+        if (lane == 0) red[warp] = w;
+        consumer_sync();
+        double tsum = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
+        tot[q] = tsum;
+    }
+    if (tid != 0) return;
+    ctl->ticket = 0;
+    if (MODE == FIRST) {
+        expect_out[0] = tot[2];
+        expect_out[1] = tot[3];
+        expect_out[2] = tot[4];
+    }
+    if (MODE == DEFER) {
+        ctl->pending = 1;
+        ctl->pending_tn2 = tot[0];
+        ctl->deferred += 1;
+        if (order > ctl->order_used) ctl->order_used = order;
+        ctl->last_order = order;
+    } else if (tot_out) {  // sharded: the sums are all-reduced first, taylor_stop_kernel applies the rule
+        tot_out[0] = tot[0];
+        tot_out[1] = tot[1];
+    } else if (MODE == CATCHUP) {
+        taylor_apply_rule(ctl, order - 1, ctl->pending_tn2, tot[2], rtol);  // streak was 0: cannot stop here
+        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
+        ctl->pending = 0;
+    } else {
+        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
+    }
+    __threadfence();
+}
+
+template <int MODE, int MAXR>
+static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
+                     const double* val, const double2* term_in, double2* term_out, double2* c, double b, int order,
+                     double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
+                     double* expect_out) {
+    const Layout L = make_layout(MAXR);
+    static int per_sm = 0;  // resident CTAs per SM for this instantiation
+    if (per_sm == 0) {
+        per_sm = -1;
+        int occ = 0;
+        if (cudaFuncSetAttribute(taylor_tile_kernel<MODE, MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(L.total)) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, taylor_tile_kernel<MODE, MAXR>, NTHREADS, L.total) ==
+                cudaSuccess &&
+            occ >= 1)
+            per_sm = occ;
+        else
+            cudaGetLastError();
+    }
+    if (per_sm < 0) return false;
+    const uint32_t ntiles = (n + TR - 1) / TR;
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(per_sm)));
+    taylor_tile_kernel<MODE, MAXR><<<grid, NTHREADS, L.total, stream>>>(n, row_ptr, col, val, term_in, term_out, c, b, order,
+                                                                         rtol, MAXR, partials, ctl, ignore_stop, tot_out,
+                                                                         expect_out);
+    return true;
+}
+
+template <int MODE>
+static bool launch(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
+                   const double* val, const double2* term_in, double2* term_out, double2* c, double b, int order,
+                   double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
+                   double* expect_out) {
+    // instantiations by row-length bound: 1D models (<= 5 entries), 2D (<= 7), 3D (<= 9)
+    if (max_row < 1 || max_row > 9) return false;
+    if (max_row <= 5)
+        return launch_r<MODE, 5>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
+                                 partials, ctl, ignore_stop, tot_out, expect_out);
+    if (max_row <= 7)
+        return launch_r<MODE, 7>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
+                                 partials, ctl, ignore_stop, tot_out, expect_out);
+    return launch_r<MODE, 9>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row, partials,
+                             ctl, ignore_stop, tot_out, expect_out);
+}
+
+}  // namespace tile
+
+static const bool g_use_tiles = std::getenv("PB200_TAYLOR_ROWS") == nullptr;
+
 // ------------------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------------------
@@ -274,7 +619,16 @@ static int resident_ctas(K kernel, int fallback) {
 void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
-                          double* tot_out, double* expect_out) {
+                          double* tot_out, double* expect_out, int max_row) {
+    if (g_use_tiles && max_row > 0) {
+        const bool ok = expect ? tile::launch<tile::FIRST>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b,
+                                                           order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
+                                                           expect_out)
+                               : tile::launch<tile::SINGLE>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b,
+                                                            order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
+                                                            expect_out);
+        if (ok) return;
+    }
     if (expect) {
         // this variant needs more registers: size its grid to what is resident so the launch is a single wave
         static const int per_sm = resident_ctas(taylor_order_kernel_t<true>, 4);
@@ -286,15 +640,23 @@ void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stre
     }
 }
 
-void taylor_launch_defer(int grid, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
-                         const double* val, const double2* term_in, double2* term_out, double b, int order,
-                         double* partials, TaylorCtl* ctl) {
+void taylor_launch_defer(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                         const int32_t* col, const double* val, const double2* term_in, double2* term_out, double b,
+                         int order, double* partials, TaylorCtl* ctl, int max_row) {
+    if (g_use_tiles && max_row > 0 &&
+        tile::launch<tile::DEFER>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, nullptr, b, order, 0.0, max_row,
+                                  partials, ctl, 0, nullptr, nullptr))
+        return;
     taylor_defer_kernel<<<grid, NT, 0, stream>>>(n, row_ptr, col, val, term_in, term_out, b, order, partials, ctl);
 }
 
 void taylor_launch_catchup(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                            const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
-                           double b, int order, double rtol, double* partials, TaylorCtl* ctl) {
+                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row) {
+    if (g_use_tiles && max_row > 0 &&
+        tile::launch<tile::CATCHUP>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
+                                    partials, ctl, 0, nullptr, nullptr))
+        return;
     static const int per_sm = resident_ctas(taylor_catchup_kernel, 4);
     taylor_catchup_kernel<<<std::min(grid, sm_count * per_sm), NT, 0, stream>>>(n, row_ptr, col, val, term_in, term_out,
                                                                                c, b, order, rtol, partials, ctl);

@@ -82,7 +82,9 @@ static void compare_runs(const char* name, const RunConfig& cfg) {
     for (std::size_t i = 0; i < std::min(a.histograms.size(), b.histograms.size()); ++i) {
         const auto &x = a.histograms[i].second, &y = b.histograms[i].second;
         CHECK(close(a.histograms[i].first, b.histograms[i].first, 1e-14) && x.support == y.support && x.q50 == y.q50 &&
-                  x.q90 == y.q90 && x.q99 == y.q99 && x.q9999 == y.q9999 && x.tail_exponent == y.tail_exponent &&
+                  x.q90 == y.q90 && x.q99 == y.q99 && x.q9999 == y.q9999 &&
+                  close(x.tail_exponent, y.tail_exponent, 1e-10, 1e-12) &&  // device log + tree sums, not the host loop
+                 
                   x.rank == y.rank && x.weight == y.weight,
               "%s: weight histogram %zu", name, i);
     }
@@ -145,10 +147,10 @@ static void compare_functions() {
     CHECK(std::abs(dipole_amplitude(psi, terms) - b200::dipole_amplitude(dev, psi, terms)) <= 1e-12, "dipole");
     auto pn = phonon_numbers(psi, terms), gpn = b200::phonon_numbers(dev, psi, terms);
     for (std::size_t k = 0; k < pn.size(); ++k) CHECK(close(pn[k], gpn[k], 1e-10, 1e-18), "phonon numbers %zu", k);
-    {  // weight_histogram (observables.hpp:123-176; test_observables.cpp:170-220): every field identical
+    {  // weight_histogram (observables.hpp:123-176; test_observables.cpp:170-220): counts and curve exact, slope 1e-10
         const WeightHistogram wh = weight_histogram(psi, 16), gwh = b200::weight_histogram(dev, psi, 16);
         CHECK(wh.support == gwh.support && wh.q50 == gwh.q50 && wh.q90 == gwh.q90 && wh.q99 == gwh.q99 &&
-                  wh.q9999 == gwh.q9999 && wh.tail_exponent == gwh.tail_exponent && wh.rank == gwh.rank &&
+                  wh.q9999 == gwh.q9999 && close(wh.tail_exponent, gwh.tail_exponent, 1e-10, 1e-12) && wh.rank == gwh.rank &&
                   wh.weight == gwh.weight,
               "weight_histogram");
     }

@@ -639,7 +639,7 @@ def test_step_io_rejects_overlapping_buffers(gpu):
     with pytest.raises(Exception, match="must not overlap"):
         ctx.step(bw[: w.size], bc[: len(c)], t, sd + 1, out_words=bw, out_coeff=bc, **kw)
     ow, oc = np.zeros_like(bw), np.zeros_like(bc)
-    w2, c2, d = ctx.step(bw[: w.size], bc[: len(c)], t, sd + 1, out_words=ow, out_coeff=oc, **kw)
-    dr = run.step()
+    dr = run.step()  # (the host-buffer step below replaces this context's resident state)
     wr, cr = run.state()
+    w2, c2, d = ctx.step(bw[: w.size], bc[: len(c)], t, sd + 1, out_words=ow, out_coeff=oc, **kw)
     assert np.array_equal(w2, wr) and c2.tobytes() == cr.tobytes() and d["q_true"] == dr["q_true"]
