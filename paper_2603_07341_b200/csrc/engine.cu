@@ -255,16 +255,16 @@ void Engine::dedup_candidates_async(uint32_t n, uint32_t nc_bound) {
     seg_rank.ensure(size_t(nc_bound) * 4 + 4);
     row_len.ensure((size_t(n) + 2) * 4);
     PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
-    place_candidates_kernel<<<gc_grid, NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc_ptr, gap.as<uint32_t>(),
+    place_candidates_kernel<<<gc_grid, NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc_ptr, nc_bound, 0, gap.as<uint32_t>(),
                                                         row_len.as<uint32_t>(), perm.as<uint32_t>());
     check_launch();
     PB_CUDA(cudaMemsetAsync(row_len.p, 0, (size_t(n) + 2) * 4, stream));
     PB_DISPATCH_W(W, segment_dedup_kernel<W><<<gc_grid, NT, 0, stream>>>(
-                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr,
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, nc_bound, 0,
                          gap.as<uint32_t>(), seg_rank.as<uint32_t>(), row_len.as<uint32_t>(), &c->grow));
     check_launch();
     PB_DISPATCH_W(W, segment_rank_kernel<W><<<gc_grid, NT, 0, stream>>>(
-                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr,
+                         cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, nc_bound, 0,
                          gap.as<uint32_t>(), seg_rank.as<uint32_t>()));
     check_launch();
     // kept_before[g] = number of new keys in gaps < g; kept_before[n+1] = total
@@ -466,10 +466,17 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         throw PacesError("truncate_select: state has no support");
     }
 
-    uint32_t* keep = flag_keep.as<uint32_t>();
+    // compact: uint32 keep flags for the compaction of the kept keys (full expansion); otherwise the kept rows are
+    // marked as BFS distance 0 for the incremental adapt phase (incremental.cuh), which never materialises them
+    uint32_t* keep = compact ? flag_keep.as<uint32_t>() : nullptr;
+    uint8_t* dist0 = nullptr;
+    if (!compact) {
+        inc_dist.ensure(size_t(n) + 16);
+        dist0 = inc_dist.as<uint8_t>();
+    }
     uint64_t kept64 = sc.support;
     if (sc.support <= q_nom) {
-        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
+        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr, dist0);
         check_launch();
     } else {
         kept64 = q_nom;
@@ -487,14 +494,14 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
         const uint64_t need = q_nom - sc.count_gt;  // 1 <= need <= count_eq
         if (need >= sc.count_eq) {
             // every tie is admitted: the shuffle loop of engine.hpp:138-141 does not run
-            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr);
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr, dist0);
             check_launch();
         } else {
             // ties in ascending table index -> host -> seeded Fisher-Yates exactly as engine.hpp:137-142
             flag_tie.ensure((size_t(n) + 1) * 4);
             pos_a.ensure((size_t(n) + 1) * 4);
             select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 0, keep,
-                                                      flag_tie.as<uint32_t>());
+                                                      flag_tie.as<uint32_t>(), dist0);
             check_launch();
             PB_CUDA(cudaMemcpyAsync(pos_a.p, flag_tie.p, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
             exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
@@ -512,7 +519,7 @@ uint32_t Engine::select(const uint32_t* d_words, const double2* d_c, uint32_t n,
                 std::swap(ties[i - 1], ties[j]);
             }
             PB_CUDA(cudaMemcpyAsync(idx_tmp.p, ties.data(), size_t(need) * 4, cudaMemcpyHostToDevice, stream));
-            set_flags_kernel<<<grid_for(need), NT, 0, stream>>>(idx_tmp.as<uint32_t>(), uint32_t(need), keep);
+            set_flags_kernel<<<grid_for(need), NT, 0, stream>>>(idx_tmp.as<uint32_t>(), uint32_t(need), keep, dist0);
             check_launch();
             sync();  // `ties` must outlive the copy
         }
@@ -901,6 +908,10 @@ void Engine::run_step(pb200_diag* out) {
         if (incremental && !grow_incremental(old, c_old, kept, cfg.m, next, coeff[ccur ^ 1])) {
             incremental = false;
             ++inc_fallbacks;
+            // the kept rows are still the rows at distance 0: turn them into the keep flags of the full path
+            inc_keep_from_dist_kernel<<<grid_for(uint64_t(old.n) + 1), NT, 0, stream>>>(inc_dist.as<uint8_t>(), old.n,
+                                                                                      flag_keep.as<uint32_t>());
+            check_launch();
             compact_kept(old.words.as<uint32_t>(), old.n, kept);
         }
         if (incremental) {

@@ -41,168 +41,165 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     Ctl* c = dctl();
     inc_ctr.ensure(sizeof(IncCounters));
     IncCounters* ictr = inc_ctr.as<IncCounters>();
-    const uint32_t side_cap = n;  // more new keys than old rows: not a steady state, use the full path
-
-    inc_dist.ensure(size_t(n) + 1);
-    inc_elist.ensure(size_t(n) * 4 + 4);
-    uint8_t* dist = inc_dist.as<uint8_t>();
-    inc_init_dist_kernel<<<grid_for(n), NT, 0, stream>>>(flag_keep.as<uint32_t>(), n, dist);
-    check_launch();
     PB_CUDA(cudaMemsetAsync(ictr, 0, sizeof(IncCounters), stream));
 
-    uint32_t side_n = 0;
-    int scur = 0;
-    for (auto& b : inc_side_keys) b.ensure(64);
-    for (auto& b : inc_side_gap) b.ensure(64);
-    for (auto& b : inc_side_dist) b.ensure(64);
-
-    // candidate capacity: what the buffers already hold (the full path sized them for whole BFS levels), at least a
-    // quarter of the table's moves; running out of it only sends this step to the full path
+    // ---- capacities.  Nothing below is sized by a count the host would have to read back first: more new keys than
+    // a quarter of the old rows (not a steady state) or more candidates than the buffer holds only raise `overflow`,
+    // and the step is redone by the full path.
+    const uint32_t side_cap = n / 4 + (1u << 16);
+    const uint64_t n_bound = uint64_t(n) + side_cap;
+    if (n_bound > 0x7fffffffull) return false;
     {
-        const uint64_t want = std::max<uint64_t>(uint64_t(n / 4 + 1024) * uint64_t(nmoves), 1u << 16);
+        const uint64_t want = std::max<uint64_t>(uint64_t(n / 8 + 1024) * uint64_t(std::max(nmoves, 1)), 1u << 16);
         cand_keys.ensure(size_t(want) * W * 4);
         cand_gap.ensure(size_t(want) * 4);
     }
     const uint32_t cand_cap =
         uint32_t(std::min<uint64_t>({cand_keys.cap / (size_t(W) * 4), cand_gap.cap / 4, 0x7ffffff0ull}));
-    gap.ensure((size_t(n) + 2) * 4);
+    perm.ensure(size_t(cand_cap) * 4 + 4);
+    seg_rank.ensure(size_t(cand_cap) * 4 + 4);
+    for (int i = 0; i < 2; ++i) {
+        inc_side_keys[i].ensure(size_t(side_cap) * W * 4 + 64);
+        inc_side_gap[i].ensure(size_t(side_cap) * 4 + 64);
+        inc_side_dist[i].ensure(size_t(side_cap) + 64);
+    }
+    inc_new_keys.ensure(size_t(cand_cap) * W * 4 + 64);
+    inc_new_gap.ensure(size_t(cand_cap) * 4 + 64);
+    inc_elist.ensure(size_t(n) * 4 + 4);
+    // candidates are bucketed by (insertion gap >> sh): ~64 K buckets whatever the table size
+    int sh = 0;
+    while ((uint64_t(n) >> sh) > (1u << 16)) ++sh;
+    const uint32_t nbuckets = uint32_t(uint64_t(n) >> sh) + 1;  // gaps run over [0, n]
+    const size_t bstride = (size_t(nbuckets) + 2 + 3) & ~size_t(3);  // the scan reads 16-byte vectors: keep them aligned
+    inc_buckets.ensure(3 * bstride * 4);
+    uint32_t* b_start = inc_buckets.as<uint32_t>();   // counts -> segment starts
+    uint32_t* b_fill = b_start + bstride;             // placement cursors
+    uint32_t* b_kept = b_fill + bstride;              // survivors -> kept_before
+    uint8_t* dist = inc_dist.as<uint8_t>();           // 0 on the kept rows, DIST_INF elsewhere (select())
+    const int small_grid = sm_count * 4;
+
+    int scur = 0;
     for (int k = 0; k < m; ++k) {
-        PB_CUDA(cudaMemsetAsync(&ictr->n_expand, 0, 4, stream));
-        inc_mark_level_kernel<<<grid_for(n), NT, 0, stream>>>(n, k, old.full.as<uint8_t>(), old.row_ptr.as<uint32_t>(),
-                                                               old.col.as<int32_t>(), dist, inc_elist.as<uint32_t>(),
-                                                               ictr);
+        inc_level_kernel<<<grid_for(n), NT, 0, stream>>>(n, k, old.full.as<uint8_t>(), old.row_ptr.as<uint32_t>(),
+                                                          old.col.as<int32_t>(), dist, inc_elist.as<uint32_t>(), ictr);
         check_launch();
         if (nmoves == 0) continue;
-        PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
-        PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
-        PB_DISPATCH_WI(W, inc_expand_kernel<W><<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
-                              md, old.words.as<uint32_t>(), n, inc_elist.as<uint32_t>(), &ictr->n_expand,
-                              inc_side_keys[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), side_n, k, dist,
-                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cand_cap, gap.as<uint32_t>(), &c->grow,
-                              ictr));
+        PB_CUDA(cudaMemsetAsync(b_start, 0, 3 * bstride * 4, stream));
+        PB_DISPATCH_WI(W, inc_expand_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              md, old.words.as<uint32_t>(), n, inc_elist.as<uint32_t>(),
+                              inc_side_keys[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), k, nmoves, dist,
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cand_cap, sh, b_start, ictr));
         check_launch();
-        inc_clamp_kernel<<<1, 1, 0, stream>>>(&c->grow.n_cand, cand_cap);
+        // unique new keys of this level in canonical order: counting sort by bucket, dedup + rank inside the buckets
+        const uint32_t* nc_ptr = &ictr->n_cand[k];
+        exclusive_scan(b_start, uint64_t(nbuckets) + 1);
+        place_candidates_kernel<<<small_grid, NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc_ptr, cand_cap, sh, b_start,
+                                                               b_fill, perm.as<uint32_t>());
         check_launch();
-        // unique new keys of this level, canonical order (the dedup machinery of the full path, on the device-side
-        // candidate count); ONE read-back per level
-        const uint32_t n_new = dedup_candidates(n, cand_cap);
-        if (n_new == 0) continue;
-        if (uint64_t(side_n) + n_new > side_cap) return false;
-        inc_new_keys.ensure(size_t(n_new) * W * 4 + 4);
-        inc_new_gap.ensure(size_t(n_new) * 4 + 4);
-        PB_DISPATCH_WI(W, inc_emit_unique_kernel<W><<<grid_for(cand_cap), NT, 0, stream>>>(
+        PB_DISPATCH_WI(W, segment_dedup_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, cand_cap, sh,
+                              b_start, seg_rank.as<uint32_t>(), b_kept, nullptr));
+        check_launch();
+        PB_DISPATCH_WI(W, segment_rank_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, cand_cap, sh,
+                              b_start, seg_rank.as<uint32_t>()));
+        check_launch();
+        exclusive_scan(b_kept, uint64_t(nbuckets) + 1);
+        PB_DISPATCH_WI(W, inc_emit_unique_kernel<W><<<small_grid, NT, 0, stream>>>(
                               cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
-                              seg_rank.as<uint32_t>(), &c->grow.n_cand, row_len.as<uint32_t>(),
-                              inc_new_keys.as<uint32_t>(), inc_new_gap.as<uint32_t>()));
+                              seg_rank.as<uint32_t>(), k, cand_cap, sh, b_kept, nbuckets, inc_new_keys.as<uint32_t>(),
+                              inc_new_gap.as<uint32_t>(), ictr));
         check_launch();
-        const uint32_t merged = side_n + n_new;
-        inc_side_keys[scur ^ 1].ensure(size_t(merged) * W * 4 + 4);
-        inc_side_gap[scur ^ 1].ensure(size_t(merged) * 4 + 4);
-        inc_side_dist[scur ^ 1].ensure(size_t(merged) + 4);
-        PB_DISPATCH_WI(W, inc_side_merge_kernel<W><<<grid_for(merged), NT, 0, stream>>>(
+        PB_DISPATCH_WI(W, inc_side_merge_kernel<W><<<small_grid, NT, 0, stream>>>(
                               inc_side_keys[scur].as<uint32_t>(), inc_side_gap[scur].as<uint32_t>(),
-                              inc_side_dist[scur].as<uint8_t>(), side_n, inc_new_keys.as<uint32_t>(),
-                              inc_new_gap.as<uint32_t>(), n_new, k + 1, inc_side_keys[scur ^ 1].as<uint32_t>(),
-                              inc_side_gap[scur ^ 1].as<uint32_t>(), inc_side_dist[scur ^ 1].as<uint8_t>()));
+                              inc_side_dist[scur].as<uint8_t>(), inc_new_keys.as<uint32_t>(), inc_new_gap.as<uint32_t>(), k,
+                              side_cap, inc_side_keys[scur ^ 1].as<uint32_t>(), inc_side_gap[scur ^ 1].as<uint32_t>(),
+                              inc_side_dist[scur ^ 1].as<uint8_t>(), ictr));
         check_launch();
         scur ^= 1;
-        side_n = merged;
     }
+    const int levels = nmoves == 0 ? 0 : m;  // index of the final side count in IncCounters::side_n
 
-    // ---- index maps: pk = kept old rows before i, nb = side keys before row i
-    pos_a.ensure((size_t(n) + 2) * 4);
-    inc_keepflag_kernel<<<grid_for(uint64_t(n) + 1), NT, 0, stream>>>(dist, n, m, pos_a.as<uint32_t>());
-    check_launch();
-    exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
-    gap.ensure((size_t(n) + 2) * 4);
-    PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
-    if (side_n) {
-        inc_count_gaps_kernel<<<grid_for(side_n), NT, 0, stream>>>(inc_side_gap[scur].as<uint32_t>(), side_n,
-                                                                    gap.as<uint32_t>());
-        check_launch();
-    }
-    exclusive_scan(gap.as<uint32_t>(), uint64_t(n) + 2);
-    // one read-back: overflow flag, statistics and the number of surviving old rows
-    PB_CUDA(cudaMemcpyAsync(&ictr->n_keep, pos_a.as<uint32_t>() + n, 4, cudaMemcpyDeviceToDevice, stream));
-    const IncCounters fin = read_back<IncCounters>(ictr);
-    if (fin.overflow) return false;
-    inc_expanded_total += fin.expanded_total;
-    const uint32_t n_keep = fin.n_keep;
-    const uint64_t n_new64 = uint64_t(n_keep) + side_n;
-    if (n_new64 > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
-    const uint32_t n_new = uint32_t(n_new64);
-    require_memory(uint64_t(n_new) * 16 * 4, "state vectors");
-
-    // ---- new table, full flags, coefficients
-    next.words.ensure(size_t(n_new) * W * 4 + 4);
-    next.full.ensure(size_t(n_new) + 1);
-    c_new.ensure(size_t(n_new) * 16 + 16);
-    PB_CUDA(cudaMemsetAsync(c_new.p, 0, size_t(n_new) * 16, stream));
+    // ---- from the distances to the new space (see incremental.cuh): side-key neighbours, per-tile reductions, one
+    // small scan, then one pass over the old rows for the index maps / table / coefficients / row pointer and one for
+    // the entries
+    next.words.ensure(size_t(n_bound) * W * 4 + 64);
+    next.full.ensure(size_t(n_bound) + 64);
+    c_new.ensure(size_t(n_bound) * 16 + 16);
     inc_newidx.ensure(size_t(n) * 4 + 4);
-    inc_side_newidx.ensure(size_t(side_n) * 4 + 4);
-    inc_scatter_old_kernel<<<grid_for(n), NT, 0, stream>>>(c_old, n, m, dist, pos_a.as<uint32_t>(), gap.as<uint32_t>(),
-                                                           inc_newidx.as<uint32_t>(), next.full.as<uint8_t>(),
-                                                           c_new.as<double2>(), partials.as<double>(), &c->ticket,
-                                                           c->out);
+    inc_side_newidx.ensure(size_t(side_cap) * 4 + 4);
+    inc_s_col.ensure(size_t(side_cap) * width * 4 + 4);
+    inc_s_val.ensure(size_t(side_cap) * width * 8 + 8);
+    inc_has_extra.ensure(size_t(n) + 64);  // `touched` flags: bit 0 = the row loses an entry, bit 1 = it gains one
+    inc_simple.ensure(size_t(n) + 64);
+    const uint32_t ctiles = uint32_t((uint64_t(n) + 1 + INC_TILE - 1) / INC_TILE);
+    inc_tile_jlo.ensure((size_t(ctiles) + 2) * 4 * 3);
+    uint32_t* tile_jlo = inc_tile_jlo.as<uint32_t>();
+    uint32_t* tile_keep = tile_jlo + (ctiles + 2);
+    uint32_t* tile_nnz = tile_keep + (ctiles + 2);
+    inc_tile_disc.ensure(size_t(ctiles) * 8 + 8);
+    next.row_ptr.ensure((size_t(n_bound) + 1) * 4 + CSR_PAD);
+    next.col.ensure(size_t(n_bound) * width * 4 + CSR_PAD);
+    next.val.ensure(size_t(n_bound) * width * 8 + CSR_PAD);
+    uint8_t* touched = inc_has_extra.as<uint8_t>();
+    PB_CUDA(cudaMemsetAsync(touched, 0, size_t(n) + 1, stream));
+    const uint32_t* skeys = inc_side_keys[scur].as<uint32_t>();
+    const uint32_t* sgap = inc_side_gap[scur].as<uint32_t>();
+    PB_DISPATCH_WI(W, inc_side_search_kernel<W><<<small_grid, NT, 0, stream>>>(
+                          md, old.words.as<uint32_t>(), n, m, levels, dist, skeys, width, inc_s_col.as<uint32_t>(),
+                          inc_s_val.as<double>(), touched, ictr));
     check_launch();
-    PB_DISPATCH_WI(W, inc_copy_rows_kernel<W><<<grid_for(uint64_t(n) * W), NT, 0, stream>>>(
-                          old.words.as<uint32_t>(), n, inc_newidx.as<uint32_t>(), next.words.as<uint32_t>()));
+    // surviving old rows that gain entries: at most nmoves per side key; more than x_cap of them -> overflow
+    const uint32_t x_cap = uint32_t(std::min<uint64_t>(uint64_t(n), uint64_t(side_cap) * 2));
+    const int xs = std::max(nmoves, 1);
+    inc_xlist.ensure(size_t(x_cap) * 4 + 4);
+    inc_x_slot.ensure(size_t(n) * 4 + 4);
+    inc_x_ref.ensure(size_t(x_cap) * xs * 4 + 4);
+    inc_x_val.ensure(size_t(x_cap) * xs * 8 + 8);
+    inc_tile_prep_kernel<<<ctiles, NT, 0, stream>>>(n, m, levels, dist, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
+                                                    sgap, tile_keep, tile_jlo, ctiles, touched, inc_xlist.as<uint32_t>(),
+                                                    inc_x_slot.as<uint32_t>(), x_cap, ictr);
     check_launch();
-    if (side_n) {
-        PB_DISPATCH_WI(W, inc_scatter_side_kernel<W><<<grid_for(side_n), NT, 0, stream>>>(
-                              inc_side_keys[scur].as<uint32_t>(), inc_side_gap[scur].as<uint32_t>(),
-                              inc_side_dist[scur].as<uint8_t>(), side_n, m, pos_a.as<uint32_t>(),
-                              inc_side_newidx.as<uint32_t>(), next.words.as<uint32_t>(), next.full.as<uint8_t>()));
-        check_launch();
-    }
+    PB_DISPATCH_WI(W, inc_extras_kernel<W><<<small_grid, NT, 0, stream>>>(
+                          md, old.words.as<uint32_t>(), levels, inc_xlist.as<uint32_t>(), x_cap, skeys, xs,
+                          inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), ictr));
+    check_launch();
+    inc_tile_nnz_kernel<<<ctiles, NT, 0, stream>>>(n, m, dist, touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
+                                                   inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs,
+                                                   inc_s_col.as<uint32_t>(), width, tile_jlo, tile_nnz);
+    check_launch();
+    inc_tile_scan_kernel<<<1, NT, 0, stream>>>(tile_keep, tile_nnz, ctiles, levels, ictr);
+    check_launch();
+    PB_DISPATCH_WI(W, inc_compact_kernel<W><<<ctiles, NT, 0, stream>>>(
+                          old.words.as<uint32_t>(), c_old, n, m, levels, dist, touched, old.row_ptr.as<uint32_t>(),
+                          old.col.as<int32_t>(), inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs, skeys, sgap, inc_side_dist[scur].as<uint8_t>(), inc_s_col.as<uint32_t>(),
+                          width, tile_jlo, tile_keep, tile_nnz, inc_newidx.as<uint32_t>(), inc_side_newidx.as<uint32_t>(),
+                          next.words.as<uint32_t>(), next.full.as<uint8_t>(), c_new.as<double2>(),
+                          next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), inc_tile_disc.as<double>(), ctiles, ictr,
+                          c->out));
+    check_launch();
+    inc_fill_kernel<<<grid_for(n), NT, 0, stream>>>(
+        n, levels, inc_newidx.as<uint32_t>(), touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
+        old.val.as<double>(), inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), xs,
+        inc_side_newidx.as<uint32_t>(), inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), width,
+        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>(), ictr);
+    check_launch();
 
-    // ---- CSR: rows of the side keys (+ symmetric extras), row lengths, fill
-    inc_xcnt.ensure(size_t(n) * 4 + 4);
-    PB_CUDA(cudaMemsetAsync(inc_xcnt.p, 0, size_t(n) * 4, stream));
-    inc_s_col.ensure(size_t(side_n) * width * 4 + 4);
-    inc_s_val.ensure(size_t(side_n) * width * 8 + 8);
-    inc_s_len.ensure(size_t(side_n) * 4 + 4);
-    if (side_n) {
-        tmp_col.ensure(size_t(n) * width * 4);  // extras slots of the old rows
-        tmp_val.ensure(size_t(n) * width * 8);
-        PB_DISPATCH_WI(W, inc_side_rows_kernel<W><<<grid_for(side_n), NT, 0, stream>>>(
-                              md, old.words.as<uint32_t>(), n, inc_newidx.as<uint32_t>(),
-                              inc_side_keys[scur].as<uint32_t>(), inc_side_newidx.as<uint32_t>(), side_n, width,
-                              inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), inc_s_len.as<uint32_t>(),
-                              tmp_col.as<uint32_t>(), tmp_val.as<double>(), inc_xcnt.as<uint32_t>()));
-        check_launch();
-    }
-    next.row_ptr.ensure((size_t(n_new) + 1) * 4 + CSR_PAD);
-    inc_simple.ensure(size_t(n) + 4);
-    inc_row_len_kernel<<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
-        n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), inc_xcnt.as<uint32_t>(),
-        inc_side_newidx.as<uint32_t>(), inc_s_len.as<uint32_t>(), side_n, next.row_ptr.as<uint32_t>(),
-        inc_simple.as<uint8_t>());
-    check_launch();
-    PB_CUDA(cudaMemsetAsync(next.row_ptr.as<uint32_t>() + n_new, 0, 4, stream));
-    exclusive_scan(next.row_ptr.as<uint32_t>(), uint64_t(n_new) + 1);
-    PB_CUDA(cudaMemcpyAsync(&c->nnz, next.row_ptr.as<uint32_t>() + n_new, 4, cudaMemcpyDeviceToDevice, stream));
-    next.col.ensure(size_t(n_new) * width * 4 + CSR_PAD);
-    next.val.ensure(size_t(n_new) * width * 8 + CSR_PAD);
-    inc_fill_kernel<<<grid_for(uint64_t(n) + side_n), NT, 0, stream>>>(
-        n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), old.val.as<double>(), width,
-        tmp_col.as<uint32_t>(), tmp_val.as<double>(), inc_xcnt.as<uint32_t>(), inc_side_newidx.as<uint32_t>(),
-        inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), inc_s_len.as<uint32_t>(), side_n,
-        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>());
-    check_launch();
-    inc_fill_simple_kernel<<<grid_for(n), NT, 0, stream>>>(
-        n, inc_newidx.as<uint32_t>(), old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(), old.val.as<double>(),
-        inc_simple.as<uint8_t>(), next.row_ptr.as<uint32_t>(), next.col.as<int32_t>(), next.val.as<double>());
-    check_launch();
-    next.n = n_new;
-    next.nnz = 0;  // arrives with the step's final read-back (Ctl::nnz)
+    // ---- the one read-back of the phase
+    const IncHead fin = read_back<IncHead>(&ictr->h);
+    if (fin.overflow) return false;
+    if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+    PB_CUDA(cudaMemcpyAsync(&c->nnz, &ictr->h.nnz_new, 4, cudaMemcpyDeviceToDevice, stream));
+    inc_expanded_total += fin.expanded_total;
+    next.n = fin.n_new;
+    next.nnz = fin.nnz_new;
     next.q_nom = kept;
     next.order = m;
     next.max_row = width;
     next.has_h = true;
     next.has_full = true;
     ++inc_steps;
-    inc_side_keys_total += side_n;
+    inc_side_keys_total += fin.side_total;
     return true;
 }
 

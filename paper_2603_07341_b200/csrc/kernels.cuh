@@ -34,15 +34,20 @@ struct GrowCounters {
 // K2  dedup: counting sort by insertion gap, then exact dedup + ranking inside each (tiny) gap segment
 // ================================================================================================
 
-/// perm[seg_start[gap] + k] = candidate id, k = arrival order inside the gap (gap_fill starts at zero).
+/// The dedup kernels work on SEGMENTS of candidates: segment id = insertion gap >> sh.  sh = 0 (the full expansion:
+/// one segment per gap, mean length 1-3) or a coarse bucket of 2^sh table rows (the incremental adapt phase: a few
+/// 1e4 candidates against a table of millions of rows -- no table-sized counter arrays).  Inside a segment candidates
+/// are ordered by KEY, which also orders them by gap (the gap is monotone in the key).  The candidate count is read
+/// from device memory and clamped to nc_cap (an overflowing expansion leaves a larger count behind).
+/// perm[seg_start[seg] + k] = candidate id, k = arrival order inside the segment (gap_fill starts at zero).
 static __global__ void __launch_bounds__(NT) place_candidates_kernel(const uint32_t* __restrict__ cand_gap,
-                                                              const uint32_t* __restrict__ nc_ptr,
+                                                              const uint32_t* __restrict__ nc_ptr, uint32_t nc_cap, int sh,
                                                               const uint32_t* __restrict__ seg_start,
                                                               uint32_t* __restrict__ gap_fill,
                                                               uint32_t* __restrict__ perm) {
-    const uint32_t nc = *nc_ptr;  // the candidate count stays on the device: no host round trip before the merge
+    const uint32_t nc = min(*nc_ptr, nc_cap);  // the count stays on the device: no host round trip before the merge
     for (uint32_t c = blockIdx.x * NT + threadIdx.x; c < nc; c += gridDim.x * NT) {
-        const uint32_t g = cand_gap[c];
+        const uint32_t g = cand_gap[c] >> sh;
         const uint32_t r = atomicAdd(gap_fill + g, 1u);
         perm[seg_start[g] + r] = c;
     }
@@ -57,14 +62,14 @@ template <int W>
 static __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t* __restrict__ cand_keys,
                                                            const uint32_t* __restrict__ cand_gap,
                                                            const uint32_t* __restrict__ perm,
-                                                           const uint32_t* __restrict__ nc_ptr,
+                                                           const uint32_t* __restrict__ nc_ptr, uint32_t nc_cap, int sh,
                                                            const uint32_t* __restrict__ seg_start,
                                                            uint32_t* __restrict__ seg_rank,
                                                            uint32_t* __restrict__ gap_kept, GrowCounters* ctr) {
-    const uint32_t nc = *nc_ptr;
+    const uint32_t nc = min(*nc_ptr, nc_cap);
     for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
         const uint32_t c = perm[s];
-        const uint32_t g = cand_gap[c];
+        const uint32_t g = cand_gap[c] >> sh;
         const uint32_t s0 = seg_start[g], s1 = seg_start[g + 1];
         const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
         bool dup = false;
@@ -72,7 +77,7 @@ static __global__ void __launch_bounds__(NT) segment_dedup_kernel(const uint32_t
         for (uint32_t t = s0; t < s && !dup; ++t) dup = row_cmp<W>(cand_keys + size_t(perm[t]) * W, k) == 0;
         seg_rank[s] = dup ? SEG_DUP : 0u;
         if (!dup) atomicAdd(gap_kept + g, 1u);
-        if (s == s0 && s1 - s0 > 32) atomicMax(&ctr->max_seg, s1 - s0);
+        if (ctr && s == s0 && s1 - s0 > 32) atomicMax(&ctr->max_seg, s1 - s0);
     }
 }
 
@@ -82,14 +87,14 @@ template <int W>
 static __global__ void __launch_bounds__(NT) segment_rank_kernel(const uint32_t* __restrict__ cand_keys,
                                                           const uint32_t* __restrict__ cand_gap,
                                                           const uint32_t* __restrict__ perm,
-                                                          const uint32_t* __restrict__ nc_ptr,
+                                                          const uint32_t* __restrict__ nc_ptr, uint32_t nc_cap, int sh,
                                                           const uint32_t* __restrict__ seg_start,
                                                           volatile uint32_t* seg_rank) {
-    const uint32_t nc = *nc_ptr;
+    const uint32_t nc = min(*nc_ptr, nc_cap);
     for (uint32_t s = blockIdx.x * NT + threadIdx.x; s < nc; s += gridDim.x * NT) {
         if (seg_rank[s] == SEG_DUP) continue;
         const uint32_t c = perm[s];
-        const uint32_t g = cand_gap[c];
+        const uint32_t g = cand_gap[c] >> sh;
         const uint32_t s0 = seg_start[g], s1 = seg_start[g + 1];
         if (s1 - s0 == 1) continue;  // alone in its gap: rank 0 already stored
         const Key<W> k = load_key<W>(cand_keys + size_t(c) * W);
@@ -467,9 +472,12 @@ static __global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned l
 
 /// mode 0: keep every supported row (w > 0).  mode 1: keep w > cutoff, and w == cutoff too when
 /// keep_ties; otherwise the ties are flagged separately for the host-side Fisher-Yates draw.
+/// keep (uint32 flags, n + 1 entries) and dist0 (the incremental adapt phase's BFS distances: 0 = kept, 255 = not)
+/// are both optional.
 static __global__ void __launch_bounds__(NT) select_flags_kernel(const double* __restrict__ w, uint32_t n, int mode,
                                                           const SelectCtl* __restrict__ ctl, int keep_ties,
-                                                          uint32_t* __restrict__ keep, uint32_t* __restrict__ tie) {
+                                                          uint32_t* __restrict__ keep, uint32_t* __restrict__ tie,
+                                                          uint8_t* __restrict__ dist0) {
     const unsigned long long cut = ctl->prefix;
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         const double ww = w[i];
@@ -489,11 +497,12 @@ static __global__ void __launch_bounds__(NT) select_flags_kernel(const double* _
                 }
             }
         }
-        keep[i] = kf;
+        if (keep) keep[i] = kf;
+        if (dist0) dist0[i] = kf ? 0 : 255;
         if (tie) tie[i] = tf;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        keep[n] = 0;
+        if (keep) keep[n] = 0;
         if (tie) tie[n] = 0;
     }
 }
@@ -506,8 +515,12 @@ static __global__ void __launch_bounds__(NT) compact_index_kernel(const uint32_t
         if (flag[i]) idx[pos[i]] = i;
 }
 
-static __global__ void set_flags_kernel(const uint32_t* __restrict__ idx, uint32_t cnt, uint32_t* __restrict__ flag) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) flag[idx[i]] = 1;
+static __global__ void set_flags_kernel(const uint32_t* __restrict__ idx, uint32_t cnt, uint32_t* __restrict__ flag,
+                                        uint8_t* __restrict__ dist0) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        if (flag) flag[idx[i]] = 1;
+        if (dist0) dist0[idx[i]] = 0;
+    }
 }
 
 /// out[pos[i]] = table[i] for flagged rows: ascending indices of a sorted parent stay sorted

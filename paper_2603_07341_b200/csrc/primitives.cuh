@@ -98,6 +98,47 @@ constexpr int LB_IPT = 16;
 constexpr int LB_TILE = NT * LB_IPT;
 constexpr unsigned long long LB_AGG = 1ull << 62, LB_PREFIX = 2ull << 62, LB_FLAGS = 3ull << 62;
 
+/// Decoupled look-back step of a single-pass scan, for kernels that fuse the scan with their own work: the CTA that
+/// owns tile `tile` (tiles are handed out through an atomic ticket, so every predecessor is already running) publishes
+/// its aggregate `total`, waits for the inclusive prefix of the tiles before it and publishes its own.  Returns the
+/// exclusive prefix of the tile in every thread.  status[] must be zero on entry; contains a CTA barrier.
+__device__ __forceinline__ uint32_t lookback_exclusive_prefix(unsigned long long* status, uint32_t tile, uint32_t total,
+                                                             uint32_t* s_prefix) {
+    if (threadIdx.x == 0) {
+        // 64-bit aligned stores are single transactions: flag and value arrive together
+        *reinterpret_cast<volatile unsigned long long*>(status + tile) = (tile == 0 ? LB_PREFIX : LB_AGG) | total;
+        if (tile == 0) *s_prefix = 0;
+    }
+    if (tile > 0 && threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        uint32_t prefix = 0;
+        int64_t idx = int64_t(tile) - 1;
+        for (;;) {
+            const int64_t j = idx - lane;
+            unsigned long long st = LB_PREFIX;  // before tile 0: an empty inclusive prefix
+            if (j >= 0) {
+                do {
+                    st = *reinterpret_cast<volatile unsigned long long*>(status + j);
+                } while ((st & LB_FLAGS) == 0);
+            }
+            const unsigned done = __ballot_sync(0xffffffffu, (st & LB_FLAGS) == LB_PREFIX);
+            const int stop = done ? __ffs(done) - 1 : 32;  // nearest tile that already knows its inclusive prefix
+            uint32_t part = (int(lane) <= stop) ? uint32_t(st) : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            prefix += part;
+            if (done) break;
+            idx -= 32;
+        }
+        if (lane == 0) {
+            *reinterpret_cast<volatile unsigned long long*>(status + tile) = LB_PREFIX | (uint32_t)(prefix + total);
+            *s_prefix = prefix;
+        }
+    }
+    __syncthreads();
+    return *s_prefix;
+}
+
 static __global__ void __launch_bounds__(NT) scan_lookback_kernel(const uint32_t* in, uint64_t n, uint32_t* out,
                                                            unsigned long long* status, unsigned* ticket) {
     __shared__ uint32_t smem[NT / 32];
@@ -123,39 +164,7 @@ static __global__ void __launch_bounds__(NT) scan_lookback_kernel(const uint32_t
     for (int i = 0; i < LB_IPT; ++i) s += v[i];
     uint32_t total;
     const uint32_t toff = block_exclusive_scan_u32(s, smem, total);
-    if (threadIdx.x == 0) {
-        // 64-bit aligned stores are single transactions: flag and value arrive together
-        *reinterpret_cast<volatile unsigned long long*>(status + tile) = (tile == 0 ? LB_PREFIX : LB_AGG) | total;
-        if (tile == 0) s_prefix = 0;
-    }
-    if (tile > 0 && threadIdx.x < 32) {
-        const uint32_t lane = threadIdx.x;
-        uint32_t prefix = 0;
-        int64_t idx = int64_t(tile) - 1;
-        for (;;) {
-            const int64_t j = idx - lane;
-            unsigned long long st = LB_PREFIX;  // before tile 0: an empty inclusive prefix
-            if (j >= 0) {
-                do {
-                    st = *reinterpret_cast<volatile unsigned long long*>(status + j);
-                } while ((st & LB_FLAGS) == 0);
-            }
-            const unsigned done = __ballot_sync(0xffffffffu, (st & LB_FLAGS) == LB_PREFIX);
-            const int stop = done ? __ffs(done) - 1 : 32;  // nearest tile that already knows its inclusive prefix
-            uint32_t part = (int(lane) <= stop) ? uint32_t(st) : 0u;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            prefix += part;
-            if (done) break;
-            idx -= 32;
-        }
-        if (lane == 0) {
-            *reinterpret_cast<volatile unsigned long long*>(status + tile) = LB_PREFIX | (uint32_t)(prefix + total);
-            s_prefix = prefix;
-        }
-    }
-    __syncthreads();
-    uint32_t run = s_prefix + toff;
+    uint32_t run = lookback_exclusive_prefix(status, tile, total, &s_prefix) + toff;
     if (base + LB_IPT <= n) {
         uint4* q = reinterpret_cast<uint4*>(out + base);
 #pragma unroll

@@ -322,7 +322,7 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
 
     uint32_t* keep = flag_keep.as<uint32_t>();
     if (support <= q_nom) {
-        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr);
+        select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr, nullptr);
         check_launch();
     } else {
         static const int shifts[6] = {53, 42, 31, 20, 9, 0};
@@ -339,7 +339,7 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
         sc = read_back<SelectCtl>(&c->select);  // identical on every rank: derived from all-reduced histograms
         const uint64_t need = q_nom - sc.count_gt;
         if (need >= sc.count_eq) {
-            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr);
+            select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr, nullptr);
             check_launch();
         } else {
             // gather the tie KEYS of all ranks, order them canonically, draw exactly as engine.hpp:137-142
@@ -351,7 +351,7 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
             flag_tie.ensure((size_t(n) + 1) * 4);
             pos_a.ensure((size_t(n) + 1) * 4);
             select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 0, keep,
-                                                      flag_tie.as<uint32_t>());
+                                                      flag_tie.as<uint32_t>(), nullptr);
             check_launch();
             PB_CUDA(cudaMemcpyAsync(pos_a.p, flag_tie.p, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
             exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
