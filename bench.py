@@ -298,6 +298,9 @@ def main():
     ap.add_argument("--cpu-baseline-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N = 1: run the SHARDED algorithms against a one-rank NCCL communicator (self-exchanges): what "
+                         "one rank of a multi-GPU job executes, minus the wire")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "torch", "gloo"],
                     help="N > 1: nccl = NCCL inside libpaces_b200.so (default); torch = torch.distributed callbacks over "
                          "NCCL; gloo = host-staged callbacks (test hook: several ranks on one GPU)")
@@ -339,6 +342,10 @@ def main():
         from paper_2603_07341_b200.dist import NcclComm, TorchComm
 
         comm = NcclComm(device=local) if transport == "nccl" else TorchComm(device=local)
+    elif args.sharded:
+        from paper_2603_07341_b200.dist import NcclComm
+
+        comm = NcclComm(device=local, rank=0, world=1)
 
     stream = torch.cuda.Stream()
     ctx = pb.Context(pb.ModelDef(**model), device=local, comm=comm)
@@ -360,7 +367,8 @@ def main():
         sampler = ClockSampler(local)
         run.reset_times()
         launches0 = ctx.kernel_launches
-        adapt0 = run.adapt_stats() if world == 1 else None
+        single = world == 1 and not args.sharded
+        adapt0 = run.adapt_stats() if single else None
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         sampler.start()
@@ -376,7 +384,7 @@ def main():
         dev_ms = ev0.elapsed_time(ev1)
         # ---- everything the line reports about the timed window is read HERE, before any further step
         times = run.times()
-        adapt1 = run.adapt_stats() if world == 1 else None
+        adapt1 = run.adapt_stats() if single else None
         launches = ctx.kernel_launches - launches0
         rows, nnz, t_now, steps_done = run.info()
         rows_g, nnz_g = run.global_sizes()
@@ -465,7 +473,7 @@ def main():
 
         # ---- e2e: paces::step with a host SparseState in and out, every step (pinned host buffers)
         e2e = e2e_miss = None
-        if not args.no_e2e and world == 1:
+        if not args.no_e2e and single:
             rows_now = run.info()[0]
             cap = int(rows_now * 1.25) + 1024
             hw = [torch.empty(cap * W, dtype=torch.int32).pin_memory() for _ in range(2)]
@@ -519,7 +527,7 @@ def main():
 
     # ---- CPU baseline on the same state (rank 0, N = 1)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.sharded:
         pyoracle, orc, kind = cpu_checker()
         om = orc.model(pyoracle.ModelDef(**model))
         w, c = run.state()
@@ -548,7 +556,7 @@ def main():
         phases["note"] = ("grow_ms = the whole incremental adapt phase (expansion + assembly + remap fused into one "
                           "pass over the previous H_eff); expmv_ms includes <H> (first Taylor order); the separate "
                           "assemble/remap/expectation timers are empty on this path and are not reported")
-        if world > 1 or (adapt1 and adapt1["incremental_steps"] == adapt0["incremental_steps"]):
+        if not single or (adapt1 and adapt1["incremental_steps"] == adapt0["incremental_steps"]):
             phases.update({k: times[k] / args.steps for k in ("assemble_ms", "remap_ms", "expectation_ms")})
             phases["note"] = "full expansion path: grow / assemble / remap / expectation are separate phases"
         line = {
@@ -562,7 +570,9 @@ def main():
                       "taylor_order": d["taylor_order"], "spinup_steps": spin, "words_per_key": W,
                       "adapt_in_window": ({k: adapt1[k] - adapt0[k] for k in adapt1} if adapt1 else None),
                       "note": "sizes at the end of the timed window"},
-            "parallelism": "single GPU" if world == 1 else
+            "transport": ctx.comm_describe() or None,
+            "parallelism": ("single GPU" if single else "single GPU, sharded algorithms over a one-rank NCCL communicator")
+            if world == 1 else
             f"state and subspace sharded over {world} GPUs by hash of the basis key (phonon part); NCCL all-to-all of "
             "candidate keys / look-ups / halos inside libpaces_b200.so",
             "l2": "per-step working set (~150 B/row x q_true) exceeds the 126 MB L2; no flush between steps",

@@ -102,8 +102,8 @@ uint64_t pb200_kernel_launches(const pb200_ctx* ctx);
 uint64_t pb200_mix_seed(uint64_t x);
 
 /* ---- multi-GPU: one process (and one context) per GPU; the table is sharded by hash of the phonon part of the
- * basis key.  The library does not talk to NCCL itself: the host supplies the collectives
- * (torch.distributed over NCCL in production -- plumbing -- or any other transport) through this table.  Device
+ * basis key.  The collectives come either from NCCL inside the library (pb200_ctx_set_comm_nccl,
+ * below -- the production path) or from the host through this table (any other transport; tests).  Device
  * variants receive DEVICE pointers on the context's device plus the context's stream; they must be complete or
  * stream-ordered on that stream when they return.  Host variants are small blocking collectives on host memory.
  * All ranks call every pb200_* function collectively and in the same order.  Every callback returns 0 on success. */
@@ -118,9 +118,24 @@ typedef struct pb200_comm_ops {
                          const uint64_t* recv_counts, uint64_t elem_bytes, void* stream);
     int (*allreduce_f64_dev)(void* user, double* buf, uint64_t n, void* stream);   /* sum, in place */
     int (*allreduce_u32_dev)(void* user, uint32_t* buf, uint64_t n, void* stream); /* sum, in place */
+    /* Optional (may be NULL): alltoallv_dev on an INDEPENDENT channel that is allowed to run concurrently with the
+     * other collectives (the halo exchange of a Taylor order, issued on its own stream beside the interior rows of
+     * the SpMV).  NULL: the halo exchange is ordered on the context's stream like everything else. */
+    int (*alltoallv_dev2)(void* user, const void* send, const uint64_t* send_counts, void* recv,
+                          const uint64_t* recv_counts, uint64_t elem_bytes, void* stream);
 } pb200_comm_ops;
 /* Must be called before pb200_model_set; world == 1 (or never calling it) is the single-GPU path. */
 int pb200_ctx_set_comm(pb200_ctx* ctx, int rank, int world, const pb200_comm_ops* ops);
+/* The production transport: NCCL inside the library (NVLink 5 / NVSwitch on a B200 box; libnccl.so.2 is resolved at
+ * run time).  Rank 0 calls pb200_nccl_unique_id and hands the PB200_NCCL_ID_BYTES bytes to every rank (MPI, a file,
+ * torch.distributed, ... -- the only thing the host has to move); then every rank calls pb200_ctx_set_comm_nccl
+ * (collective: it creates the communicators) before pb200_model_set.  The callback table above stays available for
+ * other transports and for tests (several ranks on one GPU, which NCCL refuses). */
+#define PB200_NCCL_ID_BYTES 256
+int pb200_nccl_unique_id(uint8_t* id);
+int pb200_ctx_set_comm_nccl(pb200_ctx* ctx, int rank, int world, const uint8_t* id);
+/* One line about the context's transport (NCCL version, rank, collectives issued so far); "" without one. */
+const char* pb200_comm_describe(pb200_ctx* ctx);
 /* Shard owner of a key (host-side restatement of the device rule), and this context's rank/world. */
 int pb200_owner_of(const pb200_ctx* ctx, const uint32_t* key, uint32_t world, uint32_t* owner);
 

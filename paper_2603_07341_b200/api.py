@@ -26,7 +26,7 @@ intp = C.POINTER(C.c_int)
 
 EXPORTED_SYMBOLS = [
     "pb200_ctx_create", "pb200_ctx_destroy", "pb200_last_error", "pb200_version", "pb200_ctx_set_stream",
-    "pb200_kernel_launches", "pb200_mix_seed", "pb200_ctx_set_comm", "pb200_owner_of", "pb200_model_set", "pb200_model_info", "pb200_pack", "pb200_unpack",
+    "pb200_kernel_launches", "pb200_mix_seed", "pb200_ctx_set_comm", "pb200_nccl_unique_id", "pb200_ctx_set_comm_nccl", "pb200_comm_describe", "pb200_owner_of", "pb200_model_set", "pb200_model_info", "pb200_pack", "pb200_unpack",
     "pb200_apply_terms", "pb200_grow", "pb200_space_info", "pb200_space_get", "pb200_truncate_select", "pb200_remap",
     "pb200_csr_matvec", "pb200_csr_expectation", "pb200_expmv", "pb200_state_norm", "pb200_exciton_density",
     "pb200_dipole_amplitude", "pb200_phonon_numbers", "pb200_weight_histogram", "pb200_run_weight_histogram", "pb200_run_begin", "pb200_run_step", "pb200_run_info",
@@ -130,6 +130,10 @@ def load_library():
     L.pb200_mix_seed.argtypes = [C.c_uint64]
     L.pb200_mix_seed.restype = C.c_uint64
     L.pb200_ctx_set_comm.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.pb200_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.pb200_ctx_set_comm_nccl.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_uint8)]
+    L.pb200_comm_describe.argtypes = [vp]
+    L.pb200_comm_describe.restype = C.c_char_p
     L.pb200_owner_of.argtypes = [vp, u32p, C.c_uint32, u32p]
     L.pb200_model_set.argtypes = [vp, C.c_int, C.c_int, u32p, f64p, C.c_int, f64p, C.c_int, f64p, C.c_int, f64p,
                                   C.c_int, C.c_uint32]
@@ -232,7 +236,13 @@ class Context:
         """Sharded (multi-GPU) mode: `comm` is a paper_2603_07341_b200.dist.TorchComm (or anything exposing
         rank, world and a pb200_comm_ops struct as .ops).  Call before set_model."""
         self.comm = comm  # keeps the callbacks alive
+        if hasattr(comm, "attach"):  # NcclComm: the transport lives inside the library
+            comm.attach(self)
+            return
         self._ck(self.lib.pb200_ctx_set_comm(self.h, int(comm.rank), int(comm.world), C.addressof(comm.ops)))
+
+    def comm_describe(self) -> str:
+        return self.lib.pb200_comm_describe(self.h).decode()
 
     def owner_of(self, key, world):
         key = _u32(key)

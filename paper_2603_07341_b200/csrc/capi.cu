@@ -115,7 +115,13 @@ uint64_t pb200_mix_seed(uint64_t x) {
 
 int pb200_ctx_set_comm(pb200_ctx* ctx, int rank, int world, const pb200_comm_ops* ops) {
     return guarded(ctx, [&](Engine& e) {
-        need(world >= 1 && world <= 64 && rank >= 0 && rank < world, "set_comm: bad rank/world (world <= 64)");
+        // the routing kernels keep per-peer counters in 64-entry shared-memory tables (sharded.cuh)
+        need(world >= 1 && world <= MAX_PEERS && rank >= 0 && rank < world, "set_comm: bad rank/world (world <= 64)");
+        if (e.nccl) {
+            e.sync();
+            nccl_transport_destroy(e.nccl);
+            e.nccl = nullptr;
+        }
         if (world > 1) {
             need(ops && ops->allreduce_f64_host && ops->allreduce_u64_host && ops->alltoall_u64_host &&
                      ops->allgather_host && ops->alltoallv_dev && ops->allreduce_f64_dev && ops->allreduce_u32_dev,
@@ -124,8 +130,51 @@ int pb200_ctx_set_comm(pb200_ctx* ctx, int rank, int world, const pb200_comm_ops
         }
         e.rank = rank;
         e.world = world;
+        e.sharded = world > 1;
         e.has_state = false;
     });
+}
+
+int pb200_nccl_unique_id(uint8_t* id) {
+    if (!id) return PB200_ERR_ARG;
+    try {
+        nccl_make_unique_id(id);
+        return PB200_OK;
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        return PB200_ERR_CUDA;
+    }
+}
+
+int pb200_ctx_set_comm_nccl(pb200_ctx* ctx, int rank, int world, const uint8_t* id) {
+    return guarded(ctx, [&](Engine& e) {
+        need(id != nullptr, "set_comm_nccl: null id");
+        need(world >= 1 && world <= MAX_PEERS && rank >= 0 && rank < world, "set_comm_nccl: bad rank/world (world <= 64)");
+        e.sync();
+        if (e.nccl) {
+            nccl_transport_destroy(e.nccl);
+            e.nccl = nullptr;
+        }
+        try {
+            e.nccl = nccl_transport_create(e.device, rank, world, id, &e.stream);
+        } catch (const std::exception& ex) {
+            throw CudaFail(ex.what());
+        }
+        e.ops = nccl_transport_ops(e.nccl);
+        e.rank = rank;
+        e.world = world;
+        // a one-rank communicator still runs the sharded algorithms (every exchange is a self-exchange): the
+        // transport's self-test on a single GPU
+        e.sharded = true;
+        e.has_state = false;
+    });
+}
+
+const char* pb200_comm_describe(pb200_ctx* ctx) {
+    if (!ctx) return "";
+    Engine& e = ctx->eng;
+    e.comm_info = e.nccl ? nccl_transport_describe(e.nccl) : (e.sharded ? std::string("host-supplied callbacks") : std::string());
+    return e.comm_info.c_str();
 }
 
 int pb200_owner_of(const pb200_ctx* ctx, const uint32_t* key, uint32_t world, uint32_t* owner) {
@@ -397,7 +446,7 @@ int pb200_run_weight_histogram(pb200_ctx* ctx, uint64_t bins, pb200_weight_hist*
     return guarded(ctx, [&](Engine& e) {
         need(out != nullptr, "run_weight_histogram: null pointer");
         if (!e.has_state) throw ArgError("no resident run: call pb200_run_begin first");
-        if (e.world > 1) throw ArgError("run_weight_histogram: gather the shards first (single-GPU operator)");
+        if (e.sharded) throw ArgError("run_weight_histogram: gather the shards first (single-GPU operator)");
         e.weight_histogram(e.coeff[e.ccur].as<double2>(), e.space[e.cur].n, bins, out, rank, weight, cap, npts);
     });
 }
@@ -429,8 +478,8 @@ int pb200_run_global(const pb200_ctx* ctx, uint64_t* rows_global, uint64_t* nnz_
     if (!ctx || !ctx->eng.has_state) return PB200_ERR_ARG;
     const Engine& e = ctx->eng;
     const Space& sp = e.space[e.cur];
-    if (rows_global) *rows_global = e.world > 1 ? sp.n_global : sp.n;
-    if (nnz_global) *nnz_global = e.world > 1 ? sp.nnz_global : sp.nnz;
+    if (rows_global) *rows_global = e.sharded ? sp.n_global : sp.n;
+    if (nnz_global) *nnz_global = e.sharded ? sp.nnz_global : sp.nnz;
     return PB200_OK;
 }
 
@@ -569,7 +618,7 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         // uploaded -- the comparison needs it -- but the keys no longer sit on the critical path: their upload and
         // comparison run on the copy stream beside the step and are checked before anything is committed.
         const Space& res = e.space[e.cur];
-        const bool candidate = e.world == 1 && e.has_state && e.has_cfg && res.has_h && res.has_full && res.n == rows &&
+        const bool candidate = !e.sharded && e.has_state && e.has_cfg && res.has_h && res.has_full && res.n == rows &&
                                e.steps_done + 1 == step_index && e.t == t && e.cfg.m == c.m && e.cfg.q_nom == c.q_nom &&
                                e.cfg.dt == c.dt && e.cfg.rtol == c.rtol && e.cfg.max_order == c.max_order &&
                                e.cfg.substeps == c.substeps && e.cfg.seed == c.seed &&

@@ -60,6 +60,9 @@ Engine::Engine(int dev) : device(dev) {
     for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
     PB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PB_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
+    PB_CUDA(cudaStreamCreateWithFlags(&halo_stream, cudaStreamNonBlocking));
+    PB_CUDA(cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming));
+    PB_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_words, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_table, cudaEventDisableTiming));
     ctl.ensure(sizeof(Ctl));
@@ -83,6 +86,13 @@ Engine::~Engine() {
         cudaStreamSynchronize(io_stream);
         cudaStreamDestroy(io_stream);
     }
+    if (halo_stream) {
+        cudaStreamSynchronize(halo_stream);
+        cudaStreamDestroy(halo_stream);
+    }
+    if (nccl) nccl_transport_destroy(nccl);
+    if (ev_pack) cudaEventDestroy(ev_pack);
+    if (ev_halo) cudaEventDestroy(ev_halo);
     if (ev_words) cudaEventDestroy(ev_words);
     if (ev_table) cudaEventDestroy(ev_table);
     if (pinned) cudaFreeHost(pinned);
@@ -569,7 +579,7 @@ double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t n
                      uint32_t nd, double2* dst_c) {
     remap_async(src_words, src_c, ns, dst_words, nd, dst_c);
     const double d = read_back<double>(dctl()->out);
-    return world > 1 ? allreduce_host(d) : d;
+    return sharded ? allreduce_host(d) : d;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -583,7 +593,7 @@ void Engine::expectation_async(const Space& sp, const double2* x) {
 
 void Engine::expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite) {
     Ctl* c = dctl();
-    if (world > 1) {
+    if (sharded) {
         // the SpMV reads halo columns: stage x next to its halo
         term[0].ensure((size_t(sp.n) + sp.halo_n) * 16 + 16);
         PB_CUDA(cudaMemcpyAsync(term[0].p, x, size_t(sp.n) * 16, cudaMemcpyDeviceToDevice, stream));
@@ -595,7 +605,7 @@ void Engine::expectation(const Space& sp, const double2* x, double* exp_out, dou
         double v[3];
     };
     R r = read_back<R>(c->out + 1);
-    if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, r.v, 3), "allreduce_f64_host");
+    if (sharded) comm_check(ops.allreduce_f64_host(ops.user, r.v, 3), "allreduce_f64_host");
     if (exp_out) *exp_out = r.v[0];
     if (norm2_out) *norm2_out = r.v[1];
     if (check_finite && r.v[2] != 0.0) throw PacesError("expmv: non-finite input coefficient");
@@ -747,7 +757,7 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
         check_launch();
         PB_CUDA(cudaMemcpyAsync(density, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
         sync();
-        if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, density, uint64_t(L)), "allreduce_f64_host");
+        if (sharded) comm_check(ops.allreduce_f64_host(ops.user, density, uint64_t(L)), "allreduce_f64_host");
     }
     if (phonons) {
         if (md.kind != 1) throw PacesError("phonon numbers: not a Holstein model");
@@ -761,14 +771,14 @@ void Engine::observe(const uint32_t* words, const double2* cvec, uint32_t n, dou
         check_launch();
         PB_CUDA(cudaMemcpyAsync(phonons, d_out, size_t(L) * 8, cudaMemcpyDeviceToHost, stream));
         sync();
-        if (world > 1) comm_check(ops.allreduce_f64_host(ops.user, phonons, uint64_t(L)), "allreduce_f64_host");
+        if (sharded) comm_check(ops.allreduce_f64_host(ops.user, phonons, uint64_t(L)), "allreduce_f64_host");
     }
     if (amp) {
         PB_DISPATCH_W(W, dipole_kernel<W><<<1, 256, 0, stream>>>(md, words, cvec, n, d_found, d_out));
         check_launch();
         PB_CUDA(cudaMemcpyAsync(amp, d_out, 16, cudaMemcpyDeviceToHost, stream));
         sync();
-        if (world > 1) {
+        if (sharded) {
             // the L vacuum keys share one phonon configuration, hence one owner; the others contribute zeros,
             // but the 1/sqrt(L) factor was applied per rank, which is exact for the single non-zero term
             comm_check(ops.allreduce_f64_host(ops.user, amp, 2), "allreduce_f64_host");
@@ -808,7 +818,7 @@ void Engine::run_begin(const pb200_run_cfg& c) {
     std::vector<cplx> amps;
     build_seed_state(hm, c.init_kind, c.init_site, c.n_entries, c.entry_occ, c.entry_amp, words, amps);
     const int W = md.W;
-    if (world > 1) {
+    if (sharded) {
         // every rank builds the same normalised seed list and keeps the keys it owns
         std::vector<uint32_t> w2;
         std::vector<cplx> a2;
@@ -827,7 +837,7 @@ void Engine::run_begin(const pb200_run_cfg& c) {
     PB_CUDA(cudaMemcpyAsync(aux_coeff.p, amps.data(), amps.size() * 16, cudaMemcpyHostToDevice, stream));
     sync();
     Space& sp = space[cur];
-    if (world > 1)
+    if (sharded)
         grow_sharded(aux_words.as<uint32_t>(), ns, c.m_init, sp);
     else
         grow(aux_words.as<uint32_t>(), ns, c.m_init, sp);
@@ -858,14 +868,14 @@ void Engine::run_step(pb200_diag* out) {
         PB_CUDA(cudaEventRecord(ev[5], stream));
         rec.norm_pre = std::sqrt(n2);
         rec.norm_post = rec.norm_pre;
-        rec.q_true = world > 1 ? old.n_global : old.n;
+        rec.q_true = sharded ? old.n_global : old.n;
         rec.energy = e;
         coeff[ccur ^ 1].ensure(size_t(old.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
         PB_CUDA(cudaMemcpyAsync(psi, c_old, size_t(old.n) * 16, cudaMemcpyDeviceToDevice, stream));
         int order = 0;
         double ltn = 0, lcn = 0;
-        if (world > 1)
+        if (sharded)
             expmv_sharded(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         else
             expmv(old, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
@@ -892,14 +902,14 @@ void Engine::run_step(pb200_diag* out) {
             bool& flag;
             ~DeferGuard() { flag = false; }
         } defer_guard{defer_reads};
-        defer_reads = (world == 1);
+        defer_reads = (!sharded);
         // incremental adapt (incremental.cuh): needs the previous H_eff with its expansion flags; the full path
         // remains for the first step after a load, m = 0, a memory cap (its transcript accounting) and overflows
         // (BFS distances are bytes with DIST_INF = 255: larger neighbour orders take the full path)
-        bool incremental = world == 1 && (!io || io->cached) && old.has_h && old.has_full && cfg.m >= 1 &&
+        bool incremental = !sharded && (!io || io->cached) && old.has_h && old.has_full && cfg.m >= 1 &&
                            cfg.m <= INC_MAX_ORDER && memory_cap_bytes() == 0 &&
                            std::getenv("PB200_NO_INCREMENTAL") == nullptr;
-        const uint32_t kept = world > 1
+        const uint32_t kept = sharded
                                   ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
                                   : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
                                            !incremental);
@@ -916,7 +926,7 @@ void Engine::run_step(pb200_diag* out) {
         }
         if (incremental) {
             PB_CUDA(cudaEventRecord(ev[2], stream));
-        } else if (world > 1) {
+        } else if (sharded) {
             // grow() = expansion + assembly; split the timer inside via ev[2]
             grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
         } else {
@@ -936,7 +946,7 @@ void Engine::run_step(pb200_diag* out) {
                 PB_CUDA(cudaMemcpyAsync(io->out_words, next.words.p, size_t(next.n) * md.W * 4, cudaMemcpyDeviceToHost,
                                         copy_stream));
         }
-        require_memory((world > 1 ? next.n_global : uint64_t(next.n)) * 16 * 4, "state vectors");
+        require_memory((sharded ? next.n_global : uint64_t(next.n)) * 16 * 4, "state vectors");
         coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
         double e = 0, n2 = 0;
@@ -955,7 +965,7 @@ void Engine::run_step(pb200_diag* out) {
         }
         int order = 0;
         double ltn = 0, lcn = 0;
-        if (world > 1) {
+        if (sharded) {
             expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         } else {
             try {
@@ -975,7 +985,7 @@ void Engine::run_step(pb200_diag* out) {
             require_memory(uint64_t(next.nnz) * 2 * 16, "matrix assembly buffer");
         }
         rec.norm_post = std::sqrt(n2);
-        rec.q_true = world > 1 ? next.n_global : next.n;
+        rec.q_true = sharded ? next.n_global : next.n;
         rec.energy = e;
         PB_CUDA(cudaEventRecord(ev[6], stream));
         if (io && next.n)

@@ -17,6 +17,7 @@
 #include "window.cuh"
 #include "incremental.cuh"
 #include "sharded.cuh"
+#include "nccl_comm.hpp"
 
 namespace pb {
 
@@ -105,6 +106,7 @@ struct DevBuf {
 /// Slack behind row_ptr / col / val: the Taylor tile kernels fetch 16-byte-aligned slices with bulk copies, which may
 /// read up to 15 bytes past the last element.
 constexpr size_t CSR_PAD = 64;
+constexpr int MAX_PEERS = 64;  // per-peer counters live in 64-entry shared-memory tables (sharded.cuh)
 
 /// EffectiveSpace (subspace.hpp:76-82) on the device: sorted key table + CSR H_eff.
 struct Space {
@@ -126,6 +128,9 @@ struct Space {
     DevBuf send_idx;                          // local rows to pack, grouped by destination rank
     std::vector<uint64_t> halo_send, halo_recv;  // per-peer element counts
     uint64_t n_global = 0, nnz_global = 0;
+    // rows without / with halo columns (sharded SpMV: the former run while the halo is in flight)
+    uint32_t n_interior = 0, n_boundary = 0;
+    DevBuf rows_int, rows_bnd;
 };
 
 struct Engine {
@@ -197,7 +202,13 @@ struct Engine {
 
     // multi-GPU (one context per rank); world == 1 is the single-GPU path
     int rank = 0, world = 1;
+    bool sharded = false;          // the sharded algorithms are in use (world > 1, or a one-rank NCCL communicator)
     pb200_comm_ops ops{};
+    NcclTransport* nccl = nullptr;  // owned: the in-library transport (pb200_ctx_set_comm_nccl)
+    std::string comm_info;
+    cudaStream_t halo_stream = nullptr;  // halo exchange beside the interior rows (ops.alltoallv_dev2)
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    DevBuf row_class, scan_aligned;
     DevBuf out_keys, out_dest, route_pos, route_ctr, sendbuf, recvbuf, req_keys, req_dest, req_pos, reply, answer,
         found, halo_flag, tmp_cnt, halo_stage, sel_keys;
     std::vector<uint64_t> h_send, h_recv;
@@ -222,6 +233,11 @@ struct Engine {
     /// exchanges h_send -> h_recv and the bucketed device buffer; returns total received elements
     uint64_t exchange(const void* send, void* recv_buf_owner, DevBuf& recv, uint64_t elem_bytes);
     void halo_exchange(const Space& sp, double2* x);
+    /// pack on the context's stream, exchange on the halo stream (when the transport has an independent channel);
+    /// halo_wait() makes the context's stream wait for the arrival
+    void halo_start(const Space& sp, double2* x);
+    void halo_wait();
+    void classify_rows(Space& sp);
     void grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out);
     void assemble_sharded(Space& sp);
     uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,

@@ -90,6 +90,54 @@ void Engine::halo_exchange(const Space& sp, double2* x) {
                "alltoallv_dev(halo)");
 }
 
+void Engine::halo_start(const Space& sp, double2* x) {
+    halo_stage.ensure(size_t(sp.send_total) * 16 + 16);
+    if (sp.send_total) {
+        halo_pack_kernel<<<grid_for(sp.send_total), NT, 0, stream>>>(x, sp.send_idx.as<uint32_t>(), sp.send_total,
+                                                                     halo_stage.as<double2>());
+        check_launch();
+    }
+    if (ops.alltoallv_dev2) {
+        // independent channel: the exchange runs on its own stream beside the rows that need no halo
+        PB_CUDA(cudaEventRecord(ev_pack, stream));
+        PB_CUDA(cudaStreamWaitEvent(halo_stream, ev_pack, 0));
+        comm_check(ops.alltoallv_dev2(ops.user, halo_stage.p, sp.halo_send.data(), x + sp.n, sp.halo_recv.data(), 16,
+                                      halo_stream),
+                   "alltoallv_dev2(halo)");
+        PB_CUDA(cudaEventRecord(ev_halo, halo_stream));
+    } else {
+        comm_check(ops.alltoallv_dev(ops.user, halo_stage.p, sp.halo_send.data(), x + sp.n, sp.halo_recv.data(), 16, stream),
+                   "alltoallv_dev(halo)");
+    }
+}
+
+void Engine::halo_wait() {
+    if (ops.alltoallv_dev2) PB_CUDA(cudaStreamWaitEvent(stream, ev_halo, 0));
+}
+
+/// Splits the rows of a sharded space into those without halo columns (they can run while the halo is in flight)
+/// and those with.
+void Engine::classify_rows(Space& sp) {
+    const uint32_t n = sp.n;
+    row_class.ensure((size_t(n) + 1) * 4 + 8);
+    uint32_t* flag = row_class.as<uint32_t>();
+    row_has_halo_kernel<<<grid_for(uint64_t(n) + 1), NT, 0, stream>>>(n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(), flag);
+    check_launch();
+    scan_aligned.ensure((size_t(n) + 1) * 4 + 64);
+    PB_CUDA(cudaMemcpyAsync(scan_aligned.p, flag, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
+    exclusive_scan(scan_aligned.as<uint32_t>(), uint64_t(n) + 1);
+    const uint32_t nb = read_back<uint32_t>(scan_aligned.as<uint32_t>() + n);
+    sp.n_boundary = nb;
+    sp.n_interior = n - nb;
+    sp.rows_int.ensure(size_t(sp.n_interior) * 4 + 4);
+    sp.rows_bnd.ensure(size_t(nb) * 4 + 4);
+    if (n) {
+        split_rows_kernel<<<grid_for(n), NT, 0, stream>>>(n, flag, scan_aligned.as<uint32_t>(), sp.rows_int.as<uint32_t>(),
+                                                          sp.rows_bnd.as<uint32_t>());
+        check_launch();
+    }
+}
+
 // ------------------------------------------------------------------------------------------------
 // grow_subspace on shards
 // ------------------------------------------------------------------------------------------------
@@ -286,6 +334,7 @@ void Engine::assemble_sharded(Space& sp) {
     sp.nnz = nnz;
     sp.max_row = width;
     sp.has_h = true;
+    classify_rows(sp);
     uint64_t g[2] = {n, nnz};
     comm_check(ops.allreduce_u64_host(ops.user, g, 2), "allreduce_u64_host");
     sp.n_global = g[0];
@@ -414,7 +463,10 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
 }
 
 // ------------------------------------------------------------------------------------------------
-// expmv on shards: halo exchange before every SpMV, all-reduced norms before the stop rule
+// expmv on shards.  Per order: pack + halo exchange (own channel / stream when the transport has one), the rows
+// without halo columns meanwhile, then the rows with halo columns, ONE all-reduce of the partial norms, the stop rule
+// on every rank.  Orders are paired as on one GPU (taylor.cu): an order whose predecessor missed the stop rule leaves
+// c alone and its |term|^2 rides on the next order's all-reduce.  Nothing here returns to the host between orders.
 // ------------------------------------------------------------------------------------------------
 void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
                            int* order_used, double* last_term_norm, double* last_c_norm) {
@@ -428,7 +480,11 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
     term[0].ensure(ext);
     term[1].ensure(ext);
     const double dt_sub = dt / substeps;
-    const int g = grid_for(n);
+    const int gi = grid_for(sp.n_interior), gb = grid_for(sp.n_boundary);
+    const uint32_t* rp = sp.row_ptr.as<uint32_t>();
+    const int32_t* cl = sp.col.as<int32_t>();
+    const double* vl = sp.val.as<double>();
+    double* pt = partials.as<double>();
     TaylorCtl tc{};
     PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
     for (int s = 0; s < substeps; ++s) {
@@ -442,25 +498,46 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
         }
         int order = 1;
         bool converged = false;
+        bool singles = !taylor_defer;
+        const int k0 = (last_order > 2 && (last_order & 1) == 0) ? 3 : 2;
         int batch = last_order > 2 ? last_order : 8;
         while (order <= max_order) {
             const int end = std::min(max_order, order + batch - 1);
             for (; order <= end; ++order) {
                 const double b = -dt_sub / double(order);
-                halo_exchange(sp, term[(order - 1) & 1].as<double2>());
-                taylor_launch_single(false, g, sm_count, stream, n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-                                     sp.val.as<double>(), term[(order - 1) & 1].as<double2>(),
-                                     term[order & 1].as<double2>(), c_vec, b, order, rtol, partials.as<double>(),
-                                     &c->taylor, 0, c->out, nullptr, sp.max_row);
+                double2* tin = term[(order - 1) & 1].as<double2>();
+                double2* tout = term[order & 1].as<double2>();
+                int mode = TAYLOR_ROWS_SINGLE;
+                if (!singles && order >= k0 && ((order - k0) & 1))
+                    mode = TAYLOR_ROWS_CATCHUP;
+                else if (!singles && order >= k0 && order < max_order)
+                    mode = TAYLOR_ROWS_DEFER;
+                halo_start(sp, tin);
+                taylor_launch_rows(mode, gi, stream, sp.n_interior, sp.rows_int.as<uint32_t>(), rp, cl, vl, tin, tout, c_vec, b,
+                                   order, pt, &c->taylor, c->out);
                 check_launch();
-                comm_check(ops.allreduce_f64_dev(ops.user, c->out, 2, stream), "allreduce_f64_dev");
-                taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
+                halo_wait();
+                taylor_launch_rows(mode, gb, stream, sp.n_boundary, sp.rows_bnd.as<uint32_t>(), rp, cl, vl, tin, tout, c_vec, b,
+                                   order, pt, &c->taylor, c->out + 4);
+                check_launch();
+                if (mode == TAYLOR_ROWS_DEFER) continue;  // its |term|^2 rides on the next order's all-reduce
+                comm_check(ops.allreduce_f64_dev(ops.user, c->out, 8, stream), "allreduce_f64_dev");
+                if (mode == TAYLOR_ROWS_CATCHUP)
+                    taylor_stop_pair_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
+                else
+                    taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
                 check_launch();
             }
             tc = read_back<TaylorCtl>(&c->taylor);
             if (tc.done) {
                 converged = true;
                 break;
+            }
+            if (tc.bail) {  // order tc.bail has to run SINGLE (everything launched after it returned at once)
+                order = tc.bail;
+                singles = true;
+                tc.bail = 0;
+                PB_CUDA(cudaMemsetAsync(&c->taylor.bail, 0, sizeof(int), stream));
             }
             batch = 2;
         }
@@ -470,6 +547,8 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
             throw PacesError("expmv: Taylor series did not converge within max_order=" + std::to_string(max_order) +
                              "; reduce dt or increase substeps");
     }
+    times.taylor_deferred += uint64_t(tc.deferred);
+    times.taylor_deferred_rows += uint64_t(tc.deferred) * n;
     last_order = tc.order_used;
     if (order_used) *order_used = tc.order_used;
     if (last_term_norm) *last_term_norm = tc.last_term_norm;

@@ -249,11 +249,13 @@ static __global__ void __launch_bounds__(NT) halo_pack_kernel(const double2* __r
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < cnt; j += gridDim.x * NT) send[j] = x[send_idx[j]];
 }
 
-/// Stop rule of propagator.hpp:76-84 on globally reduced sums tot = (|term|^2, |c|^2).
+/// Stop rule of propagator.hpp:76-84 on the globally reduced sums of one order.  tot[0..3] / tot[4..7] are the
+/// deposits of the two launches of the order (rows without / with halo columns): |term|^2 = tot[0] + tot[4],
+/// |c|^2 = tot[1] + tot[5].  Every rank holds the same all-reduced numbers, hence the same flags.
 static __global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restrict__ tot, int order, double rtol) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (ctl->done) return;
-    const double tn = __dsqrt_rn(tot[0]), rn = __dsqrt_rn(tot[1]);
+    if (ctl->done || ctl->bail) return;
+    const double tn = __dsqrt_rn(__dadd_rn(tot[0], tot[4])), rn = __dsqrt_rn(__dadd_rn(tot[1], tot[5]));
     if (order > ctl->order_used) ctl->order_used = order;
     ctl->last_order = order;
     ctl->last_term_norm = tn;
@@ -261,6 +263,52 @@ static __global__ void taylor_stop_kernel(TaylorCtl* ctl, const double* __restri
     const int streak = (tn <= __dmul_rn(rtol, rn)) ? ctl->streak + 1 : 0;
     ctl->streak = streak;
     if (streak >= 2) ctl->done = 1;
+}
+
+/// Paired orders on shards: order - 1 ran deferred (|term_{k}|^2 in tot[3] + tot[7], c untouched), order caught up
+/// (|c_k|^2 in tot[2] + tot[6], then the sums of its own order).  One all-reduce served both orders.
+static __global__ void taylor_stop_pair_kernel(TaylorCtl* ctl, const double* __restrict__ tot, int order, double rtol) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (ctl->done || ctl->bail) return;
+    {
+        const double tn = __dsqrt_rn(__dadd_rn(tot[3], tot[7])), rn = __dsqrt_rn(__dadd_rn(tot[2], tot[6]));
+        ctl->streak = (tn <= __dmul_rn(rtol, rn)) ? ctl->streak + 1 : 0;  // the streak was 0: this cannot stop the series
+        ctl->deferred += 1;
+    }
+    const double tn = __dsqrt_rn(__dadd_rn(tot[0], tot[4])), rn = __dsqrt_rn(__dadd_rn(tot[1], tot[5]));
+    if (order > ctl->order_used) ctl->order_used = order;
+    ctl->last_order = order;
+    ctl->last_term_norm = tn;
+    ctl->last_c_norm = rn;
+    const int streak = (tn <= __dmul_rn(rtol, rn)) ? ctl->streak + 1 : 0;
+    ctl->streak = streak;
+    if (streak >= 2) ctl->done = 1;
+}
+
+/// flag[i] = 1 when row i has a halo column (col >= n): it has to wait for the halo exchange.
+static __global__ void __launch_bounds__(NT) row_has_halo_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                                 const int32_t* __restrict__ col,
+                                                                 uint32_t* __restrict__ flag) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i <= n; i += gridDim.x * NT) {
+        uint32_t f = 0;
+        if (i < n) {
+            const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+            for (uint32_t e = kb; e < ke; ++e) f |= (uint32_t(__ldg(col + e)) >= n) ? 1u : 0u;
+        }
+        flag[i] = f;
+    }
+}
+
+/// pos = exclusive scan of flag: row i goes to bnd[pos[i]] when flagged, else to intr[i - pos[i]].
+static __global__ void __launch_bounds__(NT) split_rows_kernel(uint32_t n, const uint32_t* __restrict__ flag,
+                                                               const uint32_t* __restrict__ pos,
+                                                               uint32_t* __restrict__ intr, uint32_t* __restrict__ bnd) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        if (flag[i])
+            bnd[pos[i]] = i;
+        else
+            intr[i - pos[i]] = i;
+    }
 }
 
 /// Marks the locally owned keys among the globally selected tie keys (truncate_select, engine.hpp:137-142).

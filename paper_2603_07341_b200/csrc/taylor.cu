@@ -606,6 +606,87 @@ static bool launch(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t
 
 static const bool g_use_tiles = std::getenv("PB200_TAYLOR_ROWS") == nullptr;
 
+// ================================================================================================
+// K4 on a shard: row-list form.  A Taylor order on a sharded space runs as TWO launches -- the rows without halo
+// columns while the halo exchange is in flight, then the rows with halo columns -- and its norms are global: every
+// launch only deposits its partial sums (tot_out[0..3] = |term|^2, |c|^2, |c + pending term|^2, deferred |term|^2);
+// the sums of the two launches are all-reduced together and taylor_stop_kernel / taylor_stop_pair_kernel apply the
+// stop rule identically on every rank.  Same row arithmetic as the kernels above.
+// ================================================================================================
+template <int MODE>  // tile::SINGLE, tile::DEFER, tile::CATCHUP
+__global__ void __launch_bounds__(NT) taylor_rows_kernel(uint32_t nrows, const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                         const double2* __restrict__ term_in,
+                                                         double2* __restrict__ term_out, double2* __restrict__ c, double b,
+                                                         int order, double* __restrict__ partials, TaylorCtl* ctl,
+                                                         double* __restrict__ tot_out) {
+    __shared__ double smem[NT / 32];
+    if (ld_flag(&ctl->done) | ld_flag(&ctl->bail)) return;
+    if (MODE == tile::DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
+        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
+        return;
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t t = blockIdx.x * NT + threadIdx.x; t < nrows; t += gridDim.x * NT) {
+        const uint32_t i = __ldg(rows + t);
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        double ar = 0.0, ai = 0.0;
+        for (uint32_t k = kb; k < ke; ++k) {
+            const double v = __ldg(val + k);
+            const double2 x = __ldg(term_in + __ldg(col + k));
+            ar = __dadd_rn(ar, __dmul_rn(v, x.x));
+            ai = __dadd_rn(ai, __dmul_rn(v, x.y));
+        }
+        const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
+        const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
+        term_out[i] = make_double2(tr, ti);
+        const double t2 = __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti));
+        if (MODE == tile::DEFER) {
+            acc[3] = __dadd_rn(acc[3], t2);
+            continue;
+        }
+        acc[0] = __dadd_rn(acc[0], t2);
+        double2 cc = c[i];
+        if (MODE == tile::CATCHUP) {
+            const double2 tp = __ldg(term_in + i);
+            cc.x = __dadd_rn(cc.x, tp.x);
+            cc.y = __dadd_rn(cc.y, tp.y);
+            acc[2] = __dadd_rn(acc[2], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+        }
+        cc.x = __dadd_rn(cc.x, tr);
+        cc.y = __dadd_rn(cc.y, ti);
+        c[i] = cc;
+        acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+    }
+    double tot[4];
+    if (grid_sum<4>(acc, partials, &ctl->ticket, tot, smem) && threadIdx.x == 0) {
+        if (MODE == tile::DEFER) {
+            tot_out[3] = tot[3];
+        } else {
+            tot_out[0] = tot[0];
+            tot_out[1] = tot[1];
+            if (MODE == tile::CATCHUP) tot_out[2] = tot[2];
+        }
+        __threadfence();
+    }
+}
+
+void taylor_launch_rows(int mode, int grid, cudaStream_t stream, uint32_t nrows, const uint32_t* rows,
+                        const uint32_t* row_ptr, const int32_t* col, const double* val, const double2* term_in,
+                        double2* term_out, double2* c, double b, int order, double* partials, TaylorCtl* ctl,
+                        double* tot_out) {
+    if (mode == tile::DEFER)
+        taylor_rows_kernel<tile::DEFER><<<grid, NT, 0, stream>>>(nrows, rows, row_ptr, col, val, term_in, term_out, c, b, order,
+                                                                partials, ctl, tot_out);
+    else if (mode == tile::CATCHUP)
+        taylor_rows_kernel<tile::CATCHUP><<<grid, NT, 0, stream>>>(nrows, rows, row_ptr, col, val, term_in, term_out, c, b,
+                                                                  order, partials, ctl, tot_out);
+    else
+        taylor_rows_kernel<tile::SINGLE><<<grid, NT, 0, stream>>>(nrows, rows, row_ptr, col, val, term_in, term_out, c, b,
+                                                                 order, partials, ctl, tot_out);
+}
+
 // ------------------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------------------

@@ -40,4 +40,12 @@ void taylor_launch_catchup(int grid, int sm_count, cudaStream_t stream, uint32_t
                            const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                            double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row);
 
+/// Sharded SpMV (taylor.cu, row-list form): mode 0 = SINGLE, 2 = DEFER, 3 = CATCHUP; the launch covers rows[0..nrows)
+/// and deposits its partial sums in tot_out[0..3].
+constexpr int TAYLOR_ROWS_SINGLE = 0, TAYLOR_ROWS_DEFER = 2, TAYLOR_ROWS_CATCHUP = 3;
+void taylor_launch_rows(int mode, int grid, cudaStream_t stream, uint32_t nrows, const uint32_t* rows,
+                        const uint32_t* row_ptr, const int32_t* col, const double* val, const double2* term_in,
+                        double2* term_out, double2* c, double b, int order, double* partials, TaylorCtl* ctl,
+                        double* tot_out);
+
 }  // namespace pb

@@ -1,10 +1,12 @@
-"""Collectives for the sharded (multi-GPU) path, supplied to libpaces_b200.so as C callbacks.
+"""Transports of the sharded (multi-GPU) path.
 
-The library never talks to NCCL itself (include/paces_b200.h, pb200_comm_ops): torch.distributed is the plumbing.
-One process per GPU; with the ``nccl`` backend the device collectives run on device memory over NVLink/NVSwitch,
-stream-ordered after the context's stream.  Any other backend (``gloo``) is staged through host memory, which is how
-the sharded path is tested with two ranks on a single GPU.  ``device=None`` treats the "device" pointers as host
-pointers (pure-CPU unit tests of the callback plumbing).
+``NcclComm``  the production transport: NCCL INSIDE libpaces_b200.so (pb200_ctx_set_comm_nccl).  This module only
+              moves the 256-byte unique id from rank 0 to the other ranks (torch.distributed broadcast, or any callable).
+``TorchComm`` the collectives as C callbacks (pb200_comm_ops) backed by torch.distributed: ``gloo`` stages them through
+              host memory, which is how the sharded path is tested with several ranks on ONE GPU (NCCL refuses two
+              ranks on a device); ``device=None`` treats the "device" pointers as host pointers (pure-CPU unit tests
+              of the callback plumbing).
+One process per GPU.
 """
 from __future__ import annotations
 
@@ -39,6 +41,7 @@ class CommOps(C.Structure):
         ("alltoallv_dev", CB_ALLTOALLV_DEV),
         ("allreduce_f64_dev", CB_ALLREDUCE_F64_DEV),
         ("allreduce_u32_dev", CB_ALLREDUCE_U32_DEV),
+        ("alltoallv_dev2", CB_ALLTOALLV_DEV),  # optional independent halo channel; NULL here
     ]
 
 
@@ -54,6 +57,39 @@ def _host_bytes(ptr, nbytes):
     if nbytes == 0:
         return np.zeros(0, np.uint8)
     return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(int(nbytes),))
+
+
+class NcclComm:
+    """NCCL inside the library.  rank/world default to the torch.distributed world (used only to broadcast the unique
+    id); pass ``bcast`` (a callable: bytes on rank 0 / None elsewhere -> bytes) for any other rendezvous."""
+
+    ID_BYTES = 256
+
+    def __init__(self, device: int, rank: int | None = None, world: int | None = None, bcast=None):
+        self.device = device
+        if rank is None:
+            rank, world = (dist.get_rank(), dist.get_world_size()) if dist.is_initialized() else (0, 1)
+        self.rank, self.world = int(rank), int(world)
+        self._bcast = bcast
+
+    def unique_id(self, lib) -> bytes:
+        buf = (C.c_uint8 * self.ID_BYTES)()
+        if self.rank == 0 and lib.pb200_nccl_unique_id(buf) != 0:
+            raise RuntimeError("pb200_nccl_unique_id failed: " + lib.pb200_last_error(None).decode())
+        raw = bytes(buf)
+        if self._bcast is not None:
+            return self._bcast(raw if self.rank == 0 else None)
+        if self.world > 1:
+            box = [raw if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            raw = box[0]
+        return raw
+
+    def attach(self, ctx):
+        """Called by Context.set_comm: creates the communicators (collective)."""
+        raw = self.unique_id(ctx.lib)
+        buf = (C.c_uint8 * self.ID_BYTES).from_buffer_copy(raw)
+        ctx._ck(ctx.lib.pb200_ctx_set_comm_nccl(ctx.h, self.rank, self.world, buf))
 
 
 class TorchComm:
@@ -76,7 +112,7 @@ class TorchComm:
             CB_ALLTOALLV_DEV(self._alltoallv_dev), CB_ALLREDUCE_F64_DEV(self._allreduce_f64_dev),
             CB_ALLREDUCE_U32_DEV(self._allreduce_u32_dev),
         ]
-        self.ops = CommOps(None, *self._cbs)
+        self.ops = CommOps(None, *self._cbs, CB_ALLTOALLV_DEV())
 
     # ---- helpers -------------------------------------------------------------------------------------------
     def _guard(self, fn):

@@ -1,6 +1,9 @@
-"""Worker of the sharded-path test: launched by torch.distributed.run with WORLD_SIZE ranks that all use cuda:0
-(gloo backend, exchanges staged through host memory), it runs the sharded trajectory and rank 0 compares the
-gathered global state with the CPU oracle step by step."""
+"""Worker of the sharded-path tests: launched by torch.distributed.run with WORLD_SIZE ranks, it runs the sharded
+trajectory and rank 0 compares the gathered global state with the CPU oracle step by step.
+  default          every rank uses cuda:0, exchanges through gloo callbacks staged in host memory (several ranks on
+                   ONE GPU, which NCCL refuses)
+  PB200_WORKER_TRANSPORT=nccl   rank r uses cuda:r and the library's own NCCL transport (needs WORLD_SIZE GPUs; with
+                   WORLD_SIZE=1 it is a one-rank communicator: every NCCL call of the path runs for real on one GPU)"""
 import json
 import os
 import sys
@@ -14,7 +17,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
 import paper_2603_07341_b200 as pb  # noqa: E402
-from paper_2603_07341_b200.dist import TorchComm, gather_state  # noqa: E402
+from paper_2603_07341_b200.dist import NcclComm, TorchComm, gather_state  # noqa: E402
 from cases import CASES  # noqa: E402
 
 
@@ -27,8 +30,10 @@ def main():
     max_steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(0)
-    comm = TorchComm(device=0)
+    use_nccl = os.environ.get("PB200_WORKER_TRANSPORT") == "nccl"
+    dev = int(os.environ.get("LOCAL_RANK", "0")) if use_nccl else 0
+    torch.cuda.set_device(dev)
+    comm = NcclComm(device=dev) if use_nccl else TorchComm(device=0)
     report = {}
     port = None
     if rank == 0:
@@ -37,7 +42,7 @@ def main():
         port = pyoracle.load_port()
     for name in names:
         case = CASES[name]
-        ctx = pb.Context(pb.ModelDef(**case["model"]), device=0, comm=comm)
+        ctx = pb.Context(pb.ModelDef(**case["model"]), device=dev, comm=comm)
         run = ctx.run(**case["run"])
         ro = None
         if rank == 0:
@@ -73,7 +78,8 @@ def main():
                 assert close(ob[k], oo[k], 1e-10, 1e-12), (name, k, ob[k], oo[k])
         allsizes = [None] * world
         dist.all_gather_object(allsizes, sizes[-1] if sizes else 0)
-        report[name] = dict(steps=len(sizes), shard_rows=allsizes, calls=dict(comm.calls))
+        report[name] = dict(steps=len(sizes), shard_rows=allsizes, transport=ctx.comm_describe(),
+                            calls=dict(getattr(comm, "calls", {})), deferred=run.times()["taylor_deferred"])
     if rank == 0:
         print("SHARDED_OK " + json.dumps(report), flush=True)
     dist.barrier()

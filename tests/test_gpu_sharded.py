@@ -11,10 +11,10 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _launch(world, names, steps, port):
+def _launch(world, names, steps, port, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}", "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "dist_worker.py"), names, str(steps)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ, **(env or {})))
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-6000:])
     assert "SHARDED_OK" in r.stdout, r.stdout[-3000:]
     return r.stdout
@@ -29,3 +29,40 @@ def test_two_ranks_match_oracle():
 def test_three_and_four_ranks_match_oracle():
     _launch(3, "ties_holstein_L5_d6,square_3x3_d5", 25, 29612)
     _launch(4, "cfg2_layout_L16_d16_small,substeps_L4_d4_m1,tb_chain_31", 20, 29613)
+
+
+@pytest.mark.gpu
+def test_eight_ranks_match_oracle():
+    """The full width of a B200 box: 8 shards (sharing one GPU here), bit for bit against the oracle, including the
+    exact-tie configuration and a 3D model; paired Taylor orders must really have run on the shards."""
+    import json
+
+    out = _launch(8, "ties_holstein_L5_d6,cube_2x2x2_d16,cfg2_layout_L16_d16_small", 16, 29614)
+    rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
+    assert all(len(v["shard_rows"]) == 8 for v in rep.values())
+    assert any(v["deferred"] > 0 for v in rep.values()), rep
+
+
+@pytest.mark.gpu
+def test_nccl_transport_one_rank_self_exchange():
+    """The library's own NCCL transport (pb200_ctx_set_comm_nccl) on ONE GPU: a one-rank communicator still runs the
+    sharded algorithms, so every ncclSend/ncclRecv group, all-reduce and all-gather of the path executes for real
+    (self-exchanges) and the trajectory must match the oracle bit for bit."""
+    import json
+
+    out = _launch(1, "cfg1_holstein_L4_d8,ties_holstein_L5_d6,cube_2x2x2_d16", 20, 29615,
+                  env={"PB200_WORKER_TRANSPORT": "nccl"})
+    rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
+    for v in rep.values():
+        assert v["transport"].startswith("NCCL "), v
+        assert "alltoallv 0," not in v["transport"] and "allreduce 0," not in v["transport"], v
+
+
+@pytest.mark.gpu
+def test_nccl_transport_two_gpus():
+    """Two processes, two GPUs, NCCL over NVLink inside the library; skipped where the box has one GPU."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (this pool's boxes have one)")
+    _launch(2, "cfg1_holstein_L4_d8,ties_holstein_L5_d6,cube_2x2x2_d16", 20, 29616, env={"PB200_WORKER_TRANSPORT": "nccl"})
