@@ -361,8 +361,15 @@ __host__ __device__ inline Layout make_layout(int max_row) {
     return L;
 }
 
+/// Resident CTAs per SM the kernels are compiled for -- and the grid every mode uses (SMs x this), so that SINGLE,
+/// DEFER, CATCHUP and FIRST share one reduction shape whatever their register appetite.
+template <int MAXR>
+constexpr int tile_ctas_per_sm() {
+    return MAXR <= 5 ? 4 : 3;
+}
+
 template <int MODE, int MAXR>
-__global__ void __launch_bounds__(NTHREADS, TILE_MINB) taylor_tile_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_tile_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                                const int32_t* __restrict__ col,
                                                                const double* __restrict__ val,
                                                                const double2* __restrict__ term_in,
@@ -563,22 +570,23 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
                      double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
                      double* expect_out) {
     const Layout L = make_layout(MAXR);
-    static int per_sm = 0;  // resident CTAs per SM for this instantiation
-    if (per_sm == 0) {
-        per_sm = -1;
+    static int ready = 0;  // 1: usable, -1: not (the launch falls back to the row kernels)
+    if (ready == 0) {
+        ready = -1;
         int occ = 0;
         if (cudaFuncSetAttribute(taylor_tile_kernel<MODE, MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(L.total)) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, taylor_tile_kernel<MODE, MAXR>, NTHREADS, L.total) ==
                 cudaSuccess &&
             occ >= 1)
-            per_sm = occ;
+            ready = 1;
         else
             cudaGetLastError();
     }
-    if (per_sm < 0) return false;
+    if (ready < 0) return false;
     const uint32_t ntiles = (n + TR - 1) / TR;
-    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(per_sm)));
+    const uint32_t grid =
+        std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
     taylor_tile_kernel<MODE, MAXR><<<grid, NTHREADS, L.total, stream>>>(n, row_ptr, col, val, term_in, term_out, c, b, order,
                                                                          rtol, MAXR, partials, ctl, ignore_stop, tot_out,
                                                                          expect_out);
