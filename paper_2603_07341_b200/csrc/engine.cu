@@ -1,5 +1,6 @@
 // engine.cu -- implementation of the device-resident paces step (see engine.cuh, kernels.cuh).
 #include <atomic>
+#include <chrono>
 #include "engine.cuh"
 
 #include <cmath>
@@ -117,14 +118,31 @@ void Engine::publish(const void* dptr, uint32_t nwords) {
     publish_kernel<<<1, 128, 0, stream>>>(static_cast<const uint32_t*>(dptr), base + 16, nwords, base, want);
     check_launch();
     volatile uint32_t* flag = static_cast<volatile uint32_t*>(mapped);
+    // A failed kernel never raises the flag: look at the stream now and then; a kernel that neither finishes nor
+    // fails (a wedged device) ends the wait after PB200_READBACK_TIMEOUT_S seconds (default 120) instead of spinning
+    // for ever.
+    static const double timeout_s = [] {
+        const char* e = std::getenv("PB200_READBACK_TIMEOUT_S");
+        const double v = e ? std::atof(e) : 120.0;
+        return v > 0 ? v : 120.0;
+    }();
+    std::chrono::steady_clock::time_point t0{};
+    bool timing = false;
     for (uint64_t spins = 1; *flag != want; ++spins) {
-        if ((spins & 0x3fff) == 0) {  // a failed kernel never raises the flag: look at the stream now and then
+        if ((spins & 0x3fff) == 0) {
             const cudaError_t q = cudaStreamQuery(stream);
             if (q == cudaSuccess) {
                 if (*flag == want) break;
                 throw CudaFail("internal error: read-back flag missing after the stream drained");
             }
             if (q != cudaErrorNotReady) PB_CUDA(q);
+            if (!timing) {
+                t0 = std::chrono::steady_clock::now();
+                timing = true;
+            } else if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+                throw CudaFail("read-back timed out after " + std::to_string(int(timeout_s)) +
+                               " s: a kernel on the context's stream neither finished nor failed");
+            }
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);

@@ -363,9 +363,12 @@ __host__ __device__ inline Layout make_layout(int max_row) {
 
 /// Resident CTAs per SM the kernels are compiled for -- and the grid every mode uses (SMs x this), so that SINGLE,
 /// DEFER, CATCHUP and FIRST share one reduction shape whatever their register appetite.
+#ifndef TILE_WIDE_CTAS
+#define TILE_WIDE_CTAS 3
+#endif
 template <int MAXR>
 constexpr int tile_ctas_per_sm() {
-    return MAXR <= 5 ? 4 : 3;
+    return MAXR <= 5 ? 4 : TILE_WIDE_CTAS;
 }
 
 template <int MODE, int MAXR>
