@@ -84,6 +84,7 @@ typedef struct pb200_phase_times {
     uint64_t rows_sum, nnz_sum;    /* sum over steps of q_true and nnz(H_eff) of the space the step evolved on */
     uint64_t rows_old_sum;         /* sum over steps of the rows of the state the step started from */
     uint64_t kept_sum;             /* sum over steps of the keys truncate_select kept */
+    uint64_t spmv_nnz_coded;       /* of spmv_nnz: non-zeros streamed as 2-byte value codes (6 instead of 12 bytes each) */
     /* assemble_ms, remap_ms and expectation_ms stay ~0 in the resident single-GPU step: assembly and remap are
      * part of the incremental adapt phase (inside grow_ms), <H> rides on the first Taylor order (inside expmv_ms) */
 } pb200_phase_times;

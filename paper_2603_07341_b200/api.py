@@ -82,7 +82,7 @@ class PhaseTimes(C.Structure):
         ("spmv_nnz", C.c_uint64), ("taylor_orders", C.c_uint64), ("kernel_launches", C.c_uint64),
         ("steps", C.c_uint64), ("taylor_deferred", C.c_uint64), ("taylor_rows", C.c_uint64),
         ("taylor_deferred_rows", C.c_uint64), ("rows_sum", C.c_uint64), ("nnz_sum", C.c_uint64),
-        ("rows_old_sum", C.c_uint64), ("kept_sum", C.c_uint64),
+        ("rows_old_sum", C.c_uint64), ("kept_sum", C.c_uint64), ("spmv_nnz_coded", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -266,6 +266,7 @@ int pb200_grow(pb200_ctx* ctx, const uint32_t* seeds, uint64_t rows, int order, 
         e.has_state = false;  // the resident state no longer matches the current space
         Space& sp = e.space[e.cur];
         sp.has_h = false;
+        sp.has_code = false;
         sp.has_full = false;
         e.grow(e.aux_words.as<uint32_t>(), uint32_t(rows), order, sp);
         e.sync();
@@ -556,6 +557,7 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
         sp.n = uint32_t(rows);
         sp.nnz = 0;
         sp.has_h = false;
+        sp.has_code = false;
         sp.has_full = false;
         // engine.hpp:110: the caller's table must be sorted -- checked on the device copy (one streaming kernel)
         if (!e.rows_sorted_on_device(sp.words.as<uint32_t>(), sp.n))
@@ -691,6 +693,7 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         sp.n = uint32_t(rows);
         sp.nnz = 0;
         sp.has_h = false;
+        sp.has_code = false;
         sp.has_full = false;
         e.t = t;
         e.steps_done = step_index - 1;
@@ -809,13 +812,15 @@ int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush, double dt, double*
         PB_CUDA(cudaMemcpyAsync(e.term[0].p, e.coeff[e.ccur].p, size_t(n) * 16, cudaMemcpyDeviceToDevice, e.stream));
         PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), e.stream));
         double total = 0;
+        TaylorCodes codes_tmp;
+        const TaylorCodes* cd = e.codes_of(sp, codes_tmp);
         for (int o = 1; o <= orders; ++o) {
             if (flush) flush_l2(e);
             PB_CUDA(cudaEventRecord(e.ev[8], e.stream));
             taylor_launch_single(false, e.grid_for(n), e.sm_count, e.stream, n, sp.row_ptr.as<uint32_t>(),
                                  sp.col.as<int32_t>(), sp.val.as<double>(), e.term[(o - 1) & 1].as<double2>(),
                                  e.term[o & 1].as<double2>(), e.aux_coeff.as<double2>(), -dt / double(o), o, 1e-15,
-                                 e.partials.as<double>(), &c->taylor, 1, nullptr, nullptr, sp.max_row);
+                                 e.partials.as<double>(), &c->taylor, 1, nullptr, nullptr, sp.max_row, cd);
             e.check_launch();
             PB_CUDA(cudaEventRecord(e.ev[9], e.stream));
             e.sync();

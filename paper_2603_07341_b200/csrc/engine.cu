@@ -254,7 +254,40 @@ void Engine::set_model(const HostModel& m) {
         md.diag_uniform = uniform ? 1 : 0;
         md.omega_u = w0;
     }
+    {
+        // value table: every matrix element for_each_neighbor() can emit -- bond amplitudes, g*sqrt(double(k)) (same
+        // IEEE operations as the device generator: correctly rounded sqrt, one multiply) and, for diag_uniform models,
+        // omega_u * double(N).  Anything it misses only costs the codes (encode raises `fail`), never a wrong value.
+        std::vector<double> vt;
+        for (double a : nba)
+            if (a != 0.0) vt.push_back(a);
+        if (m.kind == 1)
+            for (size_t s2 = 0; s2 < L; ++s2)
+                if (gg[s2] != 0.0)
+                    for (uint32_t k = 1; k < m.d_pho; ++k) vt.push_back(gg[s2] * std::sqrt(double(k)));
+        if (md.diag_uniform) {
+            const uint64_t top = uint64_t(L) * (m.d_pho > 0 ? m.d_pho - 1 : 0);
+            for (uint64_t N = 1; N <= top && vt.size() <= size_t(TAYLOR_VT_MAX) + 1; ++N) vt.push_back(md.omega_u * double(N));
+        }
+        auto bits = [](double v) {
+            uint64_t b;
+            std::memcpy(&b, &v, 8);
+            return b;
+        };
+        std::sort(vt.begin(), vt.end(), [&](double a, double b) { return bits(a) < bits(b); });
+        vt.erase(std::unique(vt.begin(), vt.end(), [&](double a, double b) { return bits(a) == bits(b); }), vt.end());
+        md.vtab = nullptr;
+        md.vt_n = 0;
+        md.vt_diag = md.diag_uniform;
+        if (!vt.empty() && vt.size() <= size_t(TAYLOR_VT_MAX)) {
+            d_vtab.ensure(vt.size() * 8);
+            PB_CUDA(cudaMemcpy(d_vtab.p, vt.data(), vt.size() * 8, cudaMemcpyHostToDevice));
+            md.vtab = d_vtab.as<double>();
+            md.vt_n = int(vt.size());
+        }
+    }
     row_width = max_deg + (m.kind == 1 ? 2 : 0) + 1;
+    space[0].has_code = space[1].has_code = false;
     has_model = true;
     has_state = false;
     has_cfg = false;
@@ -452,6 +485,26 @@ void Engine::assemble(Space& sp) {
     sp.nnz = nnz;
     sp.max_row = width;
     sp.has_h = true;
+    // value codes for the Taylor tile kernels (single GPU): one more pass over the finished CSR
+    sp.has_code = false;
+    if (!sharded) {
+        uint32_t* fail = &dctl()->code_fail;
+        if (encode_values_async(sp, n, defer_reads ? uint64_t(n) * width : nnz, nullptr, fail))
+            sp.has_code = read_back<uint32_t>(fail) == 0;
+    }
+}
+
+bool Engine::encode_values_async(Space& sp, uint64_t n_bound, uint64_t nnz_bound, const uint32_t* n_ptr, uint32_t* fail) {
+    if (!use_codes || md.vt_n <= 0 || sp.max_row < 1 || sp.max_row > 9) return false;
+    sp.code.ensure(size_t(nnz_bound) * 2 + CSR_PAD);
+    if (!md.vt_diag) sp.diag.ensure(size_t(n_bound) * 8 + CSR_PAD);
+    PB_CUDA(cudaMemsetAsync(fail, 0, 4, stream));
+    encode_csr_kernel<<<grid_for(n_bound), NT, 0, stream>>>(uint32_t(n_bound), n_ptr, sp.row_ptr.as<uint32_t>(),
+                                                             sp.col.as<int32_t>(), sp.val.as<double>(), md.vtab, md.vt_n,
+                                                             md.vt_diag, sp.code.as<uint16_t>(), sp.diag.as<double>(),
+                                                             fail);
+    check_launch();
+    return true;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -680,20 +733,22 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                 const int32_t* cl = sp.col.as<int32_t>();
                 const double* vl = sp.val.as<double>();
                 double* pt = partials.as<double>();
+                TaylorCodes codes_tmp;
+                const TaylorCodes* cd = codes_of(sp, codes_tmp);
                 if (fuse_expectation && s == 0 && order == 1) {
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
                     // (Ctl::out[1..3], read with the final read-back)
                     taylor_launch_single(true, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                         &c->taylor, 0, nullptr, c->out + 1, sp.max_row);
+                                         &c->taylor, 0, nullptr, c->out + 1, sp.max_row, cd);
                 } else if (!singles && order >= k0 && ((order - k0) & 1)) {
                     taylor_launch_catchup(g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                          &c->taylor, sp.max_row);
+                                          &c->taylor, sp.max_row, cd);
                 } else if (!singles && order >= k0 && order < max_order) {
                     taylor_launch_defer(g, sm_count, stream, n, rp, cl, vl, tin, tout, b, order, pt, &c->taylor,
-                                        sp.max_row);
+                                        sp.max_row, cd);
                 } else {
                     taylor_launch_single(false, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                         &c->taylor, 0, nullptr, nullptr, sp.max_row);
+                                         &c->taylor, 0, nullptr, nullptr, sp.max_row, cd);
                 }
                 check_launch();
             }
@@ -748,6 +803,7 @@ void Engine::upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int3
     sp.n = uint32_t(n);
     sp.nnz = uint64_t(nnz);
     sp.has_h = true;
+    sp.has_code = false;  // arbitrary values: the Taylor kernels read `val`
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -910,6 +966,7 @@ void Engine::run_step(pb200_diag* out) {
         PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[6]));
         times.total_ms += ms;
         times.spmv_nnz += uint64_t(order) * old.nnz;
+        if (old.has_code) times.spmv_nnz_coded += uint64_t(order) * old.nnz;
     } else {
         // engine.hpp:268-291
         Space& next = space[cur ^ 1];
@@ -1039,6 +1096,7 @@ void Engine::run_step(pb200_diag* out) {
         PB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[6]));
         times.total_ms += ms;
         times.spmv_nnz += uint64_t(order) * next.nnz;
+        if (next.has_code) times.spmv_nnz_coded += uint64_t(order) * next.nnz;
         times.rows_sum += next.n;
         times.nnz_sum += next.nnz;
         times.rows_old_sum += old.n;

@@ -115,6 +115,10 @@ struct Space {
     DevBuf row_ptr;  // uint32[n+1]
     DevBuf col;      // int32[nnz] ascending per row
     DevBuf val;      // double[nnz]
+    // value codes of a model-built H_eff (taylor.cuh, TaylorCodes; Engine::encode_values)
+    DevBuf code;     // uint16[nnz]
+    DevBuf diag;     // double[n], only when the model's diagonal elements are not tabulated
+    bool has_code = false;
     uint64_t nnz = 0;
     int max_row = 0;  // upper bound on the entries of a row (0 = unknown): selects the Taylor tile kernels
     uint64_t q_nom = 0;
@@ -144,7 +148,8 @@ struct Engine {
     bool has_model = false;
     HostModel hm;
     ModelDev md{};
-    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n, d_diag_masks;
+    DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n, d_diag_masks, d_vtab;
+    bool use_codes = std::getenv("PB200_NO_VALUE_CODES") == nullptr;
     int row_width = 1;  // max entries of an H_eff row for this model
 
     // resident trajectory
@@ -307,7 +312,8 @@ struct Engine {
         double out[8];  // reduction outputs: [0] remap (discarded weight), [1..3] expectation, [4..] scratch
         uint32_t nnz;   // row_ptr[n] of the last assembly (read with the step's final read-back)
         uint32_t n_new; // unique new keys of the last merge (read together with the expansion counters)
-        uint32_t pad2[2];
+        uint32_t code_fail;  // encode_csr_kernel met a value outside the model's table
+        uint32_t pad2[1];
     };
     /// Snapshot of the control block taken by the last read-back of expmv(): the step's deferred scalars
     /// (discarded weight, <H>, norm, nnz) ride along instead of costing a stream synchronisation each.
@@ -330,6 +336,18 @@ struct Engine {
     void dedup_candidates_async(uint32_t n, uint32_t nc_bound);
     uint32_t dedup_candidates(uint32_t n, uint32_t nc_bound);  // returns the number of unique new keys
     void assemble(Space& sp);
+    /// Enqueues the value-code pass over sp's CSR (n_ptr: row count on the device, or nullptr -> sp.n); a value outside
+    /// the model's table raises *fail.  The caller sets sp.has_code once it has seen the flag.
+    bool encode_values_async(Space& sp, uint64_t n_bound, uint64_t nnz_bound, const uint32_t* n_ptr, uint32_t* fail);
+    /// the codes of sp for the Taylor launchers, or nullptr
+    const TaylorCodes* codes_of(const Space& sp, TaylorCodes& tmp) const {
+        if (!sp.has_code) return nullptr;
+        tmp.code = sp.code.as<uint16_t>();
+        tmp.diag = md.vt_diag ? nullptr : sp.diag.as<double>();
+        tmp.vtab = md.vtab;
+        tmp.vt_n = md.vt_n;
+        return &tmp;
+    }
     /// returns kept count; result in this->seeds
     uint32_t select(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
                     double* norm2_out, bool compact = true);
@@ -341,7 +359,7 @@ struct Engine {
     bool grow_incremental(const Space& old, const double2* c_old, uint32_t kept, int m, Space& next, DevBuf& c_new);
     DevBuf inc_dist, inc_elist, inc_side_keys[2], inc_side_gap[2], inc_side_dist[2], inc_new_keys, inc_new_gap,
         inc_newidx, inc_inv, inc_side_newidx, inc_s_col, inc_s_val, inc_has_extra, inc_ctr, inc_simple, inc_buckets,
-        inc_tile_disc, inc_tile_jlo, inc_xlist, inc_x_slot, inc_x_ref, inc_x_val;
+        inc_tile_disc, inc_tile_jlo, inc_xlist, inc_x_slot, inc_x_ref, inc_x_val, inc_s_code, inc_x_code;
     uint64_t inc_steps = 0, inc_fallbacks = 0, inc_side_keys_total = 0, inc_expanded_total = 0;
     double remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
                  uint32_t nd, double2* dst_c);

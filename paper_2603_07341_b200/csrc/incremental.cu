@@ -143,11 +143,19 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     next.val.ensure(size_t(n_bound) * width * 8 + CSR_PAD);
     uint8_t* touched = inc_has_extra.as<uint8_t>();
     PB_CUDA(cudaMemsetAsync(touched, 0, size_t(n) + 1, stream));
+    // value codes (taylor.cuh) travel with the entries when the previous space has them
+    const bool carry_codes = use_codes && old.has_code && md.vt_n > 0;
+    if (carry_codes) {
+        inc_s_code.ensure(size_t(side_cap) * width * 2 + 4);
+        next.code.ensure(size_t(n_bound) * width * 2 + CSR_PAD);
+        if (!md.vt_diag) next.diag.ensure(size_t(n_bound) * 8 + CSR_PAD);
+    }
+    uint16_t* s_code = carry_codes ? inc_s_code.as<uint16_t>() : nullptr;
     const uint32_t* skeys = inc_side_keys[scur].as<uint32_t>();
     const uint32_t* sgap = inc_side_gap[scur].as<uint32_t>();
     PB_DISPATCH_WI(W, inc_side_search_kernel<W><<<small_grid, NT, 0, stream>>>(
                           md, old.words.as<uint32_t>(), n, m, levels, dist, skeys, width, inc_s_col.as<uint32_t>(),
-                          inc_s_val.as<double>(), touched, ictr));
+                          inc_s_val.as<double>(), s_code, touched, ictr));
     check_launch();
     // surviving old rows that gain entries: at most nmoves per side key; more than x_cap of them -> overflow
     const uint32_t x_cap = uint32_t(std::min<uint64_t>(uint64_t(n), uint64_t(side_cap) * 2));
@@ -156,13 +164,15 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     inc_x_slot.ensure(size_t(n) * 4 + 4);
     inc_x_ref.ensure(size_t(x_cap) * xs * 4 + 4);
     inc_x_val.ensure(size_t(x_cap) * xs * 8 + 8);
+    if (carry_codes) inc_x_code.ensure(size_t(x_cap) * xs * 2 + 4);
+    uint16_t* x_code = carry_codes ? inc_x_code.as<uint16_t>() : nullptr;
     inc_tile_prep_kernel<<<ctiles, NT, 0, stream>>>(n, m, levels, dist, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
                                                     sgap, tile_keep, tile_jlo, ctiles, touched, inc_xlist.as<uint32_t>(),
                                                     inc_x_slot.as<uint32_t>(), x_cap, ictr);
     check_launch();
     PB_DISPATCH_WI(W, inc_extras_kernel<W><<<small_grid, NT, 0, stream>>>(
                           md, old.words.as<uint32_t>(), levels, inc_xlist.as<uint32_t>(), x_cap, skeys, xs,
-                          inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), ictr));
+                          inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), x_code, ictr));
     check_launch();
     inc_tile_nnz_kernel<<<ctiles, NT, 0, stream>>>(n, m, dist, touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
                                                    inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs,
@@ -182,12 +192,22 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         n, levels, inc_newidx.as<uint32_t>(), touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
         old.val.as<double>(), inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), xs,
         inc_side_newidx.as<uint32_t>(), inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), width,
-        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>(), ictr);
+        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>(), ictr,
+        carry_codes ? old.code.as<uint16_t>() : nullptr, (carry_codes && !md.vt_diag) ? old.diag.as<double>() : nullptr,
+        x_code, s_code, next.code.as<uint16_t>(), next.diag.as<double>());
     check_launch();
+
+    // value codes of the new CSR (taylor.cuh): the row count is still on the device
+    next.max_row = width;
+    next.has_code = false;
+    // (the previous space had none -- e.g. its values were not all tabulated --: one pass over the finished CSR)
+    const bool coded = carry_codes || encode_values_async(next, n_bound, n_bound * uint64_t(width), &ictr->h.n_new,
+                                                          &ictr->h.code_fail);
 
     // ---- the one read-back of the phase
     const IncHead fin = read_back<IncHead>(&ictr->h);
     if (fin.overflow) return false;
+    next.has_code = coded && fin.code_fail == 0;
     if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     PB_CUDA(cudaMemcpyAsync(&c->nnz, &ictr->h.nnz_new, 4, cudaMemcpyDeviceToDevice, stream));
     inc_expanded_total += fin.expanded_total;

@@ -39,7 +39,9 @@ struct IncHead {
     uint32_t side_total;  // side keys after the last level
     uint32_t expanded_total;  // old rows expanded by key over all levels (statistics)
     uint32_t n_x;         // surviving old rows that gain entries (neighbours among the side keys)
-    uint32_t done_c, pad[2];
+    uint32_t done_c;
+    uint32_t code_fail;   // a matrix element outside the model's value table: the new space carries no value codes
+    uint32_t pad[1];
 };
 struct IncCounters {
     IncHead h;
@@ -234,8 +236,9 @@ static __global__ void __launch_bounds__(NT) inc_side_search_kernel(ModelDev m, 
                                                                     const uint32_t* __restrict__ side_keys, int width,
                                                                     uint32_t* __restrict__ s_ref,
                                                                     double* __restrict__ s_val,
+                                                                    uint16_t* __restrict__ s_code,
                                                                     uint8_t* __restrict__ touched,
-                                                                    const IncCounters* __restrict__ ctr) {
+                                                                    IncCounters* __restrict__ ctr) {
     const uint32_t side_n = ctr->side_n[levels];
     const uint64_t total = uint64_t(side_n) * uint32_t(width);
     for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
@@ -260,6 +263,14 @@ static __global__ void __launch_bounds__(NT) inc_side_search_kernel(ModelDev m, 
         });
         s_ref[t] = ref;
         s_val[t] = a;
+        if (s_code != nullptr && ref != IDX_NONE) {  // value code of the entry (taylor.cuh, TaylorCodes)
+            uint32_t cd = 0xffffu;                    // diagonal element kept per row
+            if (ref != (INV_SIDE | j) || m.vt_diag) {
+                cd = vt_find(m.vtab, m.vt_n, a);
+                if (cd == 0xfffeu) ctr->h.code_fail = 1u;
+            }
+            s_code[t] = uint16_t(cd);
+        }
     }
 }
 
@@ -319,7 +330,8 @@ static __global__ void __launch_bounds__(NT) inc_extras_kernel(ModelDev m, const
                                                                const uint32_t* __restrict__ xlist, uint32_t x_cap,
                                                                const uint32_t* __restrict__ side_keys, int nslots,
                                                                uint32_t* __restrict__ x_ref, double* __restrict__ x_val,
-                                                               const IncCounters* __restrict__ ctr) {
+                                                               uint16_t* __restrict__ x_code,
+                                                               IncCounters* __restrict__ ctr) {
     const uint32_t side_n = ctr->side_n[levels];
     const uint64_t total = uint64_t(min(ctr->h.n_x, x_cap)) * uint32_t(nslots);
     for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
@@ -339,6 +351,11 @@ static __global__ void __launch_bounds__(NT) inc_extras_kernel(ModelDev m, const
         });
         x_ref[t] = ref;
         x_val[t] = a;
+        if (x_code != nullptr && ref != IDX_NONE) {
+            const uint32_t cd = vt_find(m.vtab, m.vt_n, a);
+            if (cd == 0xfffeu) ctr->h.code_fail = 1u;
+            x_code[t] = uint16_t(cd);
+        }
     }
 }
 
@@ -580,8 +597,12 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
     const uint32_t* __restrict__ side_newidx,
     const uint32_t* __restrict__ s_ref, const double* __restrict__ s_val, int width,
     const uint32_t* __restrict__ row_ptr_new, const uint8_t* __restrict__ simple, int32_t* __restrict__ col_new,
-    double* __restrict__ val_new, const IncCounters* __restrict__ ctr) {
+    double* __restrict__ val_new, const IncCounters* __restrict__ ctr,
+    // value codes (taylor.cuh, TaylorCodes) travel with the entries: code_old == nullptr -> none
+    const uint16_t* __restrict__ code_old, const double* __restrict__ diag_old, const uint16_t* __restrict__ x_code,
+    const uint16_t* __restrict__ s_code, uint16_t* __restrict__ code_new, double* __restrict__ diag_new) {
     const uint32_t side_n = ctr->side_n[levels];
+    const bool coded = code_old != nullptr;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
     uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32;
@@ -605,6 +626,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
         }
         const bool kept = o != IDX_NONE;
         const bool smp = kept && simple[i];
+        if (coded && diag_old != nullptr && kept) diag_new[o] = __ldg(diag_old + i);
         const uint32_t d0 = kept ? row_ptr_new[o] : 0u;  // new offset of the row's first entry
         const unsigned smask = __ballot_sync(0xffffffffu, smp);
         const uint32_t rp0 = __shfl_sync(0xffffffffu, rp, 0);
@@ -631,11 +653,13 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                 }
                 int32_t cv[4];
                 double vv[4];
+                uint16_t cc[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (ok[u]) {
                         cv[u] = __ldg(col + eo[u]);
                         vv[u] = __ldg(val + eo[u]);
+                        if (coded) cc[u] = __ldg(code_old + eo[u]);
                     }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -645,6 +669,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                     if (ok[u]) {
                         col_new[dst[u]] = cv[u];
                         val_new[dst[u]] = vv[u];
+                        if (coded) code_new[dst[u]] = cc[u];
                     }
             }
         }
@@ -652,6 +677,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
         // extras of this row: its neighbours among the side keys, ascending
         uint32_t xc[MAX_ROW];
         double xv[MAX_ROW];
+        uint16_t xk[MAX_ROW];
         uint32_t nx = 0;
         if (touched[i] & 2) {
             const size_t xb = size_t(x_slot[i]) * nslots;
@@ -660,6 +686,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                 if (ref != IDX_NONE) {
                     xc[nx] = side_newidx[ref];
                     xv[nx] = x_val[xb + s2];
+                    if (coded) xk[nx] = x_code[xb + s2];
                     ++nx;
                 }
             }
@@ -673,19 +700,23 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
             while (xi < nx && xc[xi] < c) {
                 col_new[w] = int32_t(xc[xi]);
                 val_new[w] = xv[xi];
+                if (coded) code_new[w] = xk[xi];
                 ++w, ++xi;
             }
             col_new[w] = int32_t(c);
             val_new[w] = __ldg(val + e);
+            if (coded) code_new[w] = __ldg(code_old + e);
             ++w;
         }
         for (; xi < nx; ++xi, ++w) {
             col_new[w] = int32_t(xc[xi]);
             val_new[w] = xv[xi];
+            if (coded) code_new[w] = xk[xi];
         }
     }
     for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < side_n; j += gridDim.x * NT) {
-        uint32_t w = row_ptr_new[side_newidx[j]];
+        const uint32_t row = side_newidx[j];
+        uint32_t w = row_ptr_new[row];
         for (int s = 0; s < width; ++s) {
             const uint32_t ref = s_ref[size_t(j) * width + s];
             if (ref == IDX_NONE) continue;
@@ -693,6 +724,11 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
             if (c == IDX_NONE) continue;
             col_new[w] = int32_t(c);
             val_new[w] = s_val[size_t(j) * width + s];
+            if (coded) {
+                const uint16_t cd = s_code[size_t(j) * width + s];
+                code_new[w] = cd;
+                if (cd == uint16_t(0xffffu)) diag_new[row] = s_val[size_t(j) * width + s];
+            }
             ++w;
         }
     }

@@ -189,6 +189,38 @@ static __global__ void __launch_bounds__(NT) assemble_compact_kernel(uint32_t n,
 // ================================================================================================
 // K4  fused Taylor order: taylor.cuh / taylor.cu (own translation unit)
 // ================================================================================================
+/// Value codes of a model-built H_eff (taylor.cuh, TaylorCodes), one thread per row: code[k] = index of val[k] in the
+/// model's table of matrix elements; the diagonal entry of a row (col == row) whose values are not tabulated is coded
+/// 0xffff and its value copied to diag[row].  A value that is not in the table raises *fail: the space then keeps
+/// using `val`.  The row count is read from the device when n_ptr != nullptr (incremental adapt: the host does not
+/// know it yet).
+static __global__ void __launch_bounds__(NT) encode_csr_kernel(uint32_t n_host, const uint32_t* __restrict__ n_ptr,
+                                                               const uint32_t* __restrict__ row_ptr,
+                                                               const int32_t* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ vtab, int vt_n, int vt_diag,
+                                                               uint16_t* __restrict__ code, double* __restrict__ diag,
+                                                               uint32_t* __restrict__ fail) {
+    const uint32_t n = n_ptr ? *n_ptr : n_host;
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        for (uint32_t k = kb; k < ke; ++k) {
+            const double v = __ldg(val + k);
+            if (!vt_diag && uint32_t(__ldg(col + k)) == i) {
+                diag[i] = v;
+                code[k] = uint16_t(0xffffu);
+                continue;
+            }
+            uint32_t cd = vt_find(vtab, vt_n, v);
+            if (cd == 0xfffeu) {
+                *fail = 1u;
+                cd = 0;
+            }
+            code[k] = uint16_t(cd);
+        }
+    }
+}
+
 /// Plain y = H x (csr_matvec, subspace.hpp:35-43).
 static __global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                   const int32_t* __restrict__ col, const double* __restrict__ val,

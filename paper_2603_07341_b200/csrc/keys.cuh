@@ -40,7 +40,27 @@ struct ModelDev {
     double omega_u;              // the common omega
     const uint32_t* diag_masks;  // [bp * W] multi-word masks, bit plane b at diag_masks + b*W
     int wfirst[17];        // wfirst[w] = first phonon register whose leading bit lies in key word >= w (nph past the end)
+    // value codes (taylor.cuh, TaylorCodes): the distinct matrix elements the generator below can produce, ascending
+    // bit patterns; vt_n == 0: the model has too many (no codes).  vt_diag: the diagonal elements are tabulated too
+    // (diag_uniform models); otherwise a diagonal entry is coded CODE_DIAG and its value kept per row.
+    const double* vtab;
+    int vt_n;
+    int vt_diag;
 };
+
+/// Code of matrix element v: its index in the table, or 0xfffe (CODE_FAIL) when it is not there.
+__device__ __forceinline__ uint32_t vt_find(const double* __restrict__ vtab, int vt_n, double v) {
+    const unsigned long long key = (unsigned long long)__double_as_longlong(v);
+    int lo = 0, hi = vt_n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((unsigned long long)__double_as_longlong(__ldg(vtab + mid)) < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo < vt_n && (unsigned long long)__double_as_longlong(__ldg(vtab + lo)) == key) ? uint32_t(lo) : 0xfffeu;
+}
 
 template <int W>
 struct Key {

@@ -291,9 +291,16 @@ namespace tile {
 #ifndef TILE_EVICT_FIRST
 #define TILE_EVICT_FIRST 0
 #endif
+#ifndef TILE_STAGES_CODED
+#define TILE_STAGES_CODED 3
+#endif
 constexpr int TR = TILE_TR;        // rows per tile = consumer threads per CTA
-constexpr int STAGES = TILE_STAGES;
 constexpr int NTHREADS = TR + 32;  // + one producer warp
+/// Ring depth: a stage of the coded form is about half the size, so it affords one more.
+template <bool CODED>
+__host__ __device__ constexpr int stages() {
+    return CODED ? TILE_STAGES_CODED : TILE_STAGES;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -341,12 +348,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 enum Mode { SINGLE = 0, FIRST = 1, DEFER = 2, CATCHUP = 3 };
 
 struct Layout {  // byte offsets inside the dynamic shared memory of one CTA
-    uint32_t ecap;   // entries a stage holds (TR * max_row + 8)
-    uint32_t rp, col, val, stage_bytes, bars, total;
+    uint32_t ecap;   // entries a stage holds (TR * max_row + slack for the aligned start)
+    uint32_t rp, col, val, stage_bytes, bars, vt, total;
 };
-__host__ __device__ inline Layout make_layout(int max_row) {
+/// CODED: the stage holds a 2-byte value code per entry instead of the 8-byte value, and the model's table of
+/// distinct matrix elements (vt_n doubles) sits behind the reduction scratch.
+template <bool CODED>
+__host__ __device__ inline Layout make_layout(int max_row, int vt_n) {
     Layout L;
-    L.ecap = uint32_t(TR) * uint32_t(max_row) + 8;
+    L.ecap = uint32_t(TR) * uint32_t(max_row) + 16;
     uint32_t o = 0;
     L.rp = o;
     o += (TR + 4) * 4;
@@ -354,10 +364,11 @@ __host__ __device__ inline Layout make_layout(int max_row) {
     o += L.ecap * 4;
     o = (o + 15) & ~15u;
     L.val = o;
-    o += L.ecap * 8;
+    o += L.ecap * (CODED ? 2 : 8);
     L.stage_bytes = (o + 127) & ~127u;
-    L.bars = L.stage_bytes * STAGES;  // full[STAGES], empty[STAGES]
-    L.total = L.bars + 2 * STAGES * 8 + 128;  // + reduction scratch
+    L.bars = L.stage_bytes * stages<CODED>();  // full[STAGES], empty[STAGES]
+    L.vt = L.bars + 2 * stages<CODED>() * 8 + 128;  // + reduction scratch
+    L.total = L.vt + (CODED ? uint32_t(vt_n) * 8 : 0);
     return L;
 }
 
@@ -371,10 +382,13 @@ constexpr int tile_ctas_per_sm() {
     return MAXR <= 5 ? 4 : TILE_WIDE_CTAS;
 }
 
-template <int MODE, int MAXR>
+template <int MODE, int MAXR, bool CODED>
 __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_tile_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                                const int32_t* __restrict__ col,
                                                                const double* __restrict__ val,
+                                                               const uint16_t* __restrict__ code,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ vtab, int vt_n,
                                                                const double2* __restrict__ term_in,
                                                                double2* __restrict__ term_out, double2* __restrict__ c,
                                                                double b, int order, double rtol, int max_row,
@@ -389,7 +403,9 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
         return;
     }
-    const Layout L = make_layout(max_row);
+    constexpr int STAGES = stages<CODED>();
+    constexpr uint32_t AL = CODED ? 7u : 3u;  // the slices start at a 16-byte boundary of the narrowest array
+    const Layout L = make_layout<CODED>(max_row, vt_n);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + STAGES;
     double* red = reinterpret_cast<double*>(smem + L.bars + 2 * STAGES * 8);
@@ -401,6 +417,11 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
             mbar_init(empty + s, TR / 32);  // one arrive per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const double* vt_s = reinterpret_cast<const double*>(smem + L.vt);
+    if (CODED) {
+        double* vt_w = reinterpret_cast<double*>(smem + L.vt);
+        for (int q = int(tid); q < vt_n; q += NTHREADS) vt_w[q] = __ldg(vtab + q);
     }
     __syncthreads();
 
@@ -427,13 +448,16 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
             const uint32_t r0 = t * TR;
             const uint32_t rows = min(uint32_t(TR), n - r0);
             const uint32_t rp_bytes = ((rows + 1 + 3) & ~3u) * 4;
-            const uint32_t a0 = e0 & ~3u;
-            const uint32_t cnt = (e1 - a0 + 3) & ~3u;
-            mbar_expect_tx(full + s, rp_bytes + cnt * 12);
+            const uint32_t a0 = e0 & ~AL;
+            const uint32_t cnt = (e1 - a0 + AL) & ~AL;
+            mbar_expect_tx(full + s, rp_bytes + cnt * (CODED ? 6 : 12));
             bulk_load(st + L.rp, row_ptr + r0, rp_bytes, full + s);
             if (cnt) {
                 bulk_load(st + L.col, col + a0, cnt * 4, full + s);
-                bulk_load(st + L.val, val + a0, cnt * 8, full + s);
+                if (CODED)
+                    bulk_load(st + L.val, code + a0, cnt * 2, full + s);
+                else
+                    bulk_load(st + L.val, val + a0, cnt * 8, full + s);
             }
         }
         return;
@@ -450,16 +474,19 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         const uint32_t* rp_s = reinterpret_cast<const uint32_t*>(st + L.rp);
         const int32_t* col_s = reinterpret_cast<const int32_t*>(st + L.col);
         const double* val_s = reinterpret_cast<const double*>(st + L.val);
+        const uint16_t* code_s = reinterpret_cast<const uint16_t*>(st + L.val);
         const uint32_t i = t * TR + tid;
         const bool live = i < n;
         // independent of the ring: this row's slice of c and (catch-up / first order) of the previous term
         double2 cc = make_double2(0.0, 0.0), tp = make_double2(0.0, 0.0);
         if (HAS_C && live) cc = c[i];
         if ((MODE == CATCHUP || MODE == FIRST) && live) tp = __ldg(term_in + i);
+        double dg = 0.0;  // the row's diagonal element when the model's diagonals are not in the table
+        if (CODED && diag != nullptr && live) dg = __ldg(diag + i);
         mbar_wait(full + s, (j / STAGES) & 1);
         double ar = 0.0, ai = 0.0;
         if (live) {
-            const uint32_t base = rp_s[0] & ~3u;  // the slices start at the 16-byte boundary below the first entry
+            const uint32_t base = rp_s[0] & ~AL;  // the slices start at the 16-byte boundary below the first entry
             const uint32_t kb = rp_s[tid] - base;
             const uint32_t len = rp_s[tid + 1] - base - kb;
             double2 x[MAXR];
@@ -469,7 +496,13 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
 #pragma unroll
             for (int u = 0; u < MAXR; ++u)
                 if (uint32_t(u) < len) {
-                    const double v = val_s[kb + u];
+                    double v;
+                    if (CODED) {
+                        const uint32_t cd = code_s[kb + u];
+                        v = cd == CODE_DIAG ? dg : vt_s[cd];
+                    } else {
+                        v = val_s[kb + u];
+                    }
                     ar = __dadd_rn(ar, __dmul_rn(v, x[u].x));
                     ai = __dadd_rn(ai, __dmul_rn(v, x[u].y));
                 }
@@ -567,50 +600,66 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
     __threadfence();
 }
 
-template <int MODE, int MAXR>
+template <int MODE, int MAXR, bool CODED>
 static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
-                     const double* val, const double2* term_in, double2* term_out, double2* c, double b, int order,
-                     double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
+                     const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
+                     double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
                      double* expect_out) {
-    const Layout L = make_layout(MAXR);
-    static int ready = 0;  // 1: usable, -1: not (the launch falls back to the row kernels)
-    if (ready == 0) {
+    const int vt_n = CODED ? codes->vt_n : 0;
+    const Layout L = make_layout<CODED>(MAXR, vt_n);
+    static int ready = 0;     // 1: usable, -1: not (the launch falls back to the row kernels)
+    static uint32_t smem_set = 0;  // dynamic shared memory the kernel is currently allowed
+    if (ready == 0 || (ready > 0 && L.total > smem_set)) {
         ready = -1;
         int occ = 0;
-        if (cudaFuncSetAttribute(taylor_tile_kernel<MODE, MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(taylor_tile_kernel<MODE, MAXR, CODED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(L.total)) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, taylor_tile_kernel<MODE, MAXR>, NTHREADS, L.total) ==
-                cudaSuccess &&
-            occ >= 1)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, taylor_tile_kernel<MODE, MAXR, CODED>, NTHREADS,
+                                                          L.total) == cudaSuccess &&
+            occ >= 1) {
             ready = 1;
-        else
+            smem_set = L.total;
+        } else {
             cudaGetLastError();
+        }
     }
     if (ready < 0) return false;
     const uint32_t ntiles = (n + TR - 1) / TR;
     const uint32_t grid =
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
-    taylor_tile_kernel<MODE, MAXR><<<grid, NTHREADS, L.total, stream>>>(n, row_ptr, col, val, term_in, term_out, c, b, order,
-                                                                         rtol, MAXR, partials, ctl, ignore_stop, tot_out,
-                                                                         expect_out);
+    taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
+        n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
+        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out);
     return true;
+}
+
+template <int MODE, bool CODED>
+static bool launch_c(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
+                     const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
+                     double b, int order, double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop,
+                     double* tot_out, double* expect_out) {
+    // instantiations by row-length bound: 1D models (<= 5 entries), 2D (<= 7), 3D (<= 9)
+    if (max_row <= 5)
+        return launch_r<MODE, 5, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
+                                        partials, ctl, ignore_stop, tot_out, expect_out);
+    if (max_row <= 7)
+        return launch_r<MODE, 7, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
+                                        partials, ctl, ignore_stop, tot_out, expect_out);
+    return launch_r<MODE, 9, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
+                                    partials, ctl, ignore_stop, tot_out, expect_out);
 }
 
 template <int MODE>
 static bool launch(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
-                   const double* val, const double2* term_in, double2* term_out, double2* c, double b, int order,
-                   double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
-                   double* expect_out) {
-    // instantiations by row-length bound: 1D models (<= 5 entries), 2D (<= 7), 3D (<= 9)
+                   const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
+                   double b, int order, double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop,
+                   double* tot_out, double* expect_out) {
     if (max_row < 1 || max_row > 9) return false;
-    if (max_row <= 5)
-        return launch_r<MODE, 5>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
-                                 partials, ctl, ignore_stop, tot_out, expect_out);
-    if (max_row <= 7)
-        return launch_r<MODE, 7>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
-                                 partials, ctl, ignore_stop, tot_out, expect_out);
-    return launch_r<MODE, 9>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row, partials,
-                             ctl, ignore_stop, tot_out, expect_out);
+    if (codes != nullptr && codes->code != nullptr && codes->vt_n > 0 && codes->vt_n <= TAYLOR_VT_MAX)
+        return launch_c<MODE, true>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
+                                    max_row, partials, ctl, ignore_stop, tot_out, expect_out);
+    return launch_c<MODE, false>(sm_count, stream, n, row_ptr, col, val, nullptr, term_in, term_out, c, b, order, rtol,
+                                 max_row, partials, ctl, ignore_stop, tot_out, expect_out);
 }
 
 }  // namespace tile
@@ -711,13 +760,13 @@ static int resident_ctas(K kernel, int fallback) {
 void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
-                          double* tot_out, double* expect_out, int max_row) {
+                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes) {
     if (g_use_tiles && max_row > 0) {
-        const bool ok = expect ? tile::launch<tile::FIRST>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b,
-                                                           order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
+        const bool ok = expect ? tile::launch<tile::FIRST>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out,
+                                                           c, b, order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
                                                            expect_out)
-                               : tile::launch<tile::SINGLE>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b,
-                                                            order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
+                               : tile::launch<tile::SINGLE>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out,
+                                                            c, b, order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
                                                             expect_out);
         if (ok) return;
     }
@@ -734,20 +783,21 @@ void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stre
 
 void taylor_launch_defer(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                          const int32_t* col, const double* val, const double2* term_in, double2* term_out, double b,
-                         int order, double* partials, TaylorCtl* ctl, int max_row) {
+                         int order, double* partials, TaylorCtl* ctl, int max_row, const TaylorCodes* codes) {
     if (g_use_tiles && max_row > 0 &&
-        tile::launch<tile::DEFER>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, nullptr, b, order, 0.0, max_row,
-                                  partials, ctl, 0, nullptr, nullptr))
+        tile::launch<tile::DEFER>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, nullptr, b, order, 0.0,
+                                  max_row, partials, ctl, 0, nullptr, nullptr))
         return;
     taylor_defer_kernel<<<grid, NT, 0, stream>>>(n, row_ptr, col, val, term_in, term_out, b, order, partials, ctl);
 }
 
 void taylor_launch_catchup(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                            const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
-                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row) {
+                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row,
+                           const TaylorCodes* codes) {
     if (g_use_tiles && max_row > 0 &&
-        tile::launch<tile::CATCHUP>(sm_count, stream, n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, max_row,
-                                    partials, ctl, 0, nullptr, nullptr))
+        tile::launch<tile::CATCHUP>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
+                                    max_row, partials, ctl, 0, nullptr, nullptr))
         return;
     static const int per_sm = resident_ctas(taylor_catchup_kernel, 4);
     taylor_catchup_kernel<<<std::min(grid, sm_count * per_sm), NT, 0, stream>>>(n, row_ptr, col, val, term_in, term_out,

@@ -23,6 +23,21 @@ struct TaylorCtl {
     unsigned deferred;   // launches that ran deferred (statistics)
 };
 
+/// Value codes of a model-built H_eff (Engine::encode_values): the matrix holds only a few hundred distinct elements
+/// (bond amplitudes, g*sqrt(k), omega*N), so the tile kernels can stream a 2-byte code per entry instead of the 8-byte
+/// value -- 6 of the 12 bytes per non-zero -- and look the double up in a shared-memory copy of the table: the very
+/// same operand bits, hence the very same products and sums.  CODE_DIAG marks the diagonal entry of a row when the
+/// model's diagonal elements are not tabulated (disordered omega / eps): its value comes from diag[row].
+constexpr uint32_t CODE_DIAG = 0xffffu;
+constexpr uint32_t CODE_FAIL = 0xfffeu;  // encode: value not in the table (the space then keeps using `val`)
+constexpr int TAYLOR_VT_MAX = 2048;      // table entries the kernels copy into shared memory
+struct TaylorCodes {
+    const uint16_t* code;  // [nnz]
+    const double* diag;    // [n] or nullptr (diagonal elements are in the table)
+    const double* vtab;    // [vt_n] distinct matrix elements, ascending bit patterns
+    int vt_n;
+};
+
 /// max_row: upper bound on the entries of a row (0 = unknown).  With a bound <= 15 the launch uses the TMA tile kernels
 /// (taylor.cu, namespace tile); otherwise -- arbitrary uploaded CSR matrices -- the thread-per-row kernels.
 /// PB200_TAYLOR_ROWS=1 forces the row kernels (A/B measurements).
@@ -32,13 +47,14 @@ struct TaylorCtl {
 void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
-                          double* tot_out, double* expect_out, int max_row);
+                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes = nullptr);
 void taylor_launch_defer(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                          const int32_t* col, const double* val, const double2* term_in, double2* term_out, double b,
-                         int order, double* partials, TaylorCtl* ctl, int max_row);
+                         int order, double* partials, TaylorCtl* ctl, int max_row, const TaylorCodes* codes = nullptr);
 void taylor_launch_catchup(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                            const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
-                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row);
+                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int max_row,
+                           const TaylorCodes* codes = nullptr);
 
 /// Sharded SpMV (taylor.cu, row-list form): mode 0 = SINGLE, 2 = DEFER, 3 = CATCHUP; the launch covers rows[0..nrows)
 /// and deposits its partial sums in tot_out[0..3].

@@ -411,6 +411,53 @@ def test_incremental_adapt_equals_full_expansion(gpu, monkeypatch, name, model, 
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name,model,run_kw,steps,coded", [
+    ("1d_L16_uniform", dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+     dict(init="localized", site=-1, m_init=8, m=2, q_nom=30000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 20, True),
+    ("2d_4x3_disordered", dict(kind=1, extents=(4, 3), eps=tuple(0.05 * i - 0.2 for i in range(12)), hop=(0.55,),
+                              omega=tuple(1.0 + 0.01 * i for i in range(12)), g=(0.71,), d_pho=7),
+     dict(init="optical", m_init=4, m=2, q_nom=3000, dt=0.05, rtol=1e-15, t_max=5.0, seed=3), 16, True),
+    ("3d_4x4x4", dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+     dict(init="localized", site=-1, m_init=5, m=1, q_nom=8000, dt=0.05, rtol=1e-15, t_max=5.0, seed=7), 12, True),
+    ("tb_chain", dict(kind=0, extents=(61,), eps=tuple(0.01 * i for i in range(61)), hop=(1.0,)),
+     dict(init="localized", site=-1, m_init=3, m=2, q_nom=9, dt=0.05, rtol=1e-15, t_max=5.0, seed=1), 12, True),
+    # 90 sites x 31 levels of a disordered coupling: more distinct matrix elements than the table holds -> no codes
+    ("1d_L90_disordered_g", dict(kind=1, extents=(90,), eps=(0.0,), hop=(1.0,), omega=(1.0,),
+                                g=tuple(0.5 + 0.001 * i for i in range(90)), d_pho=32),
+     dict(init="localized", site=-1, m_init=3, m=1, q_nom=500, dt=0.05, rtol=1e-15, t_max=5.0, seed=2), 6, False),
+])
+def test_value_codes_equal_double_values(gpu, port, monkeypatch, name, model, run_kw, steps, coded):
+    """Taylor tile kernels reading 2-byte value codes + the model's table of matrix elements (taylor.cuh, TaylorCodes;
+    the codes travel with the entries through the incremental adapt phase) against the same kernels reading the 8-byte
+    values (PB200_NO_VALUE_CODES=1) and against the oracle: coefficients bit-identical at every step.  Uniform models
+    (diagonal tabulated), disordered omega / eps (diagonal kept per row), tight binding, and a model whose table
+    would be too large (falls back to the values by itself)."""
+    from oracle import pyoracle
+
+    monkeypatch.delenv("PB200_NO_VALUE_CODES", raising=False)
+    rc = _ctx(gpu, model).run(**run_kw)
+    monkeypatch.setenv("PB200_NO_VALUE_CODES", "1")
+    rv = _ctx(gpu, model).run(**run_kw)
+    monkeypatch.delenv("PB200_NO_VALUE_CODES", raising=False)
+    ro = port.model(pyoracle.ModelDef(**model)).run(**run_kw)
+    for s in range(1, steps + 1):
+        dc, dv, do = rc.step(), rv.step(), ro.step()
+        assert dc["q_true"] == dv["q_true"] == do["q_true"], (name, s)
+        assert dc["taylor_order"] == dv["taylor_order"] == do["taylor_order"], (name, s)
+        (wc, cc), (wv, cv), (wo, co) = rc.state(), rv.state(), ro.state()
+        assert np.array_equal(wc, wv) and np.array_equal(wc, wo), (name, s)
+        assert cc.tobytes() == cv.tobytes() == co.tobytes(), (name, s)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(rc.csr(), ro.csr())), name
+    tc, tv = rc.times(), rv.times()
+    assert tv["spmv_nnz_coded"] == 0
+    if coded:
+        assert tc["spmv_nnz_coded"] == tc["spmv_nnz"] > 0, (name, tc)
+        assert rc.adapt_stats()["incremental_steps"] >= steps // 2
+    else:
+        assert tc["spmv_nnz_coded"] == 0, (name, tc)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("rtol,substeps,max_order", [(1e-15, 1, 200), (1e-6, 1, 200), (1e-3, 2, 200), (0.5, 1, 200),
                                                      (1e-15, 3, 200), (1e-15, 1, 9)])
 def test_paired_taylor_orders_equal_single_orders(gpu, port, monkeypatch, rtol, substeps, max_order):
