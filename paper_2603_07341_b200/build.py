@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     r = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-ldl"],
                        cwd=CSRC, capture_output=True, text=True)
     for obj in objs:
-        if os.path.exists(obj):
+        if os.path.exists(obj) and not os.environ.get("PB200_KEEP_OBJS"):  # tools/build_variants.sh relinks them
             os.remove(obj)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -64,7 +64,10 @@ void download_csr(Engine& e, const Space& sp, int64_t* row_ptr, int32_t* col, do
         for (size_t i = 0; i < rp.size(); ++i) row_ptr[i] = int64_t(rp[i]);
     }
     if (col && sp.nnz) PB_CUDA(cudaMemcpyAsync(col, sp.col.p, sp.nnz * 4, cudaMemcpyDeviceToHost, e.stream));
-    if (val && sp.nnz) PB_CUDA(cudaMemcpyAsync(val, sp.val.p, sp.nnz * 8, cudaMemcpyDeviceToHost, e.stream));
+    if (val && sp.nnz) {
+        e.ensure_val(sp);
+        PB_CUDA(cudaMemcpyAsync(val, sp.val.p, sp.nnz * 8, cudaMemcpyDeviceToHost, e.stream));
+    }
     e.sync();
 }
 }  // namespace
@@ -267,6 +270,7 @@ int pb200_grow(pb200_ctx* ctx, const uint32_t* seeds, uint64_t rows, int order, 
         Space& sp = e.space[e.cur];
         sp.has_h = false;
         sp.has_code = false;
+        sp.val_valid = true;
         sp.has_full = false;
         e.grow(e.aux_words.as<uint32_t>(), uint32_t(rows), order, sp);
         e.sync();
@@ -558,6 +562,7 @@ int pb200_step(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index, co
         sp.nnz = 0;
         sp.has_h = false;
         sp.has_code = false;
+        sp.val_valid = true;
         sp.has_full = false;
         // engine.hpp:110: the caller's table must be sorted -- checked on the device copy (one streaming kernel)
         if (!e.rows_sorted_on_device(sp.words.as<uint32_t>(), sp.n))
@@ -694,6 +699,7 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
         sp.nnz = 0;
         sp.has_h = false;
         sp.has_code = false;
+        sp.val_valid = true;
         sp.has_full = false;
         e.t = t;
         e.steps_done = step_index - 1;

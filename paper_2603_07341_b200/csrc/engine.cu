@@ -485,6 +485,7 @@ void Engine::assemble(Space& sp) {
     sp.nnz = nnz;
     sp.max_row = width;
     sp.has_h = true;
+    sp.val_valid = true;
     // value codes for the Taylor tile kernels (single GPU): one more pass over the finished CSR
     sp.has_code = false;
     if (!sharded) {
@@ -492,6 +493,18 @@ void Engine::assemble(Space& sp) {
         if (encode_values_async(sp, n, defer_reads ? uint64_t(n) * width : nnz, nullptr, fail))
             sp.has_code = read_back<uint32_t>(fail) == 0;
     }
+}
+
+void Engine::ensure_val(const Space& csp) {
+    if (csp.val_valid) return;
+    Space& sp = const_cast<Space&>(csp);
+    if (!sp.has_code) throw CudaFail("internal error: H_eff has neither values nor value codes");
+    const uint64_t zb = sp.nnz ? sp.nnz : uint64_t(sp.n) * uint64_t(std::max(sp.max_row, 1));
+    sp.val.ensure(size_t(zb) * 8 + CSR_PAD);
+    decode_csr_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.code.as<uint16_t>(),
+                                                        sp.diag.as<double>(), md.vtab, sp.val.as<double>());
+    check_launch();
+    sp.val_valid = true;
 }
 
 bool Engine::encode_values_async(Space& sp, uint64_t n_bound, uint64_t nnz_bound, const uint32_t* n_ptr, uint32_t* fail) {
@@ -656,6 +669,7 @@ double Engine::remap(const uint32_t* src_words, const double2* src_c, uint32_t n
 // ------------------------------------------------------------------------------------------------
 void Engine::expectation_async(const Space& sp, const double2* x) {
     Ctl* c = dctl();
+    ensure_val(sp);
     expectation_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                           sp.val.as<double>(), x, partials.as<double>(), &c->ticket,
                                                           c->out + 1);
@@ -683,6 +697,7 @@ void Engine::expectation(const Space& sp, const double2* x, double* exp_out, dou
 }
 
 void Engine::spmv(const Space& sp, const double2* x, double2* y) {
+    ensure_val(sp);
     spmv_kernel<<<grid_for(sp.n), NT, 0, stream>>>(sp.n, sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
                                                    sp.val.as<double>(), x, y);
     check_launch();
@@ -804,6 +819,7 @@ void Engine::upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int3
     sp.nnz = uint64_t(nnz);
     sp.has_h = true;
     sp.has_code = false;  // arbitrary values: the Taylor kernels read `val`
+    sp.val_valid = true;
 }
 
 // ------------------------------------------------------------------------------------------------

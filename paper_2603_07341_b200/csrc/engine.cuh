@@ -119,6 +119,9 @@ struct Space {
     DevBuf code;     // uint16[nnz]
     DevBuf diag;     // double[n], only when the model's diagonal elements are not tabulated
     bool has_code = false;
+    // false: `val` was left behind by an incremental adapt step that carried the codes only (the Taylor tile kernels
+    // do not read it); Engine::ensure_val() rebuilds it from the codes for whoever asks.  !val_valid implies has_code.
+    bool val_valid = true;
     uint64_t nnz = 0;
     int max_row = 0;  // upper bound on the entries of a row (0 = unknown): selects the Taylor tile kernels
     uint64_t q_nom = 0;
@@ -149,7 +152,10 @@ struct Engine {
     HostModel hm;
     ModelDev md{};
     DevBuf d_eps, d_omega, d_g, d_nbs, d_nba, d_omega_n, d_diag_masks, d_vtab;
-    bool use_codes = std::getenv("PB200_NO_VALUE_CODES") == nullptr;
+    bool use_codes = std::getenv("PB200_NO_VALUE_CODES") == nullptr && std::getenv("PB200_TAYLOR_ROWS") == nullptr;
+    bool drop_val = std::getenv("PB200_KEEP_VALUES") == nullptr;  // coded spaces carry no 8-byte values between steps
+    /// Makes sp.val current (decodes it from the value codes when an incremental step left it behind).
+    void ensure_val(const Space& sp);
     int row_width = 1;  // max entries of an H_eff row for this model
 
     // resident trajectory

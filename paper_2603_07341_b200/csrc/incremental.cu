@@ -140,7 +140,6 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     inc_tile_disc.ensure(size_t(ctiles) * 8 + 8);
     next.row_ptr.ensure((size_t(n_bound) + 1) * 4 + CSR_PAD);
     next.col.ensure(size_t(n_bound) * width * 4 + CSR_PAD);
-    next.val.ensure(size_t(n_bound) * width * 8 + CSR_PAD);
     uint8_t* touched = inc_has_extra.as<uint8_t>();
     PB_CUDA(cudaMemsetAsync(touched, 0, size_t(n) + 1, stream));
     // value codes (taylor.cuh) travel with the entries when the previous space has them
@@ -151,6 +150,12 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
         if (!md.vt_diag) next.diag.ensure(size_t(n_bound) * 8 + CSR_PAD);
     }
     uint16_t* s_code = carry_codes ? inc_s_code.as<uint16_t>() : nullptr;
+    // a coded space leaves the 8-byte values behind: the Taylor tile kernels read the codes (ensure_val() decodes)
+    const bool with_val = !(carry_codes && drop_val);
+    if (with_val) {
+        ensure_val(old);
+        next.val.ensure(size_t(n_bound) * width * 8 + CSR_PAD);
+    }
     const uint32_t* skeys = inc_side_keys[scur].as<uint32_t>();
     const uint32_t* sgap = inc_side_gap[scur].as<uint32_t>();
     PB_DISPATCH_WI(W, inc_side_search_kernel<W><<<small_grid, NT, 0, stream>>>(
@@ -190,11 +195,13 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     check_launch();
     inc_fill_kernel<<<grid_for(n), NT, 0, stream>>>(
         n, levels, inc_newidx.as<uint32_t>(), touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
-        old.val.as<double>(), inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), inc_x_val.as<double>(), xs,
+        with_val ? old.val.as<double>() : nullptr, inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(),
+        inc_x_val.as<double>(), xs,
         inc_side_newidx.as<uint32_t>(), inc_s_col.as<uint32_t>(), inc_s_val.as<double>(), width,
-        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(), next.val.as<double>(), ictr,
-        carry_codes ? old.code.as<uint16_t>() : nullptr, (carry_codes && !md.vt_diag) ? old.diag.as<double>() : nullptr,
-        x_code, s_code, next.code.as<uint16_t>(), next.diag.as<double>());
+        next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), next.col.as<int32_t>(),
+        with_val ? next.val.as<double>() : nullptr, ictr, carry_codes ? old.code.as<uint16_t>() : nullptr,
+        (carry_codes && !md.vt_diag) ? old.diag.as<double>() : nullptr, x_code, s_code, next.code.as<uint16_t>(),
+        next.diag.as<double>());
     check_launch();
 
     // value codes of the new CSR (taylor.cuh): the row count is still on the device
@@ -207,7 +214,9 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     // ---- the one read-back of the phase
     const IncHead fin = read_back<IncHead>(&ictr->h);
     if (fin.overflow) return false;
+    if (!with_val && fin.code_fail) return false;  // a value outside the table and no values carried: full path
     next.has_code = coded && fin.code_fail == 0;
+    next.val_valid = with_val;
     if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     PB_CUDA(cudaMemcpyAsync(&c->nnz, &ictr->h.nnz_new, 4, cudaMemcpyDeviceToDevice, stream));
     inc_expanded_total += fin.expanded_total;

@@ -603,6 +603,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
     const uint16_t* __restrict__ s_code, uint16_t* __restrict__ code_new, double* __restrict__ diag_new) {
     const uint32_t side_n = ctr->side_n[levels];
     const bool coded = code_old != nullptr;
+    const bool with_val = val_new != nullptr;  // a coded space may leave the 8-byte values behind (Space::val_valid)
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
     uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32;
@@ -658,7 +659,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                 for (int u = 0; u < 4; ++u)
                     if (ok[u]) {
                         cv[u] = __ldg(col + eo[u]);
-                        vv[u] = __ldg(val + eo[u]);
+                        if (with_val) vv[u] = __ldg(val + eo[u]);
                         if (coded) cc[u] = __ldg(code_old + eo[u]);
                     }
 #pragma unroll
@@ -668,7 +669,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                 for (int u = 0; u < 4; ++u)
                     if (ok[u]) {
                         col_new[dst[u]] = cv[u];
-                        val_new[dst[u]] = vv[u];
+                        if (with_val) val_new[dst[u]] = vv[u];
                         if (coded) code_new[dst[u]] = cc[u];
                     }
             }
@@ -699,18 +700,18 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
             if (c == IDX_NONE) continue;
             while (xi < nx && xc[xi] < c) {
                 col_new[w] = int32_t(xc[xi]);
-                val_new[w] = xv[xi];
+                if (with_val) val_new[w] = xv[xi];
                 if (coded) code_new[w] = xk[xi];
                 ++w, ++xi;
             }
             col_new[w] = int32_t(c);
-            val_new[w] = __ldg(val + e);
+            if (with_val) val_new[w] = __ldg(val + e);
             if (coded) code_new[w] = __ldg(code_old + e);
             ++w;
         }
         for (; xi < nx; ++xi, ++w) {
             col_new[w] = int32_t(xc[xi]);
-            val_new[w] = xv[xi];
+            if (with_val) val_new[w] = xv[xi];
             if (coded) code_new[w] = xk[xi];
         }
     }
@@ -723,7 +724,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
             const uint32_t c = (ref & INV_SIDE) ? side_newidx[ref & ~INV_SIDE] : newidx[ref];
             if (c == IDX_NONE) continue;
             col_new[w] = int32_t(c);
-            val_new[w] = s_val[size_t(j) * width + s];
+            if (with_val) val_new[w] = s_val[size_t(j) * width + s];
             if (coded) {
                 const uint16_t cd = s_code[size_t(j) * width + s];
                 code_new[w] = cd;

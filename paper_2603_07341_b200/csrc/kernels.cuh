@@ -221,6 +221,22 @@ static __global__ void __launch_bounds__(NT) encode_csr_kernel(uint32_t n_host, 
     }
 }
 
+/// The 8-byte values of a coded H_eff, for whoever still wants them (CSR export, <H>, the row kernels): val[k] = the
+/// table entry of code[k], or the row's diag for 0xffff.
+static __global__ void __launch_bounds__(NT) decode_csr_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
+                                                               const uint16_t* __restrict__ code,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ vtab,
+                                                               double* __restrict__ val) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const uint32_t kb = __ldg(row_ptr + i), ke = __ldg(row_ptr + i + 1);
+        for (uint32_t k = kb; k < ke; ++k) {
+            const uint32_t cd = __ldg(code + k);
+            val[k] = cd == 0xffffu ? __ldg(diag + i) : __ldg(vtab + cd);
+        }
+    }
+}
+
 /// Plain y = H x (csr_matvec, subspace.hpp:35-43).
 static __global__ void __launch_bounds__(NT) spmv_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                   const int32_t* __restrict__ col, const double* __restrict__ val,

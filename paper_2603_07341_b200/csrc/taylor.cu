@@ -377,9 +377,12 @@ __host__ __device__ inline Layout make_layout(int max_row, int vt_n) {
 #ifndef TILE_WIDE_CTAS
 #define TILE_WIDE_CTAS 3
 #endif
+#ifndef TILE_NARROW_CTAS
+#define TILE_NARROW_CTAS 4
+#endif
 template <int MAXR>
 constexpr int tile_ctas_per_sm() {
-    return MAXR <= 5 ? 4 : TILE_WIDE_CTAS;
+    return MAXR <= 5 ? TILE_NARROW_CTAS : TILE_WIDE_CTAS;
 }
 
 template <int MODE, int MAXR, bool CODED>

@@ -2,6 +2,7 @@
 import csv, subprocess, sys
 rep, pat = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+sub = sys.argv[4] if len(sys.argv) > 4 else ""  # pick the first launch whose full name contains this
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + pat],
                      capture_output=True, text=True).stdout.splitlines()
 # several launches may match: take the first block
@@ -9,7 +10,8 @@ blocks, cur = [], None
 for ln in out:
     if ln.startswith('"Kernel Name"'):
         cur = []
-        blocks.append(cur)
+        if sub in ln:
+            blocks.append(cur)
     elif cur is not None:
         cur.append(ln)
 rows = list(csv.reader(blocks[0]))
