@@ -707,7 +707,8 @@ void Engine::spmv(const Space& sp, const double2* x, double2* y) {
 // expmv (propagator.hpp:52-92)
 // ------------------------------------------------------------------------------------------------
 void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
-                   int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_expectation) {
+                   int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_expectation,
+                   bool state_in_term0) {
     if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
     if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
     if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
@@ -720,8 +721,14 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
     const int g = grid_for(n);
     TaylorCtl tc{};
     PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
+    // state_in_term0 (resident step after an incremental adapt phase, which remaps the coefficients straight into
+    // term[0]): the first order takes the state from there and only writes c_vec -- no copy, no read of c_vec
+    const bool from_x = state_in_term0 && fuse_expectation;
+    if (state_in_term0 && !from_x)
+        PB_CUDA(cudaMemcpyAsync(c_vec, term[0].p, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
     for (int s = 0; s < substeps; ++s) {
-        PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
+        if (!(from_x && s == 0))
+            PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
         if (s > 0) {
             // new substep: streak and done restart, order_used keeps its running maximum
             tc.done = 0;
@@ -754,7 +761,7 @@ void Engine::expmv(const Space& sp, double2* c_vec, double dt, double rtol, int 
                     // the first order's row sums are H x: <x|H|x>, |x|^2 and the finiteness check ride along
                     // (Ctl::out[1..3], read with the final read-back)
                     taylor_launch_single(true, g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
-                                         &c->taylor, 0, nullptr, c->out + 1, sp.max_row, cd);
+                                         &c->taylor, 0, nullptr, c->out + 1, sp.max_row, cd, from_x ? 1 : 0);
                 } else if (!singles && order >= k0 && ((order - k0) & 1)) {
                     taylor_launch_catchup(g, sm_count, stream, n, rp, cl, vl, tin, tout, c_vec, b, order, rtol, pt,
                                           &c->taylor, sp.max_row, cd);
@@ -1006,7 +1013,8 @@ void Engine::run_step(pb200_diag* out) {
                                            !incremental);
         rec.norm_pre = std::sqrt(n2_pre);
         PB_CUDA(cudaEventRecord(ev[1], stream));
-        if (incremental && !grow_incremental(old, c_old, kept, cfg.m, next, coeff[ccur ^ 1])) {
+        // (the incremental path remaps the coefficients straight into term[0], the first Taylor order's input)
+        if (incremental && !grow_incremental(old, c_old, kept, cfg.m, next, term[0])) {
             incremental = false;
             ++inc_fallbacks;
             // the kept rows are still the rows at distance 0: turn them into the keep flags of the full path
@@ -1060,7 +1068,7 @@ void Engine::run_step(pb200_diag* out) {
             expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
         } else {
             try {
-                expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, true);
+                expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, true, incremental);
             } catch (const PacesError&) {
                 // the reference checks its input before it iterates (propagator.hpp:55-57)
                 if (last_ctl.out[3] != 0.0) throw PacesError("expmv: non-finite input coefficient");

@@ -377,8 +377,9 @@ struct Engine {
     /// out: <x|H|x>, |x|^2; throws on non-finite input when check_finite
     void expectation(const Space& sp, const double2* x, double* exp_out, double* norm2_out, bool check_finite);
     /// fuse_expectation: the first order also writes <x|H|x>, |x|^2, #non-finite of the INPUT vector to Ctl::out[1..3]
+    /// state_in_term0: the input state is in term[0] (not in c, which is then output only)
     void expmv(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps, int* order_used,
-               double* last_term_norm, double* last_c_norm, bool fuse_expectation = false);
+               double* last_term_norm, double* last_c_norm, bool fuse_expectation = false, bool state_in_term0 = false);
     void spmv(const Space& sp, const double2* x, double2* y);
     void upload_csr(Space& sp, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val);
     void observe(const uint32_t* words, const double2* c, uint32_t n, double* density, double* amp, double* phonons);

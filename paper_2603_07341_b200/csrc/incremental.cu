@@ -137,7 +137,6 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     uint32_t* tile_jlo = inc_tile_jlo.as<uint32_t>();
     uint32_t* tile_keep = tile_jlo + (ctiles + 2);
     uint32_t* tile_nnz = tile_keep + (ctiles + 2);
-    inc_tile_disc.ensure(size_t(ctiles) * 8 + 8);
     next.row_ptr.ensure((size_t(n_bound) + 1) * 4 + CSR_PAD);
     next.col.ensure(size_t(n_bound) * width * 4 + CSR_PAD);
     uint8_t* touched = inc_has_extra.as<uint8_t>();
@@ -186,13 +185,23 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     inc_tile_scan_kernel<<<1, NT, 0, stream>>>(tile_keep, tile_nnz, ctiles, levels, ictr);
     check_launch();
     PB_DISPATCH_WI(W, inc_compact_kernel<W><<<ctiles, NT, 0, stream>>>(
-                          old.words.as<uint32_t>(), c_old, n, m, levels, dist, touched, old.row_ptr.as<uint32_t>(),
-                          old.col.as<int32_t>(), inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs, skeys, sgap, inc_side_dist[scur].as<uint8_t>(), inc_s_col.as<uint32_t>(),
-                          width, tile_jlo, tile_keep, tile_nnz, inc_newidx.as<uint32_t>(), inc_side_newidx.as<uint32_t>(),
-                          next.words.as<uint32_t>(), next.full.as<uint8_t>(), c_new.as<double2>(),
-                          next.row_ptr.as<uint32_t>(), inc_simple.as<uint8_t>(), inc_tile_disc.as<double>(), ctiles, ictr,
-                          c->out));
+                          n, m, levels, dist, touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
+                          inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs, skeys, sgap,
+                          inc_side_dist[scur].as<uint8_t>(), inc_s_col.as<uint32_t>(), width, tile_jlo, tile_keep, tile_nnz,
+                          inc_newidx.as<uint32_t>(), inc_side_newidx.as<uint32_t>(), next.words.as<uint32_t>(),
+                          next.full.as<uint8_t>(), c_new.as<double2>(), next.row_ptr.as<uint32_t>(),
+                          inc_simple.as<uint8_t>(), ctiles, ictr));
     check_launch();
+    {
+        // the bulk of the bytes: keys, flags and coefficients of the surviving old rows, one streaming pass
+        const int mg = grid_for(n);
+        if (size_t(mg) * 8 > partials.cap) throw CudaFail("internal error: reduction scratch too small for the grid");
+        PB_DISPATCH_WI(W, inc_move_kernel<W><<<mg, NT, 0, stream>>>(
+                              old.words.as<uint32_t>(), c_old, n, m, dist, inc_newidx.as<uint32_t>(),
+                              next.words.as<uint32_t>(), next.full.as<uint8_t>(), c_new.as<double2>(),
+                              partials.as<double>(), &c->ticket, c->out));
+        check_launch();
+    }
     inc_fill_kernel<<<grid_for(n), NT, 0, stream>>>(
         n, levels, inc_newidx.as<uint32_t>(), touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
         with_val ? old.val.as<double>() : nullptr, inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(),

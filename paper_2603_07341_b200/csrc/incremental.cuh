@@ -446,13 +446,13 @@ static __global__ void __launch_bounds__(NT) inc_tile_scan_kernel(uint32_t* __re
 
 /// The index maps and everything that hangs on them, one CTA per tile of old rows: new index of every surviving old
 /// row = (kept rows before it) + (side keys whose insertion gap is <= it), new index of side key j = (kept rows before
-/// its gap) + j.  Writes newidx (old -> new, IDX_NONE when dropped), the new table (old rows compacted, side keys
-/// merged in), the `full` flags of the new space (dist < m), the remapped coefficients (remap_state: kept rows carry
-/// theirs, side rows start at zero, dropped rows add |c|^2 to the discarded weight), the row pointer of the new CSR
-/// and, per old row, whether its new row is a straight copy (simple).
+/// its gap) + j.  Writes newidx (old -> new, IDX_NONE when dropped), the row pointer of the new CSR, per old row
+/// whether its new row is a straight copy (simple), and everything about the (few) side rows: key, `full` flag, zero
+/// coefficient (remap_state: new rows start at zero).  The old rows' keys, flags and coefficients follow in
+/// inc_move_kernel.
 template <int W>
 static __global__ void __launch_bounds__(NT) inc_compact_kernel(
-    const uint32_t* __restrict__ table, const double2* __restrict__ c_old, uint32_t n, int m, int levels,
+    uint32_t n, int m, int levels,
     const uint8_t* __restrict__ dist, const uint8_t* __restrict__ touched, const uint32_t* __restrict__ row_ptr,
     const int32_t* __restrict__ col, const uint32_t* __restrict__ x_slot, const uint32_t* __restrict__ x_ref, int nslots,
     const uint32_t* __restrict__ side_keys, const uint32_t* __restrict__ side_gap,
@@ -460,18 +460,14 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
     const uint32_t* __restrict__ tile_jlo, const uint32_t* __restrict__ tile_keep_pre,
     const uint32_t* __restrict__ tile_nnz_pre, uint32_t* __restrict__ newidx, uint32_t* __restrict__ side_newidx,
     uint32_t* __restrict__ out_table, uint8_t* __restrict__ out_full, double2* __restrict__ c_new,
-    uint32_t* __restrict__ row_ptr_new, uint8_t* __restrict__ simple, double* __restrict__ tile_disc, uint32_t ntiles,
-    IncCounters* ctr, double* __restrict__ disc_out) {
+    uint32_t* __restrict__ row_ptr_new, uint8_t* __restrict__ simple, uint32_t ntiles, IncCounters* ctr) {
     __shared__ uint32_t o_s[INC_TILE];    // local rank among the new rows of the tile (IDX_NONE: dropped)
     __shared__ uint32_t pk_s[INC_TILE];   // kept rows of the tile before local row r
     __shared__ uint32_t cnt_s[INC_TILE];  // side keys whose gap is local row r
     __shared__ uint32_t len_s[INC_TILE];  // entries of local row r (0 when dropped); then: entries before it in the tile
     __shared__ uint32_t sl_s[INC_TILE];   // entries of the side rows whose gap is local row r
     __shared__ uint32_t scan_s[NT / 32];
-    __shared__ double red_s[NT / 32];
-    __shared__ uint32_t s_last;
     const uint32_t tile = blockIdx.x;
-    const uint32_t side_n = ctr->side_n[levels];
     const uint64_t t0 = uint64_t(tile) * INC_TILE;  // first old row of the tile
     const uint64_t t1 = min(t0 + INC_TILE, uint64_t(n) + 1);
     const uint32_t jlo = __ldg(tile_jlo + tile), jhi = __ldg(tile_jlo + tile + 1);
@@ -529,30 +525,18 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
     }
     __syncthreads();
     const uint32_t base = P + jlo;  // new index of the first new row of this tile
-    // ---- old rows: index maps, flags, coefficients, row pointer
-    double acc = 0.0;
+    // ---- old rows: index map and row pointer (their keys, flags and coefficients move in inc_move_kernel)
     for (uint32_t r = threadIdx.x; r < INC_TILE; r += NT) {
         const uint64_t i = t0 + r;
         if (i >= n) break;
         const uint32_t lo = o_s[r];
-        const double2 x = c_old[i];
         if (lo != IDX_NONE) {
             const uint32_t o = base + lo;
             newidx[i] = o;
-            out_full[o] = dist[i] < uint8_t(m) ? 1 : 0;
-            c_new[o] = x;
             row_ptr_new[o] = Q + len_s[r] + sl_s[r];
         } else {
             newidx[i] = IDX_NONE;
-            acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
         }
-    }
-    // ---- key words, one thread per word (coalesced reads and, over runs of surviving rows, writes)
-    const uint64_t wend = (min(t1, uint64_t(n)) - min(t0, uint64_t(n))) * W;
-    for (uint64_t w = threadIdx.x; w < wend; w += NT) {
-        const uint32_t r = uint32_t(w / W);
-        const uint32_t lo = o_s[r];
-        if (lo != IDX_NONE) out_table[uint64_t(base + lo) * W + (w - uint64_t(r) * W)] = __ldg(table + t0 * W + w);
     }
     // ---- side keys whose gap lies in this tile (those that share a gap are consecutive: a short backward walk)
     for (uint32_t j = jlo + threadIdx.x; j < jhi; j += NT) {
@@ -567,21 +551,63 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
         c_new[o] = make_double2(0.0, 0.0);
         row_ptr_new[o] = Q + len_s[r] + before;
     }
-    // ---- discarded weight: per-tile partials, combined in tile order by the last CTA to finish
-    const double tsum = block_sum(acc, red_s);
-    if (threadIdx.x == 0) {
-        tile_disc[tile] = tsum;
-        if (tile == ntiles - 1) row_ptr_new[ctr->h.n_new] = ctr->h.nnz_new;
-        __threadfence();
-        s_last = (atomicAdd(&ctr->h.done_c, 1u) == ntiles - 1) ? 1u : 0u;
+    if (threadIdx.x == 0 && tile == ntiles - 1) row_ptr_new[ctr->h.n_new] = ctr->h.nnz_new;
+}
+
+/// The bulk of the data movement, as one streaming pass over the old rows (a warp per 32 consecutive rows, several
+/// batches in flight): surviving rows carry their key, `full` flag (dist < m) and coefficient to their new index
+/// (remap_state, subspace.hpp:281-305: kept rows carry theirs), dropped rows add |c|^2 to the discarded weight
+/// (per-CTA partials combined in CTA order by the last CTA).  Key words move word by word across the warp -- coalesced
+/// reads and, over runs of surviving rows, coalesced writes.
+template <int W>
+static __global__ void __launch_bounds__(NT) inc_move_kernel(const uint32_t* __restrict__ table,
+                                                             const double2* __restrict__ c_old, uint32_t n, int m,
+                                                             const uint8_t* __restrict__ dist,
+                                                             const uint32_t* __restrict__ newidx,
+                                                             uint32_t* __restrict__ out_table,
+                                                             uint8_t* __restrict__ out_full, double2* __restrict__ c_new,
+                                                             double* __restrict__ partials, unsigned* ticket,
+                                                             double* __restrict__ disc_out) {
+    __shared__ double red_s[NT / 32];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    double acc[1] = {0.0};
+    for (uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        const bool in = i < n;
+        uint32_t o = IDX_NONE;
+        double2 x = make_double2(0.0, 0.0);
+        uint8_t d = 0;
+        if (in) {
+            o = __ldg(newidx + i);
+            x = __ldg(c_old + i);
+            d = __ldg(dist + i);
+        }
+        // key words of the 32 rows: word w belongs to row w / W, whose new index sits in that lane
+        uint32_t kw[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            const uint64_t w = base * W + uint32_t(q) * 32 + lane;
+            kw[q] = (w < uint64_t(n) * W) ? __ldg(table + w) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            const uint32_t wl = uint32_t(q) * 32 + lane;  // word index inside the batch
+            const uint32_t r = wl / W;
+            const uint32_t orow = __shfl_sync(0xffffffffu, o, int(r));
+            if (orow != IDX_NONE) out_table[uint64_t(orow) * W + (wl - r * W)] = kw[q];
+        }
+        if (in) {
+            if (o != IDX_NONE) {
+                c_new[o] = x;
+                out_full[o] = d < uint8_t(m) ? 1 : 0;
+            } else {
+                acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+            }
+        }
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double a = 0.0;
-    for (uint32_t t = threadIdx.x; t < ntiles; t += NT) a = __dadd_rn(a, __ldcg(tile_disc + t));
-    const double total = block_sum(a, red_s);
-    if (threadIdx.x == 0) disc_out[0] = total;
+    double tot[1];
+    if (grid_sum<1>(acc, partials, ticket, tot, red_s) && threadIdx.x == 0) disc_out[0] = tot[0];
 }
 
 /// Entries of the new CSR.  Old rows, a warp per 32 consecutive rows: their old entries are one contiguous run of

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(NT, EXPECT ? 6 : 8) taylor_order_kernel_t(uint
                                                             double b, int order, double rtol,
                                                             double* __restrict__ partials, TaylorCtl* ctl,
                                                             int ignore_stop, double* __restrict__ tot_out,
-                                                            double* __restrict__ expect_out) {
+                                                            double* __restrict__ expect_out, int first_from_x) {
     constexpr int K = EXPECT ? 5 : 2;
     __shared__ double smem[NT / 32];
     if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
@@ -98,8 +98,10 @@ __global__ void __launch_bounds__(NT, EXPECT ? 6 : 8) taylor_order_kernel_t(uint
             ar = __dadd_rn(ar, __dmul_rn(v, x.x));
             ai = __dadd_rn(ai, __dmul_rn(v, x.y));
         }
+        double2 cc;
         if (EXPECT) {
             const double2 xi = __ldg(term_in + i);
+            cc = xi;  // first_from_x: the state is only in term_in so far (c is written, not read)
             // real(conj(x) * row) = xr*rr - (-xi)*ri
             acc[2] = __dadd_rn(acc[2], __dsub_rn(__dmul_rn(xi.x, ar), __dmul_rn(-xi.y, ai)));
             acc[3] = __dadd_rn(acc[3], __dadd_rn(__dmul_rn(xi.x, xi.x), __dmul_rn(xi.y, xi.y)));
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(NT, EXPECT ? 6 : 8) taylor_order_kernel_t(uint
         // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
         const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
         const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
-        double2 cc = c[i];
+        if (!(EXPECT && first_from_x)) cc = c[i];
         cc.x = __dadd_rn(cc.x, tr);
         cc.y = __dadd_rn(cc.y, ti);
         term_out[i] = make_double2(tr, ti);
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                                                                double b, int order, double rtol, int max_row,
                                                                double* __restrict__ partials, TaylorCtl* ctl,
                                                                int ignore_stop, double* __restrict__ tot_out,
-                                                               double* __restrict__ expect_out) {
+                                                               double* __restrict__ expect_out, int first_from_x) {
     constexpr bool HAS_C = MODE != DEFER;
     constexpr int K = MODE == FIRST ? 5 : (MODE == CATCHUP ? 3 : (MODE == DEFER ? 1 : 2));
     extern __shared__ __align__(128) unsigned char smem[];
@@ -482,8 +484,10 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         const bool live = i < n;
         // independent of the ring: this row's slice of c and (catch-up / first order) of the previous term
         double2 cc = make_double2(0.0, 0.0), tp = make_double2(0.0, 0.0);
-        if (HAS_C && live) cc = c[i];
+        // (first_from_x: the state is only in term_in so far -- the first order writes c, it does not read it)
+        if (HAS_C && live && !(MODE == FIRST && first_from_x)) cc = c[i];
         if ((MODE == CATCHUP || MODE == FIRST) && live) tp = __ldg(term_in + i);
+        if (MODE == FIRST && first_from_x) cc = tp;
         double dg = 0.0;  // the row's diagonal element when the model's diagonals are not in the table
         if (CODED && diag != nullptr && live) dg = __ldg(diag + i);
         mbar_wait(full + s, (j / STAGES) & 1);
@@ -607,7 +611,7 @@ template <int MODE, int MAXR, bool CODED>
 static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
                      const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
                      double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop, double* tot_out,
-                     double* expect_out) {
+                     double* expect_out, int first_from_x) {
     const int vt_n = CODED ? codes->vt_n : 0;
     const Layout L = make_layout<CODED>(MAXR, vt_n);
     static int ready = 0;     // 1: usable, -1: not (the launch falls back to the row kernels)
@@ -632,7 +636,7 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
     taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
-        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out);
+        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
     return true;
 }
 
@@ -640,29 +644,29 @@ template <int MODE, bool CODED>
 static bool launch_c(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
                      const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
                      double b, int order, double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop,
-                     double* tot_out, double* expect_out) {
+                     double* tot_out, double* expect_out, int first_from_x) {
     // instantiations by row-length bound: 1D models (<= 5 entries), 2D (<= 7), 3D (<= 9)
     if (max_row <= 5)
         return launch_r<MODE, 5, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
-                                        partials, ctl, ignore_stop, tot_out, expect_out);
+                                        partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
     if (max_row <= 7)
         return launch_r<MODE, 7, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
-                                        partials, ctl, ignore_stop, tot_out, expect_out);
+                                        partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
     return launch_r<MODE, 9, CODED>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
-                                    partials, ctl, ignore_stop, tot_out, expect_out);
+                                    partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
 }
 
 template <int MODE>
 static bool launch(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr, const int32_t* col,
                    const double* val, const TaylorCodes* codes, const double2* term_in, double2* term_out, double2* c,
                    double b, int order, double rtol, int max_row, double* partials, TaylorCtl* ctl, int ignore_stop,
-                   double* tot_out, double* expect_out) {
+                   double* tot_out, double* expect_out, int first_from_x = 0) {
     if (max_row < 1 || max_row > 9) return false;
     if (codes != nullptr && codes->code != nullptr && codes->vt_n > 0 && codes->vt_n <= TAYLOR_VT_MAX)
         return launch_c<MODE, true>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, rtol,
-                                    max_row, partials, ctl, ignore_stop, tot_out, expect_out);
+                                    max_row, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
     return launch_c<MODE, false>(sm_count, stream, n, row_ptr, col, val, nullptr, term_in, term_out, c, b, order, rtol,
-                                 max_row, partials, ctl, ignore_stop, tot_out, expect_out);
+                                 max_row, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
 }
 
 }  // namespace tile
@@ -763,11 +767,12 @@ static int resident_ctas(K kernel, int fallback) {
 void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
-                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes) {
+                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes,
+                          int first_from_x) {
     if (g_use_tiles && max_row > 0) {
         const bool ok = expect ? tile::launch<tile::FIRST>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out,
                                                            c, b, order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
-                                                           expect_out)
+                                                           expect_out, first_from_x)
                                : tile::launch<tile::SINGLE>(sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out,
                                                             c, b, order, rtol, max_row, partials, ctl, ignore_stop, tot_out,
                                                             expect_out);
@@ -777,10 +782,11 @@ void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stre
         // this variant needs more registers: size its grid to what is resident so the launch is a single wave
         static const int per_sm = resident_ctas(taylor_order_kernel_t<true>, 4);
         taylor_order_kernel_t<true><<<std::min(grid, sm_count * per_sm), NT, 0, stream>>>(
-            n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, partials, ctl, ignore_stop, tot_out, expect_out);
+            n, row_ptr, col, val, term_in, term_out, c, b, order, rtol, partials, ctl, ignore_stop, tot_out, expect_out,
+            first_from_x);
     } else {
         taylor_order_kernel_t<false><<<grid, NT, 0, stream>>>(n, row_ptr, col, val, term_in, term_out, c, b, order, rtol,
-                                                              partials, ctl, ignore_stop, tot_out, expect_out);
+                                                              partials, ctl, ignore_stop, tot_out, expect_out, 0);
     }
 }
 

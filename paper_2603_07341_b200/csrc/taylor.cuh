@@ -41,13 +41,16 @@ struct TaylorCodes {
 /// max_row: upper bound on the entries of a row (0 = unknown).  With a bound <= 15 the launch uses the TMA tile kernels
 /// (taylor.cu, namespace tile); otherwise -- arbitrary uploaded CSR matrices -- the thread-per-row kernels.
 /// PB200_TAYLOR_ROWS=1 forces the row kernels (A/B measurements).
+/// first_from_x (first order of a step, expect = true): the state vector is only in term_in so far; the launch uses it
+/// as the old c as well and only WRITES c -- no copy of the state into the term buffer, no read of c.
 /// Launch modes (see taylor.cu).  `grid` is the caller's row grid (8 CTAs per SM); the first-order and catch-up
 /// kernels clamp it to one resident wave.  All launches are asynchronous on `stream`; errors surface in the caller's
 /// cudaGetLastError check.
 void taylor_launch_single(bool expect, int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                           const int32_t* col, const double* val, const double2* term_in, double2* term_out, double2* c,
                           double b, int order, double rtol, double* partials, TaylorCtl* ctl, int ignore_stop,
-                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes = nullptr);
+                          double* tot_out, double* expect_out, int max_row, const TaylorCodes* codes = nullptr,
+                          int first_from_x = 0);
 void taylor_launch_defer(int grid, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
                          const int32_t* col, const double* val, const double2* term_in, double2* term_out, double b,
                          int order, double* partials, TaylorCtl* ctl, int max_row, const TaylorCodes* codes = nullptr);
