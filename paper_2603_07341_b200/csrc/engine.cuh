@@ -365,7 +365,7 @@ struct Engine {
     bool grow_incremental(const Space& old, const double2* c_old, uint32_t kept, int m, Space& next, DevBuf& c_new);
     DevBuf inc_dist, inc_elist, inc_side_keys[2], inc_side_gap[2], inc_side_dist[2], inc_new_keys, inc_new_gap,
         inc_newidx, inc_inv, inc_side_newidx, inc_s_col, inc_s_val, inc_has_extra, inc_ctr, inc_simple, inc_buckets,
-        inc_tile_disc, inc_tile_jlo, inc_xlist, inc_x_slot, inc_x_ref, inc_x_val, inc_s_code, inc_x_code;
+        inc_tile_disc, inc_tile_jlo, inc_xlist, inc_x_slot, inc_x_ref, inc_x_val, inc_s_code, inc_x_code, inc_row_len;
     uint64_t inc_steps = 0, inc_fallbacks = 0, inc_side_keys_total = 0, inc_expanded_total = 0;
     double remap(const uint32_t* src_words, const double2* src_c, uint32_t ns, const uint32_t* dst_words,
                  uint32_t nd, double2* dst_c);

@@ -132,6 +132,7 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     inc_s_val.ensure(size_t(side_cap) * width * 8 + 8);
     inc_has_extra.ensure(size_t(n) + 64);  // `touched` flags: bit 0 = the row loses an entry, bit 1 = it gains one
     inc_simple.ensure(size_t(n) + 64);
+    inc_row_len.ensure(size_t(n) + 64);
     const uint32_t ctiles = uint32_t((uint64_t(n) + 1 + INC_TILE - 1) / INC_TILE);
     inc_tile_jlo.ensure((size_t(ctiles) + 2) * 4 * 3);
     uint32_t* tile_jlo = inc_tile_jlo.as<uint32_t>();
@@ -180,17 +181,16 @@ bool Engine::grow_incremental(const Space& old, const double2* c_old, uint32_t k
     check_launch();
     inc_tile_nnz_kernel<<<ctiles, NT, 0, stream>>>(n, m, dist, touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
                                                    inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs,
-                                                   inc_s_col.as<uint32_t>(), width, tile_jlo, tile_nnz);
+                                                   inc_s_col.as<uint32_t>(), width, tile_jlo, tile_nnz,
+                                                   inc_row_len.as<uint8_t>(), inc_simple.as<uint8_t>());
     check_launch();
     inc_tile_scan_kernel<<<1, NT, 0, stream>>>(tile_keep, tile_nnz, ctiles, levels, ictr);
     check_launch();
     PB_DISPATCH_WI(W, inc_compact_kernel<W><<<ctiles, NT, 0, stream>>>(
-                          n, m, levels, dist, touched, old.row_ptr.as<uint32_t>(), old.col.as<int32_t>(),
-                          inc_x_slot.as<uint32_t>(), inc_x_ref.as<uint32_t>(), xs, skeys, sgap,
-                          inc_side_dist[scur].as<uint8_t>(), inc_s_col.as<uint32_t>(), width, tile_jlo, tile_keep, tile_nnz,
-                          inc_newidx.as<uint32_t>(), inc_side_newidx.as<uint32_t>(), next.words.as<uint32_t>(),
-                          next.full.as<uint8_t>(), c_new.as<double2>(), next.row_ptr.as<uint32_t>(),
-                          inc_simple.as<uint8_t>(), ctiles, ictr));
+                          n, m, levels, dist, inc_row_len.as<uint8_t>(), skeys, sgap, inc_side_dist[scur].as<uint8_t>(),
+                          inc_s_col.as<uint32_t>(), width, tile_jlo, tile_keep, tile_nnz, inc_newidx.as<uint32_t>(),
+                          inc_side_newidx.as<uint32_t>(), next.words.as<uint32_t>(), next.full.as<uint8_t>(),
+                          c_new.as<double2>(), next.row_ptr.as<uint32_t>(), ctiles, ictr));
     check_launch();
     {
         // the bulk of the bytes: keys, flags and coefficients of the surviving old rows, one streaming pass

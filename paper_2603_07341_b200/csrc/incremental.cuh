@@ -91,7 +91,7 @@ static __global__ void __launch_bounds__(NT) inc_level_kernel(uint32_t n, int k,
 template <int W>
 __device__ __forceinline__ bool side_find(const uint32_t* __restrict__ side_keys, uint32_t side_n, const Key<W>& k,
                                           uint32_t& pos) {
-    return find_row_in<W>(side_keys, 0, side_n, k, pos);
+    return find_row_in4<W>(side_keys, 0, side_n, k, pos);
 }
 
 /// Key-based expansion of one BFS level, one thread per (source, neighbour slot): sources are the queued old rows
@@ -125,7 +125,7 @@ static __global__ void __launch_bounds__(NT) inc_expand_kernel(ModelDev m, const
         for_each_neighbor<W>(m, key, false, [&](int, const Key<W>& kk, double, bool) {
             if (idx++ != slot) return;
             uint32_t pos, spos;
-            if (find_row<W>(table, n, kk, pos)) {
+            if (find_row_in4<W>(table, 0, n, kk, pos)) {
                 if (dist[pos] > uint8_t(k + 1)) dist[pos] = uint8_t(k + 1);
             } else if (!side_find<W>(side_keys, side_n, kk, spos)) {
                 const uint32_t c = append_slot(&ctr->n_cand[k]);
@@ -254,7 +254,7 @@ static __global__ void __launch_bounds__(NT) inc_side_search_kernel(ModelDev m, 
             a = amp;
             if (is_diag) {
                 ref = INV_SIDE | j;
-            } else if (find_row<W>(table, n, kk, pos)) {
+            } else if (find_row_in4<W>(table, 0, n, kk, pos)) {
                 ref = pos;
                 if (dist[pos] <= uint8_t(order)) touched[pos] |= 2;  // every writer of this byte stores the same value here
             } else if (side_find<W>(side_keys, side_n, kk, pos)) {
@@ -384,7 +384,9 @@ __device__ __forceinline__ uint32_t side_row_len(const uint32_t* __restrict__ s_
     return len;
 }
 
-/// Per tile of old rows: entries of the new rows the tile produces (its surviving rows + its side keys).
+/// Per tile of old rows: entries of the new rows the tile produces (its surviving rows + its side keys); per old row,
+/// the length of its new row and whether that row is a straight copy (simple) -- inc_compact_kernel and
+/// inc_fill_kernel read them instead of walking the touched rows again.
 static __global__ void __launch_bounds__(NT) inc_tile_nnz_kernel(uint32_t n, int m, const uint8_t* __restrict__ dist,
                                                                  const uint8_t* __restrict__ touched,
                                                                  const uint32_t* __restrict__ row_ptr,
@@ -393,7 +395,9 @@ static __global__ void __launch_bounds__(NT) inc_tile_nnz_kernel(uint32_t n, int
                                                                  const uint32_t* __restrict__ x_ref, int nslots,
                                                                  const uint32_t* __restrict__ s_ref, int width,
                                                                  const uint32_t* __restrict__ tile_jlo,
-                                                                 uint32_t* __restrict__ tile_nnz) {
+                                                                 uint32_t* __restrict__ tile_nnz,
+                                                                 uint8_t* __restrict__ row_len_new,
+                                                                 uint8_t* __restrict__ simple) {
     __shared__ uint32_t scan_s[NT / 32];
     const uint32_t tile = blockIdx.x;
     const uint64_t t0 = uint64_t(tile) * INC_TILE;
@@ -401,10 +405,13 @@ static __global__ void __launch_bounds__(NT) inc_tile_nnz_kernel(uint32_t n, int
 #pragma unroll
     for (int q = 0; q < INC_IPT; ++q) {
         const uint64_t i = t0 + uint32_t(q) * NT + threadIdx.x;
-        if (i < n && dist[i] <= uint8_t(m)) {
-            bool smp;
-            cnt += new_row_len(uint32_t(i), m, dist, touched[i], row_ptr, col, x_slot, x_ref, nslots, smp);
-        }
+        if (i >= n) continue;
+        uint32_t len = 0;
+        bool smp = false;
+        if (dist[i] <= uint8_t(m)) len = new_row_len(uint32_t(i), m, dist, touched[i], row_ptr, col, x_slot, x_ref, nslots, smp);
+        row_len_new[i] = uint8_t(len);  // (0 for a dropped row; a row holds at most MAX_ROW entries)
+        simple[i] = smp ? 1 : 0;
+        cnt += len;
     }
     const uint32_t jlo = tile_jlo[tile], jhi = tile_jlo[tile + 1];
     for (uint32_t j = jlo + threadIdx.x; j < jhi; j += NT) cnt += side_row_len(s_ref, j, width, dist, m);
@@ -444,6 +451,11 @@ static __global__ void __launch_bounds__(NT) inc_tile_scan_kernel(uint32_t* __re
     }
 }
 
+/// Index of local row r inside the tile's shared arrays: one pad word per 32 rows, so that both the coalesced pass
+/// (thread t -> rows t, t + NT, ...) and the scan pass (thread t -> rows 8t .. 8t + 7) are free of bank conflicts.
+__device__ __forceinline__ uint32_t tile_slot(uint32_t r) { return r + (r >> 5); }
+constexpr int INC_TILE_PAD = INC_TILE + INC_TILE / 32;
+
 /// The index maps and everything that hangs on them, one CTA per tile of old rows: new index of every surviving old
 /// row = (kept rows before it) + (side keys whose insertion gap is <= it), new index of side key j = (kept rows before
 /// its gap) + j.  Writes newidx (old -> new, IDX_NONE when dropped), the row pointer of the new CSR, per old row
@@ -452,46 +464,38 @@ static __global__ void __launch_bounds__(NT) inc_tile_scan_kernel(uint32_t* __re
 /// inc_move_kernel.
 template <int W>
 static __global__ void __launch_bounds__(NT) inc_compact_kernel(
-    uint32_t n, int m, int levels,
-    const uint8_t* __restrict__ dist, const uint8_t* __restrict__ touched, const uint32_t* __restrict__ row_ptr,
-    const int32_t* __restrict__ col, const uint32_t* __restrict__ x_slot, const uint32_t* __restrict__ x_ref, int nslots,
+    uint32_t n, int m, int levels, const uint8_t* __restrict__ dist, const uint8_t* __restrict__ row_len_new,
     const uint32_t* __restrict__ side_keys, const uint32_t* __restrict__ side_gap,
     const uint8_t* __restrict__ side_dist, const uint32_t* __restrict__ s_ref, int width,
     const uint32_t* __restrict__ tile_jlo, const uint32_t* __restrict__ tile_keep_pre,
     const uint32_t* __restrict__ tile_nnz_pre, uint32_t* __restrict__ newidx, uint32_t* __restrict__ side_newidx,
     uint32_t* __restrict__ out_table, uint8_t* __restrict__ out_full, double2* __restrict__ c_new,
-    uint32_t* __restrict__ row_ptr_new, uint8_t* __restrict__ simple, uint32_t ntiles, IncCounters* ctr) {
-    __shared__ uint32_t o_s[INC_TILE];    // local rank among the new rows of the tile (IDX_NONE: dropped)
-    __shared__ uint32_t pk_s[INC_TILE];   // kept rows of the tile before local row r
-    __shared__ uint32_t cnt_s[INC_TILE];  // side keys whose gap is local row r
-    __shared__ uint32_t len_s[INC_TILE];  // entries of local row r (0 when dropped); then: entries before it in the tile
-    __shared__ uint32_t sl_s[INC_TILE];   // entries of the side rows whose gap is local row r
+    uint32_t* __restrict__ row_ptr_new, uint32_t ntiles, IncCounters* ctr) {
+    __shared__ uint32_t o_s[INC_TILE_PAD];    // local rank among the new rows of the tile (IDX_NONE: dropped)
+    __shared__ uint32_t pk_s[INC_TILE_PAD];   // kept rows of the tile before local row r
+    __shared__ uint32_t cnt_s[INC_TILE_PAD];  // side keys whose gap is local row r
+    __shared__ uint32_t len_s[INC_TILE_PAD];  // entries of local row r (0 when dropped); then: entries before it in the tile
+    __shared__ uint32_t sl_s[INC_TILE_PAD];   // entries of the side rows whose gap is local row r
+    __shared__ uint8_t keep_s[INC_TILE];      // the row survives
     __shared__ uint32_t scan_s[NT / 32];
     const uint32_t tile = blockIdx.x;
     const uint64_t t0 = uint64_t(tile) * INC_TILE;  // first old row of the tile
-    const uint64_t t1 = min(t0 + INC_TILE, uint64_t(n) + 1);
     const uint32_t jlo = __ldg(tile_jlo + tile), jhi = __ldg(tile_jlo + tile + 1);
     const uint32_t P = __ldg(tile_keep_pre + tile), Q = __ldg(tile_nnz_pre + tile);
-    for (int r = threadIdx.x; r < INC_TILE; r += NT) {
-        cnt_s[r] = 0;
-        sl_s[r] = 0;
-    }
-    __syncthreads();
-    // row lengths (coalesced mapping) and the side keys of the tile
+    // row lengths and survival flags (coalesced), and the side keys of the tile
     for (uint32_t r = threadIdx.x; r < INC_TILE; r += NT) {
         const uint64_t i = t0 + r;
-        uint32_t len = 0;
-        if (i < n && dist[i] <= uint8_t(m)) {
-            bool smp;
-            len = new_row_len(uint32_t(i), m, dist, touched[i], row_ptr, col, x_slot, x_ref, nslots, smp);
-            simple[i] = smp ? 1 : 0;
-        }
-        len_s[r] = len;
+        const bool kept = i < n && dist[i] <= uint8_t(m);
+        len_s[tile_slot(r)] = kept ? uint32_t(row_len_new[i]) : 0u;
+        keep_s[r] = kept ? 1 : 0;
+        cnt_s[tile_slot(r)] = 0;
+        sl_s[tile_slot(r)] = 0;
     }
+    __syncthreads();
     for (uint32_t j = jlo + threadIdx.x; j < jhi; j += NT) {
         const uint32_t r = __ldg(side_gap + j) - uint32_t(t0);
-        atomicAdd(&cnt_s[r], 1u);
-        atomicAdd(&sl_s[r], side_row_len(s_ref, j, width, dist, m));
+        atomicAdd(&cnt_s[tile_slot(r)], 1u);
+        atomicAdd(&sl_s[tile_slot(r)], side_row_len(s_ref, j, width, dist, m));
     }
     __syncthreads();
     // thread t owns local rows [t*IPT, (t+1)*IPT): three exclusive scans (kept rows, side keys, entries)
@@ -500,11 +504,10 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
     uint32_t ksum = 0, csum = 0, zsum = 0;
 #pragma unroll
     for (int q = 0; q < INC_IPT; ++q) {
-        const uint64_t i = t0 + r0 + q;
-        keep[q] = (i < n && dist[i] <= uint8_t(m)) ? 1u : 0u;
+        keep[q] = keep_s[r0 + q];
         ksum += keep[q];
-        csum += cnt_s[r0 + q];
-        zsum += len_s[r0 + q] + sl_s[r0 + q];
+        csum += cnt_s[tile_slot(r0 + q)];
+        zsum += len_s[tile_slot(r0 + q)] + sl_s[tile_slot(r0 + q)];
     }
     uint32_t tot;
     const uint32_t kpre = block_exclusive_scan_u32(ksum, scan_s, tot);
@@ -514,11 +517,12 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
         uint32_t kr = kpre, cr = cpre, zr = zpre;
 #pragma unroll
         for (int q = 0; q < INC_IPT; ++q) {
-            const uint32_t lr = len_s[r0 + q], sr = sl_s[r0 + q];
-            cr += cnt_s[r0 + q];  // side keys with gap <= this row precede it
-            pk_s[r0 + q] = kr;
-            o_s[r0 + q] = keep[q] ? kr + cr : IDX_NONE;
-            len_s[r0 + q] = zr;   // entries of the tile before the side rows of gap r (those come first, then row r)
+            const uint32_t sl = tile_slot(r0 + q);
+            const uint32_t lr = len_s[sl], sr = sl_s[sl];
+            cr += cnt_s[sl];  // side keys with gap <= this row precede it
+            pk_s[sl] = kr;
+            o_s[sl] = keep[q] ? kr + cr : IDX_NONE;
+            len_s[sl] = zr;   // entries of the tile before the side rows of gap r (those come first, then row r)
             zr += lr + sr;
             kr += keep[q];
         }
@@ -529,11 +533,12 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
     for (uint32_t r = threadIdx.x; r < INC_TILE; r += NT) {
         const uint64_t i = t0 + r;
         if (i >= n) break;
-        const uint32_t lo = o_s[r];
+        const uint32_t sl = tile_slot(r);
+        const uint32_t lo = o_s[sl];
         if (lo != IDX_NONE) {
             const uint32_t o = base + lo;
             newidx[i] = o;
-            row_ptr_new[o] = Q + len_s[r] + sl_s[r];
+            row_ptr_new[o] = Q + len_s[sl] + sl_s[sl];
         } else {
             newidx[i] = IDX_NONE;
         }
@@ -541,15 +546,15 @@ static __global__ void __launch_bounds__(NT) inc_compact_kernel(
     // ---- side keys whose gap lies in this tile (those that share a gap are consecutive: a short backward walk)
     for (uint32_t j = jlo + threadIdx.x; j < jhi; j += NT) {
         const uint32_t g = __ldg(side_gap + j);
-        const uint32_t r = g - uint32_t(t0);
-        const uint32_t o = P + pk_s[r] + j;
+        const uint32_t sl = tile_slot(g - uint32_t(t0));
+        const uint32_t o = P + pk_s[sl] + j;
         uint32_t before = 0;
         for (uint32_t jj = j; jj > jlo && __ldg(side_gap + jj - 1) == g; --jj) before += side_row_len(s_ref, jj - 1, width, dist, m);
         side_newidx[j] = o;
         store_key<W>(out_table + size_t(o) * W, load_key<W>(side_keys + size_t(j) * W));
         out_full[o] = side_dist[j] < uint8_t(m) ? 1 : 0;
         c_new[o] = make_double2(0.0, 0.0);
-        row_ptr_new[o] = Q + len_s[r] + before;
+        row_ptr_new[o] = Q + len_s[sl] + before;
     }
     if (threadIdx.x == 0 && tile == ntiles - 1) row_ptr_new[ctr->h.n_new] = ctr->h.nnz_new;
 }
