@@ -632,6 +632,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
     // value codes (taylor.cuh, TaylorCodes) travel with the entries: code_old == nullptr -> none
     const uint16_t* __restrict__ code_old, const double* __restrict__ diag_old, const uint16_t* __restrict__ x_code,
     const uint16_t* __restrict__ s_code, uint16_t* __restrict__ code_new, double* __restrict__ diag_new) {
+    __shared__ uint32_t dst_s[(NT / 32) * 32 * MAX_ROW];
     const uint32_t side_n = ctr->side_n[levels];
     const bool coded = code_old != nullptr;
     const bool with_val = val_new != nullptr;  // a coded space may leave the 8-byte values behind (Space::val_valid)
@@ -657,31 +658,35 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
             }
         }
         const bool kept = o != IDX_NONE;
-        const bool smp = kept && simple[i];
-        if (coded && diag_old != nullptr && kept) diag_new[o] = __ldg(diag_old + i);
-        const uint32_t d0 = kept ? row_ptr_new[o] : 0u;  // new offset of the row's first entry
-        const unsigned smask = __ballot_sync(0xffffffffu, smp);
         const uint32_t rp0 = __shfl_sync(0xffffffffu, rp, 0);
         const uint32_t end = __ldg(row_ptr + (base + 32 < n ? base + 32 : n));
         const uint32_t total = end - rp0;
+        // straight copies move cooperatively (below); a batch with rows longer than a model-built H_eff has (never in
+        // practice) leaves all its rows to the per-row path
+        const bool smp = kept && simple[i] && total <= 32u * MAX_ROW;
+        if (coded && diag_old != nullptr && kept) diag_new[o] = __ldg(diag_old + i);
+        const uint32_t d0 = kept ? row_ptr_new[o] : 0u;  // new offset of the row's first entry
+        const unsigned smask = __ballot_sync(0xffffffffu, smp);
         if (smask != 0) {
+            // Destination of every entry of the batch: a row lane writes d0 + j for its (<= MAX_ROW) entries into the
+            // warp's slice of shared memory (IDX_NONE for rows that are not straight copies), entry lanes read it back
+            // coalesced -- one LDS per entry instead of a search over the 32 row offsets.
+            uint32_t* dst_w = dst_s + (threadIdx.x >> 5) * (32 * MAX_ROW);
+            {
+                const uint32_t nxt = __shfl_down_sync(0xffffffffu, rp, 1);
+                const uint32_t len = (lane == 31 ? end : nxt) - rp;
+                const uint32_t st = rp - rp0;
+                for (uint32_t j = 0; j < len; ++j) dst_w[st + j] = smp ? d0 + j : IDX_NONE;
+            }
+            __syncwarp();
             for (uint32_t k0 = 0; k0 < total; k0 += 128) {
-                uint32_t eo[4], dst[4];
+                uint32_t dst[4];
                 bool ok[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t k = k0 + uint32_t(u) * 32 + lane;
-                    const uint32_t e = rp0 + (k < total ? k : total - 1);
-                    uint32_t r = 0;  // last row whose offset is <= e
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const uint32_t v = __shfl_sync(0xffffffffu, rp, (r + step) & 31);
-                        if (v <= e) r += step;
-                    }
-                    const uint32_t off = e - __shfl_sync(0xffffffffu, rp, r);
-                    dst[u] = __shfl_sync(0xffffffffu, d0, r) + off;
-                    eo[u] = e;
-                    ok[u] = k < total && ((smask >> r) & 1u);
+                    dst[u] = k < total ? dst_w[k] : IDX_NONE;
+                    ok[u] = dst[u] != IDX_NONE;
                 }
                 int32_t cv[4];
                 double vv[4];
@@ -689,9 +694,10 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (ok[u]) {
-                        cv[u] = __ldg(col + eo[u]);
-                        if (with_val) vv[u] = __ldg(val + eo[u]);
-                        if (coded) cc[u] = __ldg(code_old + eo[u]);
+                        const uint32_t e = rp0 + k0 + uint32_t(u) * 32 + lane;
+                        cv[u] = __ldg(col + e);
+                        if (with_val) vv[u] = __ldg(val + e);
+                        if (coded) cc[u] = __ldg(code_old + e);
                     }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -704,6 +710,7 @@ static __global__ void __launch_bounds__(NT) inc_fill_kernel(
                         if (coded) code_new[dst[u]] = cc[u];
                     }
             }
+            __syncwarp();  // the slice is rewritten by the next batch
         }
         if (!kept || smp) continue;
         // extras of this row: its neighbours among the side keys, ascending
