@@ -291,7 +291,7 @@ namespace tile {
 #define TILE_MINB 1
 #endif
 #ifndef TILE_EVICT_FIRST
-#define TILE_EVICT_FIRST 0
+#define TILE_EVICT_FIRST 1  // the matrix streams through once per launch: evict-first in L2 (C4 expmv -1.4 %, C2 +-0)
 #endif
 #ifndef TILE_STAGES_CODED
 #define TILE_STAGES_CODED 3
@@ -349,6 +349,113 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 enum Mode { SINGLE = 0, FIRST = 1, DEFER = 2, CATCHUP = 3 };
 
+/// What a consumer does with a finished row sum (ar, ai) = (H term_in)_i: the new term, the c update of its mode and
+/// the partial sums (acc[0] |term|^2, acc[1] |c|^2, acc[2] CATCHUP: |c + previous term|^2 / FIRST: <x|H|x>, acc[3..4]
+/// FIRST: |x|^2, #non-finite).  Same operations in the same order as the row kernels and propagator.hpp:68-84.
+template <int MODE>
+__host__ __device__ constexpr int mode_sums() {
+    return MODE == FIRST ? 5 : (MODE == CATCHUP ? 3 : (MODE == DEFER ? 1 : 2));
+}
+template <int MODE>
+__device__ __forceinline__ void finish_row(uint32_t i, double ar, double ai, double2 cc, double2 tp, double b,
+                                           double2* __restrict__ term_out, double2* __restrict__ c,
+                                           double (&acc)[mode_sums<MODE>()]) {
+    constexpr bool HAS_C = MODE != DEFER;
+    if (MODE == FIRST) {
+        // real(conj(x) * row) = xr*rr - (-xi)*ri
+        acc[2] = __dadd_rn(acc[2], __dsub_rn(__dmul_rn(tp.x, ar), __dmul_rn(-tp.y, ai)));
+        acc[3] = __dadd_rn(acc[3], __dadd_rn(__dmul_rn(tp.x, tp.x), __dmul_rn(tp.y, tp.y)));
+        if (!isfinite(tp.x) || !isfinite(tp.y)) acc[4] = acc[4] + 1.0;
+    }
+    // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
+    const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
+    const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
+    term_out[i] = make_double2(tr, ti);
+    acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti)));
+    if (HAS_C) {
+        if (MODE == CATCHUP) {
+            cc.x = __dadd_rn(cc.x, tp.x);
+            cc.y = __dadd_rn(cc.y, tp.y);
+            acc[2] = __dadd_rn(acc[2], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+        }
+        cc.x = __dadd_rn(cc.x, tr);
+        cc.y = __dadd_rn(cc.y, ti);
+        c[i] = cc;
+        acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
+    }
+}
+
+/// Reduction of the consumers' partial sums (fixed tree inside the CTA, per-CTA partials combined by the last CTA in
+/// CTA order) and, in that last CTA, the stop rule of the launch's mode.  Called by the TR consumer threads only.
+template <int MODE, int K>
+__device__ __forceinline__ void reduce_and_rule(double (&acc)[K], double* red, double* __restrict__ partials,
+                                                TaylorCtl* ctl, int order, double rtol, double* __restrict__ tot_out,
+                                                double* __restrict__ expect_out) {
+    const uint32_t tid = threadIdx.x;
+    auto consumer_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(TR) : "memory"); };
+    const int lane = tid & 31, warp = tid >> 5;
+    double blk[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const double w = warp_sum(acc[q]);
+        consumer_sync();
+        if (lane == 0) red[warp] = w;
+        consumer_sync();
+        double tsum = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
+        blk[q] = tsum;
+    }
+    uint32_t* flag = reinterpret_cast<uint32_t*>(red + 12);
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) partials[size_t(q) * gridDim.x + blockIdx.x] = blk[q];
+        __threadfence();
+        *flag = (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    consumer_sync();
+    if (*flag == 0) return;
+    __threadfence();
+    double tot[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        double a = 0.0;
+        for (uint32_t g = tid; g < gridDim.x; g += TR) a = __dadd_rn(a, __ldcg(partials + size_t(q) * gridDim.x + g));
+        const double w = warp_sum(a);
+        consumer_sync();
+        if (lane == 0) red[warp] = w;
+        consumer_sync();
+        double tsum = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
+        tot[q] = tsum;
+    }
+    if (tid != 0) return;
+    ctl->ticket = 0;
+    if (MODE == FIRST) {
+        expect_out[0] = tot[2];
+        expect_out[1] = tot[3];
+        expect_out[2] = tot[4];
+    }
+    if (MODE == DEFER) {
+        ctl->pending = 1;
+        ctl->pending_tn2 = tot[0];
+        ctl->deferred += 1;
+        if (order > ctl->order_used) ctl->order_used = order;
+        ctl->last_order = order;
+    } else if (tot_out) {  // sharded: the sums are all-reduced first, taylor_stop_kernel applies the rule
+        tot_out[0] = tot[0];
+        tot_out[1] = tot[1];
+    } else if (MODE == CATCHUP) {
+        taylor_apply_rule(ctl, order - 1, ctl->pending_tn2, tot[2], rtol);  // streak was 0: cannot stop here
+        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
+        ctl->pending = 0;
+    } else {
+        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
+    }
+    __threadfence();
+}
+
 struct Layout {  // byte offsets inside the dynamic shared memory of one CTA
     uint32_t ecap;   // entries a stage holds (TR * max_row + slack for the aligned start)
     uint32_t rp, col, val, stage_bytes, bars, vt, total;
@@ -401,7 +508,7 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                                                                int ignore_stop, double* __restrict__ tot_out,
                                                                double* __restrict__ expect_out, int first_from_x) {
     constexpr bool HAS_C = MODE != DEFER;
-    constexpr int K = MODE == FIRST ? 5 : (MODE == CATCHUP ? 3 : (MODE == DEFER ? 1 : 2));
+    constexpr int K = mode_sums<MODE>();
     extern __shared__ __align__(128) unsigned char smem[];
     if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
     if (MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
@@ -516,95 +623,10 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(empty + s);  // this warp has read everything it needs from the stage
-        if (live) {
-            if (MODE == FIRST) {
-                // real(conj(x) * row) = xr*rr - (-xi)*ri
-                acc[2] = __dadd_rn(acc[2], __dsub_rn(__dmul_rn(tp.x, ar), __dmul_rn(-tp.y, ai)));
-                acc[3] = __dadd_rn(acc[3], __dadd_rn(__dmul_rn(tp.x, tp.x), __dmul_rn(tp.y, tp.y)));
-                if (!isfinite(tp.x) || !isfinite(tp.y)) acc[4] = acc[4] + 1.0;
-            }
-            // (0, b) * (ar, ai) exactly as the compiler expands std::complex multiplication
-            const double tr = __dsub_rn(__dmul_rn(0.0, ar), __dmul_rn(b, ai));
-            const double ti = __dadd_rn(__dmul_rn(0.0, ai), __dmul_rn(b, ar));
-            term_out[i] = make_double2(tr, ti);
-            acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(tr, tr), __dmul_rn(ti, ti)));
-            if (HAS_C) {
-                if (MODE == CATCHUP) {
-                    cc.x = __dadd_rn(cc.x, tp.x);
-                    cc.y = __dadd_rn(cc.y, tp.y);
-                    acc[2] = __dadd_rn(acc[2], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
-                }
-                cc.x = __dadd_rn(cc.x, tr);
-                cc.y = __dadd_rn(cc.y, ti);
-                c[i] = cc;
-                acc[1] = __dadd_rn(acc[1], __dadd_rn(__dmul_rn(cc.x, cc.x), __dmul_rn(cc.y, cc.y)));
-            }
-        }
+        if (live) finish_row<MODE>(i, ar, ai, cc, tp, b, term_out, c, acc);
     }
 
-    // ---------------- reduction: fixed tree inside the CTA, partials combined by the last CTA in CTA order ------
-    auto consumer_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(TR) : "memory"); };
-    const int lane = tid & 31, warp = tid >> 5;
-    double blk[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        const double w = warp_sum(acc[q]);
-        consumer_sync();
-        if (lane == 0) red[warp] = w;
-        consumer_sync();
-        double tsum = 0.0;
-#pragma unroll
-        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
-        blk[q] = tsum;
-    }
-    uint32_t* flag = reinterpret_cast<uint32_t*>(red + 12);
-    if (tid == 0) {
-#pragma unroll
-        for (int q = 0; q < K; ++q) partials[size_t(q) * gridDim.x + blockIdx.x] = blk[q];
-        __threadfence();
-        *flag = (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    consumer_sync();
-    if (*flag == 0) return;
-    __threadfence();
-    double tot[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        double a = 0.0;
-        for (uint32_t g = tid; g < gridDim.x; g += TR) a = __dadd_rn(a, __ldcg(partials + size_t(q) * gridDim.x + g));
-        const double w = warp_sum(a);
-        consumer_sync();
-        if (lane == 0) red[warp] = w;
-        consumer_sync();
-        double tsum = 0.0;
-#pragma unroll
-        for (int w2 = 0; w2 < TR / 32; ++w2) tsum = __dadd_rn(tsum, red[w2]);
-        tot[q] = tsum;
-    }
-    if (tid != 0) return;
-    ctl->ticket = 0;
-    if (MODE == FIRST) {
-        expect_out[0] = tot[2];
-        expect_out[1] = tot[3];
-        expect_out[2] = tot[4];
-    }
-    if (MODE == DEFER) {
-        ctl->pending = 1;
-        ctl->pending_tn2 = tot[0];
-        ctl->deferred += 1;
-        if (order > ctl->order_used) ctl->order_used = order;
-        ctl->last_order = order;
-    } else if (tot_out) {  // sharded: the sums are all-reduced first, taylor_stop_kernel applies the rule
-        tot_out[0] = tot[0];
-        tot_out[1] = tot[1];
-    } else if (MODE == CATCHUP) {
-        taylor_apply_rule(ctl, order - 1, ctl->pending_tn2, tot[2], rtol);  // streak was 0: cannot stop here
-        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
-        ctl->pending = 0;
-    } else {
-        taylor_apply_rule(ctl, order, tot[0], tot[1], rtol);
-    }
-    __threadfence();
+    reduce_and_rule<MODE, K>(acc, red, partials, ctl, order, rtol, tot_out, expect_out);
 }
 
 template <int MODE, int MAXR, bool CODED>
