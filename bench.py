@@ -477,8 +477,14 @@ def main():
         clocks["window"] = ("timed steps + the e2e calls + ~1 s continuation of the same step loop (NVML, 10 ms "
                             "period)")
 
-        iso_ms, iso_nnz, iso_rows = run.bench_taylor(orders=20, flush_l2=True, dt=run_kw["dt"])
-        spmv_ms = run.bench_spmv(reps=20, flush_l2=True)
+        # isolated, L2-flushed launches of the single-order kernel and the plain SpMV (single-GPU spaces only: on a
+        # shard the gathered vector needs its halo)
+        if single:
+            iso_ms, iso_nnz, iso_rows = run.bench_taylor(orders=20, flush_l2=True, dt=run_kw["dt"])
+            spmv_ms = run.bench_spmv(reps=20, flush_l2=True)
+        else:
+            iso_ms = spmv_ms = None
+            iso_nnz, iso_rows = nnz, rows
         roofline = {
             "kernel": "fused Taylor order (taylor_first / taylor_defer / taylor_catchup / taylor_single): y=H_eff x, "
                       "term'=(0,-dt/n) y, |term'|^2; c+=term' and |c|^2 once per PAIR of orders; the first order also "
@@ -502,12 +508,14 @@ def main():
                         "look the double up in a shared-memory table, so they move 6*nnz instead of SURVEY 8d's "
                         "12*nnz; `frac` above keeps SURVEY's algorithmic bytes (the contract's definition), this is "
                         "the fraction of the copy peak by the bytes actually requested"},
-            "isolated_l2_flushed": {"ms": iso_ms, "rows": iso_rows, "nnz": iso_nnz,
+            "isolated_l2_flushed": None if iso_ms is None else {
+                                    "ms": iso_ms, "rows": iso_rows, "nnz": iso_nnz,
                                     "GB/s": (12.0 * iso_nnz + 72.0 * iso_rows) / (iso_ms * 1e-3) / 1e9,
                                     "note": "single-order kernel alone, after the clock continuation (later state); "
                                             "GB/s by SURVEY's 12*nnz + 72*rows"},
-            "plain_spmv_l2_flushed": {"ms": spmv_ms, "GB/s": (12.0 * iso_nnz + 40.0 * iso_rows) / (spmv_ms * 1e-3) / 1e9,
-                                      "nnz_per_s": iso_nnz / (spmv_ms * 1e-3)},
+            "plain_spmv_l2_flushed": None if spmv_ms is None else {
+                "ms": spmv_ms, "GB/s": (12.0 * iso_nnz + 40.0 * iso_rows) / (spmv_ms * 1e-3) / 1e9,
+                "nnz_per_s": iso_nnz / (spmv_ms * 1e-3)},
             "share_of_step": times["expmv_ms"] / max(times["total_ms"], 1e-9),
         }
         roofline_step = {

@@ -807,6 +807,7 @@ int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush, double dt, double*
                        uint64_t* rows) {
     return guarded(ctx, [&](Engine& e) {
         need(e.has_state && orders > 0, "bench_taylor: no resident state");
+        need(!e.sharded, "bench_taylor: single-GPU spaces only (a shard's gathers need the halo)");
         const Space& sp = e.space[e.cur];
         const uint32_t n = sp.n;
         Engine::Ctl* c = e.dctl();
@@ -843,6 +844,7 @@ int pb200_bench_taylor(pb200_ctx* ctx, int orders, int flush, double dt, double*
 int pb200_bench_spmv(pb200_ctx* ctx, int reps, int flush, double* ms_per_spmv) {
     return guarded(ctx, [&](Engine& e) {
         need(e.has_state && reps > 0, "bench_spmv: no resident state");
+        need(!e.sharded, "bench_spmv: single-GPU spaces only (a shard's gathers need the halo)");
         const Space& sp = e.space[e.cur];
         const uint32_t n = sp.n;
         e.aux_coeff.ensure(size_t(n) * 16 + 16);
