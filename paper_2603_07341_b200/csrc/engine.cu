@@ -61,7 +61,13 @@ Engine::Engine(int dev) : device(dev) {
     for (auto& x : ev) PB_CUDA(cudaEventCreate(&x));
     PB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PB_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
-    PB_CUDA(cudaStreamCreateWithFlags(&halo_stream, cudaStreamNonBlocking));
+    {
+        // highest priority: the transport's kernels of a halo exchange must get SM slots beside the Taylor launch that
+        // is meant to hide them, not behind it
+        int prio_lo = 0, prio_hi = 0;
+        PB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        PB_CUDA(cudaStreamCreateWithPriority(&halo_stream, cudaStreamNonBlocking, prio_hi));
+    }
     PB_CUDA(cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_words, cudaEventDisableTiming));
@@ -1049,12 +1055,23 @@ void Engine::run_step(pb200_diag* out) {
         coeff[ccur ^ 1].ensure(size_t(next.n) * 16 + 16);
         double2* psi = coeff[ccur ^ 1].as<double2>();
         double e = 0, n2 = 0;
+        bool shard_fused = false;
         if (defer_reads) {
             // the incremental path already produced psi and the discarded weight (Ctl::out[0])
             if (!incremental)
                 remap_async(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
             PB_CUDA(cudaEventRecord(ev[4], stream));
             PB_CUDA(cudaEventRecord(ev[5], stream));  // <H> is produced by the first Taylor order
+        } else if (sharded && shard_tiles(next)) {
+            // shards on the tile kernels: the coefficients are remapped straight into the first Taylor order's input,
+            // which also yields <H>, the norm and the finiteness check (no separate SpMV + halo exchange for <H>, no
+            // copy of the state)
+            shard_fused = true;
+            term[0].ensure((size_t(next.n) + next.halo_n) * 16 + 16);
+            rec.discarded_weight = remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n,
+                                         term[0].as<double2>());
+            PB_CUDA(cudaEventRecord(ev[4], stream));
+            PB_CUDA(cudaEventRecord(ev[5], stream));
         } else {
             rec.discarded_weight =
                 remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
@@ -1065,7 +1082,8 @@ void Engine::run_step(pb200_diag* out) {
         int order = 0;
         double ltn = 0, lcn = 0;
         if (sharded) {
-            expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn);
+            expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, shard_fused,
+                          shard_fused ? &e : nullptr, shard_fused ? &n2 : nullptr);
         } else {
             try {
                 expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, true, incremental);

@@ -17,6 +17,7 @@
 #include "window.cuh"
 #include "incremental.cuh"
 #include "sharded.cuh"
+#include "taylor.cuh"
 #include "nccl_comm.hpp"
 
 namespace pb {
@@ -136,8 +137,10 @@ struct Space {
     std::vector<uint64_t> halo_send, halo_recv;  // per-peer element counts
     uint64_t n_global = 0, nnz_global = 0;
     // rows without / with halo columns (sharded SpMV: the former run while the halo is in flight)
+    // (row-list form only -- row_lists; the tile kernels decide per row from the columns)
     uint32_t n_interior = 0, n_boundary = 0;
     DevBuf rows_int, rows_bnd;
+    bool row_lists = false;
 };
 
 struct Engine {
@@ -253,8 +256,13 @@ struct Engine {
     void assemble_sharded(Space& sp);
     uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
                             double* norm2_out);
+    /// fuse_first (tile kernels only): the first order also yields <x|H|x>, |x|^2 and the non-finite count of the input
+    /// state (*exp_out, *norm2_out; a non-finite coefficient throws) and takes that state from term[0], writing c only
     void expmv_sharded(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps,
-                       int* order_used, double* last_term_norm, double* last_c_norm);
+                       int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_first = false,
+                       double* exp_out = nullptr, double* norm2_out = nullptr);
+    /// the sharded Taylor orders of sp run on the tile kernels (else: row lists)
+    bool shard_tiles(const Space& sp) const { return taylor_tiles_usable(sp.max_row) && !sp.row_lists; }
 
     // ---- helpers
     int grid_for(uint64_t n) const {
@@ -320,6 +328,9 @@ struct Engine {
         uint32_t n_new; // unique new keys of the last merge (read together with the expansion counters)
         uint32_t code_fail;  // encode_csr_kernel met a value outside the model's table
         uint32_t pad2[1];
+        // sharded Taylor orders: [0..3] / [4..7] deposits of the two launches of an order (rows without / with halo
+        // columns), [8..10] / [11..13] the first order's <x|H|x>, |x|^2, #non-finite; all-reduced in place
+        double tsum[16];
     };
     /// Snapshot of the control block taken by the last read-back of expmv(): the step's deferred scalars
     /// (discarded weight, <H>, norm, nnz) ride along instead of costing a stream synchronisation each.

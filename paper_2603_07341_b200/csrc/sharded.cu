@@ -129,6 +129,7 @@ void Engine::classify_rows(Space& sp) {
     const uint32_t nb = read_back<uint32_t>(scan_aligned.as<uint32_t>() + n);
     sp.n_boundary = nb;
     sp.n_interior = n - nb;
+    sp.row_lists = true;
     sp.rows_int.ensure(size_t(sp.n_interior) * 4 + 4);
     sp.rows_bnd.ensure(size_t(nb) * 4 + 4);
     if (n) {
@@ -327,14 +328,29 @@ void Engine::assemble_sharded(Space& sp) {
     const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
     sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
     sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
-    assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
-                                                                    tmp_cnt.as<uint32_t>(), sp.row_ptr.as<uint32_t>(),
-                                                                    sp.col.as<int32_t>(), sp.val.as<double>());
+    // value codes for the Taylor tile kernels, produced by the compaction itself (no pass of their own)
+    const bool tiles = taylor_tiles_usable(width);
+    const bool want_codes = tiles && use_codes && md.vt_n > 0;
+    uint32_t* fail = &c->code_fail;
+    if (want_codes) {
+        sp.code.ensure(size_t(nnz) * 2 + CSR_PAD);
+        if (!md.vt_diag) sp.diag.ensure(size_t(n) * 8 + CSR_PAD);
+        PB_CUDA(cudaMemsetAsync(fail, 0, 4, stream));
+    }
+    assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(
+        n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(), tmp_cnt.as<uint32_t>(), sp.row_ptr.as<uint32_t>(),
+        sp.col.as<int32_t>(), sp.val.as<double>(), md.vtab, md.vt_n, md.vt_diag,
+        want_codes ? sp.code.as<uint16_t>() : nullptr, sp.diag.as<double>(), fail);
     check_launch();
     sp.nnz = nnz;
     sp.max_row = width;
     sp.has_h = true;
-    classify_rows(sp);
+    sp.val_valid = true;
+    sp.has_code = want_codes && read_back<uint32_t>(fail) == 0;
+    // the tile kernels tell rows without / with halo columns apart themselves; the row-list kernels need the lists
+    sp.n_interior = sp.n_boundary = 0;
+    sp.row_lists = false;
+    if (!tiles) classify_rows(sp);
     uint64_t g[2] = {n, nnz};
     comm_check(ops.allreduce_u64_host(ops.user, g, 2), "allreduce_u64_host");
     sp.n_global = g[0];
@@ -469,7 +485,8 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
 // c alone and its |term|^2 rides on the next order's all-reduce.  Nothing here returns to the host between orders.
 // ------------------------------------------------------------------------------------------------
 void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
-                           int* order_used, double* last_term_norm, double* last_c_norm) {
+                           int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_first, double* exp_out,
+                           double* norm2_out) {
     if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
     if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
     if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
@@ -480,15 +497,26 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
     term[0].ensure(ext);
     term[1].ensure(ext);
     const double dt_sub = dt / substeps;
+    // tile kernels (the single-GPU path's, with a row filter) when the rows are short enough; row lists otherwise
+    const bool tiles = shard_tiles(sp);
+    if (fuse_first && !tiles) throw CudaFail("internal error: fused first order needs the tile kernels");
+    const bool any_halo = sp.halo_n != 0;
+    TaylorCodes codes_tmp{};
+    const TaylorCodes* codes = codes_of(sp, codes_tmp);
+    if (!tiles && !sp.row_lists) throw CudaFail("internal error: sharded space without row lists");
     const int gi = grid_for(sp.n_interior), gb = grid_for(sp.n_boundary);
     const uint32_t* rp = sp.row_ptr.as<uint32_t>();
     const int32_t* cl = sp.col.as<int32_t>();
     const double* vl = sp.val.as<double>();
     double* pt = partials.as<double>();
     TaylorCtl tc{};
+    double exp_sums[4] = {0, 0, 0, -1};
     PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
+    PB_CUDA(cudaMemsetAsync(c->tsum, 0, sizeof(c->tsum), stream));  // a part that never launches deposits nothing
     for (int s = 0; s < substeps; ++s) {
-        PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
+        // (fused first order: the caller left the state in term[0]; the launch writes c_vec, it does not read it)
+        if (!(fuse_first && s == 0))
+            PB_CUDA(cudaMemcpyAsync(term[0].p, c_vec, size_t(n) * 16, cudaMemcpyDeviceToDevice, stream));
         if (s > 0) {
             tc.done = 0;
             tc.streak = 0;
@@ -508,27 +536,54 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
                 double2* tin = term[(order - 1) & 1].as<double2>();
                 double2* tout = term[order & 1].as<double2>();
                 int mode = TAYLOR_ROWS_SINGLE;
-                if (!singles && order >= k0 && ((order - k0) & 1))
+                const bool first = fuse_first && s == 0 && order == 1;
+                if (first)
+                    mode = TAYLOR_ROWS_FIRST;
+                else if (!singles && order >= k0 && ((order - k0) & 1))
                     mode = TAYLOR_ROWS_CATCHUP;
                 else if (!singles && order >= k0 && order < max_order)
                     mode = TAYLOR_ROWS_DEFER;
                 halo_start(sp, tin);
-                taylor_launch_rows(mode, gi, stream, sp.n_interior, sp.rows_int.as<uint32_t>(), rp, cl, vl, tin, tout, c_vec, b,
-                                   order, pt, &c->taylor, c->out);
-                check_launch();
-                halo_wait();
-                taylor_launch_rows(mode, gb, stream, sp.n_boundary, sp.rows_bnd.as<uint32_t>(), rp, cl, vl, tin, tout, c_vec, b,
-                                   order, pt, &c->taylor, c->out + 4);
-                check_launch();
+                if (tiles) {
+                    // part 1 (rows without halo columns) beside the exchange, part 2 once the halo has landed; a rank
+                    // without halo columns runs all its rows in one launch
+                    taylor_launch_tile_shard(mode, any_halo ? 1 : 0, sm_count, stream, n, rp, cl, vl, codes, tin, tout, c_vec,
+                                             b, order, sp.max_row, pt, &c->taylor, c->tsum, c->tsum + 8, first ? 1 : 0);
+                    check_launch();
+                    halo_wait();
+                    if (any_halo) {
+                        taylor_launch_tile_shard(mode, 2, sm_count, stream, n, rp, cl, vl, codes, tin, tout, c_vec, b, order,
+                                                 sp.max_row, pt, &c->taylor, c->tsum + 4, c->tsum + 11, first ? 1 : 0);
+                        check_launch();
+                    }
+                } else {
+                    taylor_launch_rows(mode, gi, stream, sp.n_interior, sp.rows_int.as<uint32_t>(), rp, cl, vl, tin, tout,
+                                       c_vec, b, order, pt, &c->taylor, c->tsum);
+                    check_launch();
+                    halo_wait();
+                    taylor_launch_rows(mode, gb, stream, sp.n_boundary, sp.rows_bnd.as<uint32_t>(), rp, cl, vl, tin, tout,
+                                       c_vec, b, order, pt, &c->taylor, c->tsum + 4);
+                    check_launch();
+                }
                 if (mode == TAYLOR_ROWS_DEFER) continue;  // its |term|^2 rides on the next order's all-reduce
-                comm_check(ops.allreduce_f64_dev(ops.user, c->out, 8, stream), "allreduce_f64_dev");
+                // (the first order's <x|H|x>, |x|^2 and non-finite count ride on its all-reduce)
+                comm_check(ops.allreduce_f64_dev(ops.user, c->tsum, first ? 14 : 8, stream), "allreduce_f64_dev");
                 if (mode == TAYLOR_ROWS_CATCHUP)
-                    taylor_stop_pair_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
+                    taylor_stop_pair_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->tsum, order, rtol);
                 else
-                    taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->out, order, rtol);
+                    taylor_stop_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->tsum, order, rtol);
                 check_launch();
             }
-            tc = read_back<TaylorCtl>(&c->taylor);
+            last_ctl = read_back<Ctl>(c);  // the stop flag and, after the first batch, the fused first order's sums
+            if (fuse_first && s == 0 && exp_sums[3] < 0) {
+                exp_sums[0] = last_ctl.tsum[8] + last_ctl.tsum[11];
+                exp_sums[1] = last_ctl.tsum[9] + last_ctl.tsum[12];
+                exp_sums[2] = last_ctl.tsum[10] + last_ctl.tsum[13];
+                exp_sums[3] = 0;
+                // the reference checks its input before it iterates (propagator.hpp:55-57)
+                if (exp_sums[2] != 0.0) throw PacesError("expmv: non-finite input coefficient");
+            }
+            tc = last_ctl.taylor;
             if (tc.done) {
                 converged = true;
                 break;
@@ -553,6 +608,8 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
     if (order_used) *order_used = tc.order_used;
     if (last_term_norm) *last_term_norm = tc.last_term_norm;
     if (last_c_norm) *last_c_norm = tc.last_c_norm;
+    if (exp_out) *exp_out = exp_sums[0];
+    if (norm2_out) *norm2_out = exp_sums[1];
 }
 
 }  // namespace pb

@@ -219,14 +219,21 @@ static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n,
     }
 }
 
-/// Pass 2 on a shard: compacts the scratch into CSR, skipping absent remote neighbours.
+/// Pass 2 on a shard: compacts the scratch into CSR, skipping absent remote neighbours.  code != nullptr: the value
+/// codes of the Taylor tile kernels are produced on the way (encode_csr_kernel's rule: index of the value in the
+/// model's table; the diagonal entry 0xffff + diag[row] when the diagonals are not tabulated; *fail when a value is
+/// not in the table).
 static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
                                                                       const uint32_t* __restrict__ tmp_col,
                                                                       const double* __restrict__ tmp_val,
                                                                       const uint32_t* __restrict__ tmp_cnt,
                                                                       const uint32_t* __restrict__ row_ptr,
                                                                       int32_t* __restrict__ col,
-                                                                      double* __restrict__ val) {
+                                                                      double* __restrict__ val,
+                                                                      const double* __restrict__ vtab, int vt_n,
+                                                                      int vt_diag, uint16_t* __restrict__ code,
+                                                                      double* __restrict__ diag,
+                                                                      uint32_t* __restrict__ fail) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         uint32_t k = row_ptr[i];
         const uint32_t* tc = tmp_col + size_t(i) * width;
@@ -234,8 +241,22 @@ static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uin
         const uint32_t cnt = tmp_cnt[i];
         for (uint32_t s = 0; s < cnt; ++s) {
             if (tc[s] != COL_ABSENT) {
+                const double v = tv[s];
                 col[k] = int32_t(tc[s]);
-                val[k] = tv[s];
+                val[k] = v;
+                if (code != nullptr) {
+                    if (!vt_diag && tc[s] == i) {
+                        diag[i] = v;
+                        code[k] = uint16_t(0xffffu);
+                    } else {
+                        uint32_t cd = vt_find(vtab, vt_n, v);
+                        if (cd == 0xfffeu) {
+                            *fail = 1u;
+                            cd = 0;
+                        }
+                        code[k] = uint16_t(cd);
+                    }
+                }
                 ++k;
             }
         }

@@ -387,10 +387,10 @@ __device__ __forceinline__ void finish_row(uint32_t i, double ar, double ai, dou
 
 /// Reduction of the consumers' partial sums (fixed tree inside the CTA, per-CTA partials combined by the last CTA in
 /// CTA order) and, in that last CTA, the stop rule of the launch's mode.  Called by the TR consumer threads only.
-template <int MODE, int K>
+template <int MODE, int K, bool SHARD = false>
 __device__ __forceinline__ void reduce_and_rule(double (&acc)[K], double* red, double* __restrict__ partials,
                                                 TaylorCtl* ctl, int order, double rtol, double* __restrict__ tot_out,
-                                                double* __restrict__ expect_out) {
+                                                double* __restrict__ expect_out, int part = 0) {
     const uint32_t tid = threadIdx.x;
     auto consumer_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(TR) : "memory"); };
     const int lane = tid & 31, warp = tid >> 5;
@@ -432,6 +432,28 @@ __device__ __forceinline__ void reduce_and_rule(double (&acc)[K], double* red, d
     }
     if (tid != 0) return;
     ctl->ticket = 0;
+    if (SHARD) {
+        // a shard only deposits the sums of this launch (its part of the rows): they are all-reduced with the other
+        // part's and the other ranks', taylor_stop_kernel / taylor_stop_pair_kernel apply the rule (sharded.cuh).
+        // A deferred order's |term|^2 waits in slot 3 for the catch-up order's all-reduce.
+        if (MODE == DEFER) {
+            tot_out[3] = tot[0];
+        } else {
+            tot_out[0] = tot[0];
+            tot_out[1] = tot[1];
+            if (MODE == CATCHUP) tot_out[2] = tot[2];
+        }
+        if (MODE == FIRST) {  // <x|H|x>, |x|^2, #non-finite of this part's rows
+            expect_out[0] = tot[2];
+            expect_out[1] = tot[3];
+            expect_out[2] = tot[4];
+            if (part == 0) expect_out[3] = expect_out[4] = expect_out[5] = 0.0;
+        }
+        // one launch for all rows: the other part's slots hold the previous all-reduce's sums (it works in place)
+        if (part == 0) tot_out[4] = tot_out[5] = tot_out[6] = tot_out[7] = 0.0;
+        __threadfence();
+        return;
+    }
     if (MODE == FIRST) {
         expect_out[0] = tot[2];
         expect_out[1] = tot[3];
@@ -494,7 +516,11 @@ constexpr int tile_ctas_per_sm() {
     return MAXR <= 5 ? TILE_NARROW_CTAS : TILE_WIDE_CTAS;
 }
 
-template <int MODE, int MAXR, bool CODED>
+/// SHARD (a rank's rows of a sharded space, columns >= n index the halo): `part` selects the rows of this launch -- 1:
+/// rows WITHOUT halo columns (they run while the halo exchange is in flight), 2: rows WITH halo columns (after it has
+/// landed), 0: all rows -- decided per row from the columns already in shared memory; the partial sums are deposited in
+/// tot_out[0..3] for the all-reduce instead of applying the stop rule here.
+template <int MODE, int MAXR, bool CODED, bool SHARD = false>
 __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_tile_kernel(uint32_t n, const uint32_t* __restrict__ row_ptr,
                                                                const int32_t* __restrict__ col,
                                                                const double* __restrict__ val,
@@ -506,7 +532,8 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                                                                double b, int order, double rtol, int max_row,
                                                                double* __restrict__ partials, TaylorCtl* ctl,
                                                                int ignore_stop, double* __restrict__ tot_out,
-                                                               double* __restrict__ expect_out, int first_from_x) {
+                                                               double* __restrict__ expect_out, int first_from_x,
+                                                               int part) {
     constexpr bool HAS_C = MODE != DEFER;
     constexpr int K = mode_sums<MODE>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -592,41 +619,59 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         // independent of the ring: this row's slice of c and (catch-up / first order) of the previous term
         double2 cc = make_double2(0.0, 0.0), tp = make_double2(0.0, 0.0);
         // (first_from_x: the state is only in term_in so far -- the first order writes c, it does not read it)
-        if (HAS_C && live && !(MODE == FIRST && first_from_x)) cc = c[i];
-        if ((MODE == CATCHUP || MODE == FIRST) && live) tp = __ldg(term_in + i);
-        if (MODE == FIRST && first_from_x) cc = tp;
+        // (SHARD: only once the row is known to belong to this launch's part, with the gathers)
+        if (!SHARD) {
+            if (HAS_C && live && !(MODE == FIRST && first_from_x)) cc = c[i];
+            if ((MODE == CATCHUP || MODE == FIRST) && live) tp = __ldg(term_in + i);
+            if (MODE == FIRST && first_from_x) cc = tp;
+        }
         double dg = 0.0;  // the row's diagonal element when the model's diagonals are not in the table
         if (CODED && diag != nullptr && live) dg = __ldg(diag + i);
         mbar_wait(full + s, (j / STAGES) & 1);
         double ar = 0.0, ai = 0.0;
+        bool mine = live;
         if (live) {
             const uint32_t base = rp_s[0] & ~AL;  // the slices start at the 16-byte boundary below the first entry
             const uint32_t kb = rp_s[tid] - base;
             const uint32_t len = rp_s[tid + 1] - base - kb;
-            double2 x[MAXR];
+            if (SHARD && part != 0) {
+                bool halo = false;
 #pragma unroll
-            for (int u = 0; u < MAXR; ++u)
-                if (uint32_t(u) < len) x[u] = __ldg(term_in + col_s[kb + u]);
+                for (int u = 0; u < MAXR; ++u)
+                    if (uint32_t(u) < len) halo |= uint32_t(col_s[kb + u]) >= n;
+                mine = halo == (part == 2);
+            }
+            if (mine) {
+                double2 x[MAXR];
 #pragma unroll
-            for (int u = 0; u < MAXR; ++u)
-                if (uint32_t(u) < len) {
-                    double v;
-                    if (CODED) {
-                        const uint32_t cd = code_s[kb + u];
-                        v = cd == CODE_DIAG ? dg : vt_s[cd];
-                    } else {
-                        v = val_s[kb + u];
-                    }
-                    ar = __dadd_rn(ar, __dmul_rn(v, x[u].x));
-                    ai = __dadd_rn(ai, __dmul_rn(v, x[u].y));
+                for (int u = 0; u < MAXR; ++u)
+                    if (uint32_t(u) < len) x[u] = __ldg(term_in + col_s[kb + u]);
+                if (SHARD) {
+                    if (HAS_C && !(MODE == FIRST && first_from_x)) cc = c[i];
+                    if (MODE == CATCHUP || MODE == FIRST) tp = __ldg(term_in + i);
+                    if (MODE == FIRST && first_from_x) cc = tp;
                 }
+#pragma unroll
+                for (int u = 0; u < MAXR; ++u)
+                    if (uint32_t(u) < len) {
+                        double v;
+                        if (CODED) {
+                            const uint32_t cd = code_s[kb + u];
+                            v = cd == CODE_DIAG ? dg : vt_s[cd];
+                        } else {
+                            v = val_s[kb + u];
+                        }
+                        ar = __dadd_rn(ar, __dmul_rn(v, x[u].x));
+                        ai = __dadd_rn(ai, __dmul_rn(v, x[u].y));
+                    }
+            }
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(empty + s);  // this warp has read everything it needs from the stage
-        if (live) finish_row<MODE>(i, ar, ai, cc, tp, b, term_out, c, acc);
+        if (mine) finish_row<MODE>(i, ar, ai, cc, tp, b, term_out, c, acc);
     }
 
-    reduce_and_rule<MODE, K>(acc, red, partials, ctl, order, rtol, tot_out, expect_out);
+    reduce_and_rule<MODE, K, SHARD>(acc, red, partials, ctl, order, rtol, tot_out, expect_out, part);
 }
 
 template <int MODE, int MAXR, bool CODED>
@@ -658,7 +703,7 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
     taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
-        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
+        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0);
     return true;
 }
 
@@ -689,6 +734,61 @@ static bool launch(int sm_count, cudaStream_t stream, uint32_t n, const uint32_t
                                     max_row, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
     return launch_c<MODE, false>(sm_count, stream, n, row_ptr, col, val, nullptr, term_in, term_out, c, b, order, rtol,
                                  max_row, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x);
+}
+
+// ---- shards: the same kernels with the row filter; two waves of CTAs instead of a persistent grid, so that CTAs retire
+// while the launch runs and the transport's kernels (halo exchange on its own, higher-priority stream) find room
+constexpr int SHARD_WAVES = 2;
+template <int MODE, int MAXR, bool CODED>
+static bool launch_shard_r(int part, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                           const int32_t* col, const double* val, const TaylorCodes* codes, const double2* term_in,
+                           double2* term_out, double2* c, double b, int order, double* partials, TaylorCtl* ctl,
+                           double* tot_out, double* expect_out, int first_from_x) {
+    const int vt_n = CODED ? codes->vt_n : 0;
+    const Layout L = make_layout<CODED>(MAXR, vt_n);
+    static int ready = 0;
+    static uint32_t smem_set = 0;
+    if (ready == 0 || (ready > 0 && L.total > smem_set)) {
+        ready = -1;
+        int occ = 0;
+        if (cudaFuncSetAttribute(taylor_tile_kernel<MODE, MAXR, CODED, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(L.total)) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, taylor_tile_kernel<MODE, MAXR, CODED, true>, NTHREADS,
+                                                          L.total) == cudaSuccess &&
+            occ >= 1) {
+            ready = 1;
+            smem_set = L.total;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    if (ready < 0) return false;
+    const uint32_t ntiles = (n + TR - 1) / TR;
+    const uint32_t grid = std::max<uint32_t>(
+        1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>()) * SHARD_WAVES));
+    taylor_tile_kernel<MODE, MAXR, CODED, true><<<grid, NTHREADS, L.total, stream>>>(
+        n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
+        vt_n, term_in, term_out, c, b, order, 0.0, MAXR, partials, ctl, 0, tot_out, expect_out, first_from_x, part);
+    return true;
+}
+template <int MODE>
+static bool launch_shard(int part, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                         const int32_t* col, const double* val, const TaylorCodes* codes, const double2* term_in,
+                         double2* term_out, double2* c, double b, int order, int max_row, double* partials,
+                         TaylorCtl* ctl, double* tot_out, double* expect_out = nullptr, int first_from_x = 0) {
+#define PB_SHARD_ARGS \
+    part, sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b, order, partials, ctl, tot_out, expect_out, \
+        first_from_x
+    if (codes != nullptr && codes->code != nullptr && codes->vt_n > 0 && codes->vt_n <= TAYLOR_VT_MAX) {
+        if (max_row <= 5) return launch_shard_r<MODE, 5, true>(PB_SHARD_ARGS);
+        if (max_row <= 7) return launch_shard_r<MODE, 7, true>(PB_SHARD_ARGS);
+        return launch_shard_r<MODE, 9, true>(PB_SHARD_ARGS);
+    }
+    if (val == nullptr) return false;
+    if (max_row <= 5) return launch_shard_r<MODE, 5, false>(PB_SHARD_ARGS);
+    if (max_row <= 7) return launch_shard_r<MODE, 7, false>(PB_SHARD_ARGS);
+    return launch_shard_r<MODE, 9, false>(PB_SHARD_ARGS);
+#undef PB_SHARD_ARGS
 }
 
 }  // namespace tile
@@ -774,6 +874,26 @@ void taylor_launch_rows(int mode, int grid, cudaStream_t stream, uint32_t nrows,
     else
         taylor_rows_kernel<tile::SINGLE><<<grid, NT, 0, stream>>>(nrows, rows, row_ptr, col, val, term_in, term_out, c, b,
                                                                  order, partials, ctl, tot_out);
+}
+
+bool taylor_tiles_usable(int max_row) { return g_use_tiles && max_row >= 1 && max_row <= 9; }
+
+bool taylor_launch_tile_shard(int mode, int part, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                              const int32_t* col, const double* val, const TaylorCodes* codes, const double2* term_in,
+                              double2* term_out, double2* c, double b, int order, int max_row, double* partials,
+                              TaylorCtl* ctl, double* tot_out, double* expect_out, int first_from_x) {
+    if (!taylor_tiles_usable(max_row)) return false;
+    if (mode == tile::DEFER)
+        return tile::launch_shard<tile::DEFER>(part, sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, nullptr,
+                                               b, order, max_row, partials, ctl, tot_out);
+    if (mode == tile::CATCHUP)
+        return tile::launch_shard<tile::CATCHUP>(part, sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b,
+                                                 order, max_row, partials, ctl, tot_out);
+    if (mode == tile::FIRST)
+        return tile::launch_shard<tile::FIRST>(part, sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b,
+                                               order, max_row, partials, ctl, tot_out, expect_out, first_from_x);
+    return tile::launch_shard<tile::SINGLE>(part, sm_count, stream, n, row_ptr, col, val, codes, term_in, term_out, c, b,
+                                            order, max_row, partials, ctl, tot_out);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -67,4 +67,17 @@ void taylor_launch_rows(int mode, int grid, cudaStream_t stream, uint32_t nrows,
                         double2* term_out, double2* c, double b, int order, double* partials, TaylorCtl* ctl,
                         double* tot_out);
 
+
+/// Sharded SpMV, tile form (the kernels of the single-GPU path with a row filter): part 1 = the rows without halo
+/// columns, 2 = the rows with halo columns, 0 = all rows; modes and deposits as taylor_launch_rows, plus mode 1 = FIRST
+/// (the first order of a step: <x|H|x>, |x|^2 and the non-finite count of the part's rows go to expect_out[0..2], and
+/// with first_from_x the input vector doubles as the old c).  Returns false when the tile kernels cannot take the
+/// matrix (row-length bound unknown or > 9): the caller uses the row lists.
+constexpr int TAYLOR_ROWS_FIRST = 1;
+bool taylor_tiles_usable(int max_row);
+bool taylor_launch_tile_shard(int mode, int part, int sm_count, cudaStream_t stream, uint32_t n, const uint32_t* row_ptr,
+                              const int32_t* col, const double* val, const TaylorCodes* codes, const double2* term_in,
+                              double2* term_out, double2* c, double b, int order, int max_row, double* partials,
+                              TaylorCtl* ctl, double* tot_out, double* expect_out = nullptr, int first_from_x = 0);
+
 }  // namespace pb
