@@ -242,10 +242,16 @@ struct Engine {
         comm_check(ops.allreduce_u64_host(ops.user, &v, 1), "allreduce_u64_host");
         return v;
     }
-    /// dest[] -> bucketed positions; returns per-destination counts in h_send
-    void route(const uint32_t* dest, uint32_t cnt, uint32_t* pos);
-    /// exchanges h_send -> h_recv and the bucketed device buffer; returns total received elements
-    uint64_t exchange(const void* send, void* recv_buf_owner, DevBuf& recv, uint64_t elem_bytes);
+    /// Routed exchange, device-side sizes.  route_async enqueues the bucketing of dest[0 .. *cnt_ptr) (a counter inside
+    /// the route block's ShardCounters, clamped to cnt_bound) and the all-to-all of the per-peer counts; nothing returns
+    /// to the host.  The caller scatters its payload by pos[] (same device count), then route_finish() is the ONE
+    /// read-back of the exchange: shard counters + per-peer send / receive counts (-> h_send, h_recv), and
+    /// exchange_known() moves the payload.  No blocking host collective, no stream synchronisation in between.
+    RouteBlock* route_block();
+    void route_async(const uint32_t* dest, const uint32_t* cnt_ptr, uint32_t cnt_bound, uint32_t* pos);
+    ShardCounters route_finish();
+    /// all-to-all-v of a bucketed device buffer with the per-peer counts in h_send / h_recv; returns the elements received
+    uint64_t exchange_known(const void* send, DevBuf& recv, uint64_t elem_bytes);
     void halo_exchange(const Space& sp, double2* x);
     /// pack on the context's stream, exchange on the halo stream (when the transport has an independent channel);
     /// halo_wait() makes the context's stream wait for the arrival

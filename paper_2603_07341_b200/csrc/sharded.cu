@@ -41,38 +41,44 @@ namespace pb {
 // ------------------------------------------------------------------------------------------------
 // routing helpers
 // ------------------------------------------------------------------------------------------------
-void Engine::route(const uint32_t* dest, uint32_t cnt, uint32_t* pos) {
-    const uint32_t P = uint32_t(world);
-    route_ctr.ensure(3 * 64 * 4);
-    uint32_t* counts = route_ctr.as<uint32_t>();
-    uint32_t* displ = counts + 64;
-    uint32_t* fill = counts + 128;
-    PB_CUDA(cudaMemsetAsync(counts, 0, 3 * 64 * 4, stream));
-    route_count_kernel<<<grid_for(cnt), NT, 0, stream>>>(dest, cnt, P, counts);
-    check_launch();
-    PB_CUDA(cudaMemcpyAsync(pinned, counts, P * 4, cudaMemcpyDeviceToHost, stream));
-    sync();
-    h_send.assign(P, 0);
-    uint32_t hd[64];
-    uint32_t acc = 0;
-    for (uint32_t p = 0; p < P; ++p) {
-        h_send[p] = static_cast<uint32_t*>(pinned)[p];
-        hd[p] = acc;
-        acc += uint32_t(h_send[p]);
-    }
-    std::memcpy(pinned, hd, P * 4);
-    PB_CUDA(cudaMemcpyAsync(displ, pinned, P * 4, cudaMemcpyHostToDevice, stream));
-    route_place_kernel<<<grid_for(cnt), NT, 0, stream>>>(dest, cnt, displ, fill, pos);
-    check_launch();
-    sync();  // pinned is reused by the next read-back
+RouteBlock* Engine::route_block() {
+    route_ctr.ensure(sizeof(RouteBlock));
+    return route_ctr.as<RouteBlock>();
 }
 
-uint64_t Engine::exchange(const void* send, void*, DevBuf& recv, uint64_t elem_bytes) {
+void Engine::route_async(const uint32_t* dest, const uint32_t* cnt_ptr, uint32_t cnt_bound, uint32_t* pos) {
     const uint32_t P = uint32_t(world);
+    RouteBlock* rb = route_block();
+    PB_CUDA(cudaMemsetAsync(rb->fill, 0, sizeof(rb->fill) + sizeof(rb->displ), stream));
+    PB_CUDA(cudaMemsetAsync(rb->counts, 0, sizeof(rb->counts) + sizeof(rb->rcounts), stream));
+    const int g = grid_for(cnt_bound);
+    route_count_kernel<<<g, NT, 0, stream>>>(dest, cnt_ptr, cnt_bound, P, rb->counts);
+    check_launch();
+    route_scan_kernel<<<1, 32, 0, stream>>>(rb->counts, P, rb->displ);
+    check_launch();
+    route_place_kernel<<<g, NT, 0, stream>>>(dest, cnt_ptr, cnt_bound, rb->displ, rb->fill, pos);
+    check_launch();
+    // every peer learns how much it will receive: one u32 per pair, on the device
+    std::vector<uint64_t> ones(P, 1);
+    comm_check(ops.alltoallv_dev(ops.user, rb->counts, ones.data(), rb->rcounts, ones.data(), 4, stream),
+               "alltoallv_dev(counts)");
+}
+
+ShardCounters Engine::route_finish() {
+    const uint32_t P = uint32_t(world);
+    const RouteInfo info = read_back<RouteInfo>(&route_block()->sc);
+    h_send.assign(P, 0);
     h_recv.assign(P, 0);
-    comm_check(ops.alltoall_u64_host(ops.user, h_send.data(), h_recv.data()), "alltoall_u64_host");
+    for (uint32_t p = 0; p < P; ++p) {
+        h_send[p] = info.counts[p];
+        h_recv[p] = info.rcounts[p];
+    }
+    return info.sc;
+}
+
+uint64_t Engine::exchange_known(const void* send, DevBuf& recv, uint64_t elem_bytes) {
     uint64_t total = 0;
-    for (uint32_t p = 0; p < P; ++p) total += h_recv[p];
+    for (uint64_t v : h_recv) total += v;
     recv.ensure(total * elem_bytes + 16);
     comm_check(ops.alltoallv_dev(ops.user, send, h_send.data(), recv.p, h_recv.data(), elem_bytes, stream),
                "alltoallv_dev");
@@ -156,8 +162,7 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
     bool identity_frontier = true;
     int fcur = 0;
     Ctl* c = dctl();
-    route_ctr.ensure(3 * 64 * 4 + sizeof(ShardCounters));
-    ShardCounters* dsc = reinterpret_cast<ShardCounters*>(route_ctr.as<uint32_t>() + 3 * 64);
+    ShardCounters* dsc = &route_block()->sc;
 
     for (int k = 0; k < order; ++k) {
         if (allreduce_host_u64(nf) == 0) break;  // every frontier is empty: the ball is complete
@@ -169,6 +174,7 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
         out_keys.ensure(size_t(cap) * W * 4);
         out_dest.ensure(size_t(cap) * 4);
         route_pos.ensure(size_t(cap) * 4);
+        sendbuf.ensure(size_t(cap) * W * 4 + 16);
         gap.ensure((size_t(n) + 2) * 4);
         PB_CUDA(cudaMemsetAsync(gap.p, 0, (size_t(n) + 2) * 4, stream));
         PB_CUDA(cudaMemsetAsync(&c->grow, 0, sizeof(GrowCounters), stream));
@@ -182,32 +188,32 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
                                   out_keys.as<uint32_t>(), out_dest.as<uint32_t>(), cap, dsc));
             check_launch();
         }
-        const ShardCounters hsc = read_back<ShardCounters>(dsc);
-        GrowCounters gc = read_back<GrowCounters>(&c->grow);
-        if (gc.overflow || hsc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
-        // ship the keys owned by other ranks
-        route(out_dest.as<uint32_t>(), hsc.n_out, route_pos.as<uint32_t>());
-        sendbuf.ensure(size_t(hsc.n_out) * W * 4 + 16);
-        if (hsc.n_out) {
-            PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(hsc.n_out), NT, 0, stream>>>(
-                                  out_keys.as<uint32_t>(), route_pos.as<uint32_t>(), hsc.n_out, sendbuf.as<uint32_t>()));
-            check_launch();
-        }
-        const uint64_t nr = exchange(sendbuf.p, nullptr, recvbuf, uint64_t(W) * 4);
+        // ship the keys owned by other ranks: bucketing, payload scatter and the exchange of the per-peer counts are
+        // enqueued against the device-side count; ONE read-back then tells the host what to send and what arrives
+        route_async(out_dest.as<uint32_t>(), &dsc->n_out, cap, route_pos.as<uint32_t>());
+        PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(cap), NT, 0, stream>>>(
+                              out_keys.as<uint32_t>(), route_pos.as<uint32_t>(), &dsc->n_out, cap, sendbuf.as<uint32_t>()));
+        check_launch();
+        const ShardCounters hsc = route_finish();
+        if (hsc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
+        const uint64_t nr = exchange_known(sendbuf.p, recvbuf, uint64_t(W) * 4);
         if (nr) {
-            const uint64_t need = uint64_t(gc.n_cand) + nr;
+            // the local candidates (at most cap - 1 of them, their count is still on the device) keep their places
+            const uint64_t need = uint64_t(cap) + nr;
             if (need > 0x7ffffff0ull) throw PacesError("subspace growth: candidate count exceeds 32-bit indexing");
-            sync();
-            cand_keys.ensure_keep(size_t(need) * W * 4, size_t(gc.n_cand) * W * 4);
-            cand_gap.ensure_keep(size_t(need) * 4, size_t(gc.n_cand) * 4);
+            if (size_t(need) * W * 4 > cand_keys.cap || size_t(need) * 4 > cand_gap.cap) {
+                sync();
+                cand_keys.ensure_keep(size_t(need) * W * 4, size_t(cap) * W * 4);
+                cand_gap.ensure_keep(size_t(need) * 4, size_t(cap) * 4);
+            }
             PB_DISPATCH_WS(W, classify_received_kernel<W><<<grid_for(nr), NT, 0, stream>>>(
                                   out.words.as<uint32_t>(), n, recvbuf.as<uint32_t>(), uint32_t(nr),
                                   cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), uint32_t(need), gap.as<uint32_t>(),
                                   &c->grow));
             check_launch();
-            gc = read_back<GrowCounters>(&c->grow);
-            if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow while classifying received keys");
         }
+        const GrowCounters gc = read_back<GrowCounters>(&c->grow);
+        if (gc.overflow) throw CudaFail("internal error: candidate buffer overflow during expansion");
         const uint32_t nc = gc.n_cand;
         uint32_t n_new = 0;
         if (nc) n_new = merge_level(out, n, nc, fcur);
@@ -245,8 +251,8 @@ void Engine::assemble_sharded(Space& sp) {
     req_keys.ensure(size_t(req_cap) * W * 4);
     req_dest.ensure(size_t(req_cap) * 4);
     req_pos.ensure(size_t(req_cap) * 4);
-    route_ctr.ensure(3 * 64 * 4 + sizeof(ShardCounters));
-    ShardCounters* dsc = reinterpret_cast<ShardCounters*>(route_ctr.as<uint32_t>() + 3 * 64);
+    sendbuf.ensure(size_t(req_cap) * W * 4 + 16);
+    ShardCounters* dsc = &route_block()->sc;
     PB_CUDA(cudaMemsetAsync(dsc, 0, sizeof(ShardCounters), stream));
     const uint32_t achunk = chunk_for(n);
     if (n) {
@@ -256,21 +262,17 @@ void Engine::assemble_sharded(Space& sp) {
                               req_dest.as<uint32_t>(), req_cap, dsc));
         check_launch();
     }
-    const ShardCounters hsc = read_back<ShardCounters>(dsc);
+    // requests -> owners (device-side count; one read-back for the counters and both count vectors)
+    route_async(req_dest.as<uint32_t>(), &dsc->n_req, req_cap, req_pos.as<uint32_t>());
+    PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(req_cap), NT, 0, stream>>>(
+                          req_keys.as<uint32_t>(), req_pos.as<uint32_t>(), &dsc->n_req, req_cap, sendbuf.as<uint32_t>()));
+    check_launch();
+    const ShardCounters hsc = route_finish();
     if (hsc.overflow) throw CudaFail("internal error: request buffer overflow during assembly");
     const uint32_t nreq = hsc.n_req;
-
-    // requests -> owners
-    route(req_dest.as<uint32_t>(), nreq, req_pos.as<uint32_t>());
     const std::vector<uint64_t> req_send = h_send;  // requests I send per peer
-    sendbuf.ensure(size_t(nreq) * W * 4 + 16);
-    if (nreq) {
-        PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(nreq), NT, 0, stream>>>(
-                              req_keys.as<uint32_t>(), req_pos.as<uint32_t>(), nreq, sendbuf.as<uint32_t>()));
-        check_launch();
-    }
-    const uint64_t nr = exchange(sendbuf.p, nullptr, recvbuf, uint64_t(W) * 4);
     const std::vector<uint64_t> req_recv = h_recv;  // requests I answer per peer
+    const uint64_t nr = exchange_known(sendbuf.p, recvbuf, uint64_t(W) * 4);
 
     // owner side: answers + the list of local rows to pack for every later SpMV
     answer.ensure(size_t(nr) * 4 + 4);
@@ -300,7 +302,8 @@ void Engine::assemble_sharded(Space& sp) {
 
     // replies -> requesters (same buckets, reversed roles)
     h_send = req_recv;
-    const uint64_t nrep = exchange(answer.p, nullptr, reply, 4);
+    h_recv = req_send;  // one reply per request: the counts are known on both sides
+    const uint64_t nrep = exchange_known(answer.p, reply, 4);
     if (nrep != nreq) throw CudaFail("internal error: look-up replies do not match the requests");
     halo_flag.ensure((size_t(nreq) + 1) * 4);
     reply_flags_kernel<<<grid_for(nreq), NT, 0, stream>>>(reply.as<uint32_t>(), nreq, halo_flag.as<uint32_t>());
@@ -319,9 +322,10 @@ void Engine::assemble_sharded(Space& sp) {
         sp.halo_n = pin[P];
     }
     if (uint64_t(n) + sp.halo_n > 0x7fffffffull) throw PacesError("assembly: local rows + halo exceed int32 columns");
-    resolve_requests_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_cnt.as<uint32_t>(),
-                                                            req_pos.as<uint32_t>(), reply.as<uint32_t>(),
-                                                            halo_flag.as<uint32_t>(), sp.row_ptr.as<uint32_t>());
+    resolve_requests_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
+                                                            tmp_cnt.as<uint32_t>(), req_pos.as<uint32_t>(),
+                                                            reply.as<uint32_t>(), halo_flag.as<uint32_t>(),
+                                                            sp.row_ptr.as<uint32_t>());
     check_launch();
     PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
     exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
@@ -338,8 +342,8 @@ void Engine::assemble_sharded(Space& sp) {
         PB_CUDA(cudaMemsetAsync(fail, 0, 4, stream));
     }
     assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(
-        n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(), tmp_cnt.as<uint32_t>(), sp.row_ptr.as<uint32_t>(),
-        sp.col.as<int32_t>(), sp.val.as<double>(), md.vtab, md.vt_n, md.vt_diag,
+        n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(), sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
+        sp.val.as<double>(), md.vtab, md.vt_n, md.vt_diag,
         want_codes ? sp.code.as<uint16_t>() : nullptr, sp.diag.as<double>(), fail);
     check_launch();
     sp.nnz = nnz;

@@ -62,10 +62,31 @@ static __global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
     }
 }
 
+/// Routing scratch on the device (Engine::route_ctr): everything a routed exchange needs stays here until ONE read-back
+/// brings the shard counters and both count vectors to the host together.
+struct RouteBlock {
+    uint32_t fill[64];     // arrival counters of route_place_kernel
+    uint32_t displ[64];    // exclusive scan of counts
+    ShardCounters sc;      // counters of the kernel that produced the routed list
+    uint32_t counts[64];   // elements this rank sends to each peer
+    uint32_t rcounts[64];  // elements each peer sends to this rank (all-to-all of counts, on the device)
+};
+/// what comes back to the host (the tail of RouteBlock)
+struct RouteInfo {
+    ShardCounters sc;
+    uint32_t counts[64];
+    uint32_t rcounts[64];
+};
+
+/// The length of a routed list lives on the device (a counter of the kernel that produced it), clamped to the buffer.
+__device__ __forceinline__ uint32_t routed_count(const uint32_t* cnt_ptr, uint32_t cap) { return min(__ldg(cnt_ptr), cap); }
+
 /// counts[dest[i]]++ (P is tiny: shared-memory histogram per CTA).
-static __global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restrict__ dest, uint32_t cnt, uint32_t P,
+static __global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* __restrict__ dest,
+                                                         const uint32_t* __restrict__ cnt_ptr, uint32_t cap, uint32_t P,
                                                          uint32_t* __restrict__ counts) {
     __shared__ uint32_t sh[64];
+    const uint32_t cnt = routed_count(cnt_ptr, cap);
     if (threadIdx.x < 64) sh[threadIdx.x] = 0;
     __syncthreads();
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) atomicAdd(&sh[dest[i]], 1u);
@@ -73,10 +94,23 @@ static __global__ void __launch_bounds__(NT) route_count_kernel(const uint32_t* 
     if (threadIdx.x < P && sh[threadIdx.x]) atomicAdd(counts + threadIdx.x, sh[threadIdx.x]);
 }
 
+/// displ = exclusive scan of counts over the P <= 64 peers (one warp pair; no trip to the host).
+static __global__ void route_scan_kernel(const uint32_t* __restrict__ counts, uint32_t P, uint32_t* __restrict__ displ) {
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t p = 0; p < P; ++p) {
+            displ[p] = acc;
+            acc += counts[p];
+        }
+    }
+}
+
 /// pos[i] = displ[dest[i]] + arrival order inside the bucket; fill[] starts at zero.
-static __global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restrict__ dest, uint32_t cnt,
+static __global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* __restrict__ dest,
+                                                         const uint32_t* __restrict__ cnt_ptr, uint32_t cap,
                                                          const uint32_t* __restrict__ displ,
                                                          uint32_t* __restrict__ fill, uint32_t* __restrict__ pos) {
+    const uint32_t cnt = routed_count(cnt_ptr, cap);
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) {
         const uint32_t d = dest[i];
         pos[i] = displ[d] + atomicAdd(fill + d, 1u);
@@ -85,8 +119,10 @@ static __global__ void __launch_bounds__(NT) route_place_kernel(const uint32_t* 
 
 template <int W>
 static __global__ void __launch_bounds__(NT) route_scatter_keys_kernel(const uint32_t* __restrict__ keys,
-                                                                const uint32_t* __restrict__ pos, uint32_t cnt,
+                                                                const uint32_t* __restrict__ pos,
+                                                                const uint32_t* __restrict__ cnt_ptr, uint32_t cap,
                                                                 uint32_t* __restrict__ send) {
+    const uint32_t cnt = routed_count(cnt_ptr, cap);
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT)
         store_key<W>(send + size_t(pos[i]) * W, load_key<W>(keys + size_t(i) * W));
 }
@@ -194,9 +230,10 @@ static __global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* 
     if (blockIdx.x == 0 && threadIdx.x == 0) flag[nreq] = 0;
 }
 
-/// Resolves the COL_REQ markers: found -> n_local + halo slot, absent -> COL_ABSENT; counts the surviving
-/// entries per row.
+/// Resolves the COL_REQ markers (found -> n_local + halo slot, absent -> dropped) and closes the gaps inside the
+/// row's scratch: afterwards the first row_len[i] scratch entries of row i are its CSR entries, in neighbour-key order.
 static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int width, uint32_t* __restrict__ tmp_col,
+                                                              double* __restrict__ tmp_val,
                                                               const uint32_t* __restrict__ tmp_cnt,
                                                               const uint32_t* __restrict__ req_pos,
                                                               const uint32_t* __restrict__ reply,
@@ -204,6 +241,7 @@ static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n,
                                                               uint32_t* __restrict__ row_len) {
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         uint32_t* tc = tmp_col + size_t(i) * width;
+        double* tv = tmp_val + size_t(i) * width;
         const uint32_t cnt = tmp_cnt[i];
         uint32_t len = 0;
         for (uint32_t s = 0; s < cnt; ++s) {
@@ -211,22 +249,25 @@ static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n,
             if (c != COL_ABSENT && (c & COL_REQ)) {
                 const uint32_t p = req_pos[c & ~COL_REQ];
                 c = (reply[p] != COL_ABSENT) ? n + halo_slot[p] : COL_ABSENT;
-                tc[s] = c;
             }
-            if (c != COL_ABSENT) ++len;
+            if (c != COL_ABSENT) {
+                tc[len] = c;
+                if (len != s) tv[len] = tv[s];
+                ++len;
+            }
         }
         row_len[i] = len;
     }
 }
 
-/// Pass 2 on a shard: compacts the scratch into CSR, skipping absent remote neighbours.  code != nullptr: the value
-/// codes of the Taylor tile kernels are produced on the way (encode_csr_kernel's rule: index of the value in the
-/// model's table; the diagonal entry 0xffff + diag[row] when the diagonals are not tabulated; *fail when a value is
-/// not in the table).
+/// Pass 2 on a shard: the gap-free scratch rows -> CSR.  A warp takes 32 consecutive rows, whose entries form ONE
+/// contiguous run of the CSR arrays, and writes it with coalesced stores (assemble_compact_kernel's scheme).  code !=
+/// nullptr: the value codes of the Taylor tile kernels are produced on the way (encode_csr_kernel's rule: index of the
+/// value in the model's table; the diagonal entry 0xffff + diag[row] when the diagonals are not tabulated; *fail when
+/// a value is not in the table).
 static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
                                                                       const uint32_t* __restrict__ tmp_col,
                                                                       const double* __restrict__ tmp_val,
-                                                                      const uint32_t* __restrict__ tmp_cnt,
                                                                       const uint32_t* __restrict__ row_ptr,
                                                                       int32_t* __restrict__ col,
                                                                       double* __restrict__ val,
@@ -234,30 +275,43 @@ static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uin
                                                                       int vt_diag, uint16_t* __restrict__ code,
                                                                       double* __restrict__ diag,
                                                                       uint32_t* __restrict__ fail) {
-    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
-        uint32_t k = row_ptr[i];
-        const uint32_t* tc = tmp_col + size_t(i) * width;
-        const double* tv = tmp_val + size_t(i) * width;
-        const uint32_t cnt = tmp_cnt[i];
-        for (uint32_t s = 0; s < cnt; ++s) {
-            if (tc[s] != COL_ABSENT) {
-                const double v = tv[s];
-                col[k] = int32_t(tc[s]);
-                val[k] = v;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    for (uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        const uint32_t rp = __ldg(row_ptr + (i < n ? i : n));  // rows past the end are empty
+        const uint32_t rp0 = __shfl_sync(0xffffffffu, rp, 0);
+        const uint32_t end = __ldg(row_ptr + (base + 32 < n ? base + 32 : n));
+        const uint32_t total = end - rp0;
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint32_t target = rp0 + (k < total ? k : total - 1);
+            uint32_t r = 0;  // last row whose offset is <= target
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, rp, (r + step) & 31);
+                if (v <= target) r += step;
+            }
+            const uint32_t off = target - __shfl_sync(0xffffffffu, rp, r);
+            if (k < total) {
+                const size_t src = size_t(base + r) * width + off;
+                const uint32_t cc = __ldg(tmp_col + src);
+                const double v = __ldg(tmp_val + src);
+                col[target] = int32_t(cc);
+                val[target] = v;
                 if (code != nullptr) {
-                    if (!vt_diag && tc[s] == i) {
-                        diag[i] = v;
-                        code[k] = uint16_t(0xffffu);
+                    if (!vt_diag && cc == uint32_t(base + r)) {
+                        diag[base + r] = v;
+                        code[target] = uint16_t(0xffffu);
                     } else {
                         uint32_t cd = vt_find(vtab, vt_n, v);
                         if (cd == 0xfffeu) {
                             *fail = 1u;
                             cd = 0;
                         }
-                        code[k] = uint16_t(cd);
+                        code[target] = uint16_t(cd);
                     }
                 }
-                ++k;
             }
         }
     }

@@ -15,7 +15,11 @@ MODELS = {
            dict(init="localized", site=-1, m_init=6)),
 }
 model, init_kw = MODELS[name]
-ctx = pb.Context(pb.ModelDef(**model))
+comm = None
+if os.environ.get("PB200_PROF_SHARDED"):  # the sharded algorithms over a one-rank NCCL communicator
+    from paper_2603_07341_b200.dist import NcclComm
+    comm = NcclComm(device=0, rank=0, world=1)
+ctx = pb.Context(pb.ModelDef(**model), comm=comm)
 run = ctx.run(m=2, q_nom=q, dt=0.05, rtol=1e-15, t_max=50.0, seed=7, **init_kw)
 import torch
 for s in range(spin):
