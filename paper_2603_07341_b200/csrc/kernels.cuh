@@ -435,9 +435,12 @@ __device__ __forceinline__ void hist_add_aggregated(uint32_t* sh, uint32_t digit
 /// Selection pass 1 fused with the weights: w_i = re^2 + im^2 (std::norm, engine.hpp:113-116), their sum, the
 /// support count, and the histogram of the top 11 bits (sign + exponent) of the positive weights.  The last CTA
 /// to finish stores norm2 / support and, when support > q_nom (= ctl->k on entry), picks the first digit.
+/// gsum != nullptr (a shard): the sums go to gsum[0..1] and the histogram stays as it is -- both are all-reduced over
+/// the ranks before select_pick_global_kernel picks the digit.
 static __global__ void __launch_bounds__(NT) weights_hist_kernel(const double2* __restrict__ c, uint32_t n,
                                                           double* __restrict__ w, double* __restrict__ partials,
-                                                          SelectCtl* ctl, uint32_t* __restrict__ hist) {
+                                                          SelectCtl* ctl, uint32_t* __restrict__ hist,
+                                                          double* __restrict__ gsum = nullptr) {
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ double smem[NT / 32];
     __shared__ uint32_t wsum[NT / 32];
@@ -462,6 +465,13 @@ static __global__ void __launch_bounds__(NT) weights_hist_kernel(const double2* 
     __threadfence();  // the histogram contributions are visible before this CTA takes its ticket (inside grid_sum)
     double tot[2];
     if (!grid_sum<2>(acc, partials, &ctl->ticket, tot, smem)) return;
+    if (gsum != nullptr) {
+        if (threadIdx.x == 0) {
+            gsum[0] = tot[0];
+            gsum[1] = tot[1];
+        }
+        return;
+    }
     const unsigned long long support = (unsigned long long)tot[1];
     if (threadIdx.x == 0) {
         ctl->norm2 = tot[0];
@@ -482,9 +492,10 @@ constexpr uint32_t SEL_LIST_CAP = 1u << 16;
 /// its members' bit patterns so one CTA can finish the remaining 42 bits.  Does nothing when the group is larger
 /// than the list (massive exact ties): the host then falls back to full passes.
 static __global__ void __launch_bounds__(NT) select_gather_kernel(const double* __restrict__ w, uint32_t n, int hi_shift,
-                                                           SelectCtl* ctl, unsigned long long* __restrict__ list) {
+                                                           SelectCtl* ctl, unsigned long long* __restrict__ list,
+                                                           uint32_t cap = SEL_LIST_CAP) {
     if (ctl->support <= ctl->k) return;  // nothing is cut (after a pick the wanted rank is below the support)
-    if (ctl->count_eq > SEL_LIST_CAP) return;
+    if (ctl->count_eq > cap) return;
     const unsigned long long prefix = ctl->prefix;
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         const double ww = w[i];
@@ -495,11 +506,12 @@ static __global__ void __launch_bounds__(NT) select_gather_kernel(const double* 
 }
 
 /// Single CTA: remaining digits (shifts 31, 20, 9, 0; widths 11, 11, 11, 9) over the gathered list.
-static __global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long long* __restrict__ list, SelectCtl* ctl) {
+static __global__ void __launch_bounds__(NT) select_tail_kernel(const unsigned long long* __restrict__ list, SelectCtl* ctl,
+                                                         uint32_t cap = SEL_LIST_CAP) {
     __shared__ uint32_t sh[SEL_BINS];
     __shared__ uint32_t wsum[NT / 32];
     const uint32_t cnt = ctl->list_n;
-    if (cnt == 0 || ctl->count_eq > SEL_LIST_CAP) return;
+    if (cnt == 0 || ctl->count_eq > cap) return;
     const int shifts[4] = {31, 20, 9, 0};
     const int widths[4] = {11, 11, 11, 9};
     for (int p = 0; p < 4; ++p) {

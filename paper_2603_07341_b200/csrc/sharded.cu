@@ -381,11 +381,46 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
     init.k = q_nom;
     std::memcpy(pinned, &init, sizeof(init));
     PB_CUDA(cudaMemcpyAsync(&c->select, pinned, sizeof(SelectCtl), cudaMemcpyHostToDevice, stream));
-    weights_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select);
+    // Two histogram passes (the first fused with the weights), each all-reduced; the group that still shares the
+    // cutoff's first 22 bits is almost always a handful of values, so every rank stages its members, ONE more all-reduce
+    // gathers them (disjoint zero-initialised slots) and one CTA per rank finishes the remaining 42 bits on identical
+    // data.  The sum of the weights and the support count ride on the device collectives: ONE read-back.
+    double* gsum = c->tsum;  // (free between the Taylor phases)
+    sel_list.ensure(size_t(SEL_LIST_CAP) * 8);
+    sel_stage.ensure(size_t(P) * SHARD_STAGE_WORDS * 4);
+    PB_CUDA(cudaMemsetAsync(sel_stage.p, 0, size_t(P) * SHARD_STAGE_WORDS * 4, stream));
+    weights_hist_kernel<<<g, NT, 0, stream>>>(d_c, n, weights.as<double>(), partials.as<double>(), &c->select,
+                                              hist.as<uint32_t>(), gsum);
     check_launch();
-    SelectCtl sc = read_back<SelectCtl>(&c->select);
-    const double norm2 = allreduce_host(sc.norm2);
-    const uint64_t support = allreduce_host_u64(sc.support);
+    comm_check(ops.allreduce_u32_dev(ops.user, hist.as<uint32_t>(), SEL_BINS, stream), "allreduce_u32_dev");
+    comm_check(ops.allreduce_f64_dev(ops.user, gsum, 2, stream), "allreduce_f64_dev");
+    select_pick_global_kernel<<<1, NT, 0, stream>>>(hist.as<uint32_t>(), 11, &c->select, gsum);
+    check_launch();
+    const int sg = std::min(g, sm_count * 2);
+    select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, 42, 11, &c->select, hist.as<uint32_t>(), 0);
+    check_launch();
+    comm_check(ops.allreduce_u32_dev(ops.user, hist.as<uint32_t>(), SEL_BINS, stream), "allreduce_u32_dev");
+    select_pick_global_kernel<<<1, NT, 0, stream>>>(hist.as<uint32_t>(), 11, &c->select);
+    check_launch();
+    select_gather_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 42, &c->select,
+                                               sel_list.as<unsigned long long>(), SHARD_LIST_CAP);
+    check_launch();
+    select_stage_kernel<<<4, NT, 0, stream>>>(sel_list.as<unsigned long long>(), &c->select, uint32_t(rank),
+                                              sel_stage.as<uint32_t>());
+    check_launch();
+    comm_check(ops.allreduce_u32_dev(ops.user, sel_stage.as<uint32_t>(), uint64_t(P) * SHARD_STAGE_WORDS, stream),
+               "allreduce_u32_dev(select members)");
+    select_union_kernel<<<1, NT, 0, stream>>>(sel_stage.as<uint32_t>(), P, sel_list.as<unsigned long long>(), &c->select);
+    check_launch();
+    // (PB200_SHARD_NO_TAIL=1: tests force the full-pass fallback that massive exact ties would take)
+    static const bool no_tail = std::getenv("PB200_SHARD_NO_TAIL") != nullptr;
+    if (!no_tail) {
+        select_tail_kernel<<<1, NT, 0, stream>>>(sel_list.as<unsigned long long>(), &c->select, SHARD_LIST_CAP);
+        check_launch();
+    }
+    SelectCtl sc = read_back<SelectCtl>(&c->select);  // identical on every rank (all-reduced inputs)
+    const double norm2 = sc.norm2;
+    const uint64_t support = sc.support;
     if (norm2_out) *norm2_out = norm2;
     if (support == 0) throw PacesError("truncate_select: state has no support");
 
@@ -394,18 +429,20 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
         select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 0, &c->select, 1, keep, nullptr, nullptr);
         check_launch();
     } else {
-        static const int shifts[6] = {53, 42, 31, 20, 9, 0};
-        static const int widths[6] = {11, 11, 11, 11, 11, 9};
-        const int sg = std::min(g, sm_count * 2);
-        for (int p = 0; p < 6; ++p) {
-            select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
-                                                      hist.as<uint32_t>(), 0);
-            check_launch();
-            comm_check(ops.allreduce_u32_dev(ops.user, hist.as<uint32_t>(), SEL_BINS, stream), "allreduce_u32_dev");
-            select_pick_global_kernel<<<1, NT, 0, stream>>>(hist.as<uint32_t>(), widths[p], &c->select);
-            check_launch();
+        if (!sc.tail_done) {
+            // the group sharing the first 22 bits is larger than the staged lists (massive exact ties): full passes
+            static const int shifts[4] = {31, 20, 9, 0};
+            static const int widths[4] = {11, 11, 11, 9};
+            for (int p = 0; p < 4; ++p) {
+                select_pass_kernel<<<sg, NT, 0, stream>>>(weights.as<double>(), n, shifts[p], widths[p], &c->select,
+                                                          hist.as<uint32_t>(), 0);
+                check_launch();
+                comm_check(ops.allreduce_u32_dev(ops.user, hist.as<uint32_t>(), SEL_BINS, stream), "allreduce_u32_dev");
+                select_pick_global_kernel<<<1, NT, 0, stream>>>(hist.as<uint32_t>(), widths[p], &c->select);
+                check_launch();
+            }
+            sc = read_back<SelectCtl>(&c->select);
         }
-        sc = read_back<SelectCtl>(&c->select);  // identical on every rank: derived from all-reduced histograms
         const uint64_t need = q_nom - sc.count_gt;
         if (need >= sc.count_eq) {
             select_flags_kernel<<<g, NT, 0, stream>>>(weights.as<double>(), n, 1, &c->select, 1, keep, nullptr, nullptr);

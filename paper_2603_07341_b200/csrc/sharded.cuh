@@ -402,9 +402,61 @@ static __global__ void __launch_bounds__(NT) mark_selected_kernel(ModelDev m, ui
 
 /// Gathers the keys of flagged rows (order preserving): out[pos[i]] = table[i].  (= compact_rows_kernel)
 
-/// Pick step of the radix select on an ALL-REDUCED histogram (one CTA); see select_pass_kernel.
-static __global__ void __launch_bounds__(NT) select_pick_global_kernel(uint32_t* __restrict__ hist, int width, SelectCtl* ctl) {
+/// Members of the cutoff's group a rank contributes to the single-CTA tail of the distributed selection, and the
+/// staging layout of their exchange: per rank one count word + 2 words per member.  The ranks' slots are disjoint and
+/// start from zero, so an all-reduce (sum) of the buffer IS the all-gather.
+constexpr uint32_t SHARD_LIST_CAP = 1024;
+constexpr uint32_t SHARD_STAGE_WORDS = 1 + 2 * SHARD_LIST_CAP;
+
+/// Copies this rank's members into its slot (nothing when the global group is too large for the tail, or nothing is cut).
+static __global__ void __launch_bounds__(NT) select_stage_kernel(const unsigned long long* __restrict__ list,
+                                                          const SelectCtl* __restrict__ ctl, uint32_t rank,
+                                                          uint32_t* __restrict__ stage) {
+    if (ctl->support <= ctl->k || ctl->count_eq > SHARD_LIST_CAP) return;
+    const uint32_t cnt = min(ctl->list_n, SHARD_LIST_CAP);
+    uint32_t* slot = stage + size_t(rank) * SHARD_STAGE_WORDS;
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) {
+        const unsigned long long b = list[i];
+        slot[1 + 2 * i] = uint32_t(b);
+        slot[2 + 2 * i] = uint32_t(b >> 32);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) slot[0] = cnt;
+}
+
+/// One CTA: the all-reduced slots -> one contiguous list (same order on every rank), ctl->list_n = its length.
+static __global__ void __launch_bounds__(NT) select_union_kernel(const uint32_t* __restrict__ stage, uint32_t P,
+                                                          unsigned long long* __restrict__ list, SelectCtl* ctl) {
+    __shared__ uint32_t off[65];
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t r = 0; r < P; ++r) {
+            off[r] = acc;
+            acc += min(stage[size_t(r) * SHARD_STAGE_WORDS], SHARD_LIST_CAP);
+        }
+        off[P] = acc;
+        ctl->list_n = acc;
+    }
+    __syncthreads();
+    for (uint32_t r = 0; r < P; ++r) {
+        const uint32_t* slot = stage + size_t(r) * SHARD_STAGE_WORDS;
+        const uint32_t cnt = off[r + 1] - off[r];
+        for (uint32_t i = threadIdx.x; i < cnt; i += NT)
+            list[off[r] + i] = (unsigned long long)slot[1 + 2 * i] | ((unsigned long long)slot[2 + 2 * i] << 32);
+    }
+}
+
+/// Pick step of the radix select on an ALL-REDUCED histogram (one CTA); see select_pass_kernel.  gsum != nullptr (first
+/// digit): the all-reduced sum of the weights and support count are stored first.
+static __global__ void __launch_bounds__(NT) select_pick_global_kernel(uint32_t* __restrict__ hist, int width, SelectCtl* ctl,
+                                                                const double* __restrict__ gsum = nullptr) {
     __shared__ uint32_t wsum[NT / 32];
+    if (gsum != nullptr) {
+        if (threadIdx.x == 0) {
+            ctl->norm2 = gsum[0];
+            ctl->support = (unsigned long long)gsum[1];
+        }
+        __syncthreads();
+    }
     constexpr int PER = SEL_BINS / NT;
     uint32_t loc[PER];
     uint32_t s = 0;

@@ -26,6 +26,14 @@ def test_two_ranks_match_oracle():
 
 
 @pytest.mark.gpu
+def test_two_ranks_selection_full_pass_fallback():
+    """The distributed selection normally finishes on the staged members of the cutoff's group (one CTA per rank on
+    identical data); a group larger than the staged lists -- massive exact ties -- takes four more all-reduced
+    histogram passes instead.  Forced here; the trajectories must not change."""
+    _launch(2, "ties_holstein_L5_d6,cfg1_holstein_L4_d8", 20, 29617, env={"PB200_SHARD_NO_TAIL": "1"})
+
+
+@pytest.mark.gpu
 def test_three_and_four_ranks_match_oracle():
     _launch(3, "ties_holstein_L5_d6,square_3x3_d5", 25, 29612)
     _launch(4, "cfg2_layout_L16_d16_small,substeps_L4_d4_m1,tb_chain_31", 20, 29613)
