@@ -224,7 +224,7 @@ struct Engine {
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     DevBuf row_class, scan_aligned;
     DevBuf out_keys, out_dest, route_pos, route_ctr, sendbuf, recvbuf, req_keys, req_dest, req_pos, reply, answer,
-        found, halo_flag, tmp_cnt, halo_stage, sel_keys, sel_stage;
+        found, halo_flag, tmp_cnt, halo_stage, sel_keys, sel_stage, asm_info;
     std::vector<uint64_t> h_send, h_recv;
 
     explicit Engine(int dev);

@@ -282,20 +282,22 @@ void Engine::assemble_sharded(Space& sp) {
                           found.as<uint32_t>()));
     check_launch();
     exclusive_scan(found.as<uint32_t>(), nr + 1);
-    // per-requester found counts = differences of the scan at the bucket boundaries
-    sp.halo_send.assign(P, 0);
-    {
+    // per-requester found counts = differences of the scan at the bucket boundaries: picked on the device, they come
+    // back with the halo counts and nnz in ONE read-back further down (the send list is sized by its bound meanwhile)
+    asm_info.ensure(sizeof(ShardAsmInfo));
+    ShardAsmInfo* dinfo = asm_info.as<ShardAsmInfo>();
+    auto offsets_of = [&](const std::vector<uint64_t>& per_peer) {
+        PeerOffsets o{};
         uint64_t off = 0;
-        uint32_t* pin = static_cast<uint32_t*>(pinned);
         for (uint32_t p = 0; p <= P; ++p) {
-            PB_CUDA(cudaMemcpyAsync(pin + p, found.as<uint32_t>() + off, 4, cudaMemcpyDeviceToHost, stream));
-            if (p < P) off += req_recv[p];
+            o.v[p] = uint32_t(off);
+            if (p < P) off += per_peer[p];
         }
-        sync();
-        for (uint32_t p = 0; p < P; ++p) sp.halo_send[p] = pin[p + 1] - pin[p];
-        sp.send_total = pin[P];
-    }
-    sp.send_idx.ensure(size_t(sp.send_total) * 4 + 4);
+        return o;
+    };
+    pick_boundaries_kernel<<<1, 96, 0, stream>>>(found.as<uint32_t>(), offsets_of(req_recv), P, nullptr, dinfo->found_at);
+    check_launch();
+    sp.send_idx.ensure(size_t(nr) * 4 + 4);
     build_send_list_kernel<<<grid_for(nr), NT, 0, stream>>>(answer.as<uint32_t>(), found.as<uint32_t>(), uint32_t(nr),
                                                             sp.send_idx.as<uint32_t>());
     check_launch();
@@ -309,19 +311,6 @@ void Engine::assemble_sharded(Space& sp) {
     reply_flags_kernel<<<grid_for(nreq), NT, 0, stream>>>(reply.as<uint32_t>(), nreq, halo_flag.as<uint32_t>());
     check_launch();
     exclusive_scan(halo_flag.as<uint32_t>(), uint64_t(nreq) + 1);
-    sp.halo_recv.assign(P, 0);
-    {
-        uint64_t off = 0;
-        uint32_t* pin = static_cast<uint32_t*>(pinned);
-        for (uint32_t p = 0; p <= P; ++p) {
-            PB_CUDA(cudaMemcpyAsync(pin + p, halo_flag.as<uint32_t>() + off, 4, cudaMemcpyDeviceToHost, stream));
-            if (p < P) off += req_send[p];
-        }
-        sync();
-        for (uint32_t p = 0; p < P; ++p) sp.halo_recv[p] = pin[p + 1] - pin[p];
-        sp.halo_n = pin[P];
-    }
-    if (uint64_t(n) + sp.halo_n > 0x7fffffffull) throw PacesError("assembly: local rows + halo exceed int32 columns");
     resolve_requests_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
                                                             tmp_cnt.as<uint32_t>(), req_pos.as<uint32_t>(),
                                                             reply.as<uint32_t>(), halo_flag.as<uint32_t>(),
@@ -329,7 +318,20 @@ void Engine::assemble_sharded(Space& sp) {
     check_launch();
     PB_CUDA(cudaMemsetAsync(sp.row_ptr.as<uint32_t>() + n, 0, 4, stream));
     exclusive_scan(sp.row_ptr.as<uint32_t>(), uint64_t(n) + 1);
-    const uint32_t nnz = read_back<uint32_t>(sp.row_ptr.as<uint32_t>() + n);
+    pick_boundaries_kernel<<<1, 96, 0, stream>>>(halo_flag.as<uint32_t>(), offsets_of(req_send), P,
+                                                 sp.row_ptr.as<uint32_t>() + n, dinfo->halo_at);
+    check_launch();
+    const ShardAsmInfo info = read_back<ShardAsmInfo>(dinfo);
+    sp.halo_send.assign(P, 0);
+    sp.halo_recv.assign(P, 0);
+    for (uint32_t p = 0; p < P; ++p) {
+        sp.halo_send[p] = info.found_at[p + 1] - info.found_at[p];
+        sp.halo_recv[p] = info.halo_at[p + 1] - info.halo_at[p];
+    }
+    sp.send_total = info.found_at[P];
+    sp.halo_n = info.halo_at[P];
+    if (uint64_t(n) + sp.halo_n > 0x7fffffffull) throw PacesError("assembly: local rows + halo exceed int32 columns");
+    const uint32_t nnz = info.halo_at[65];
     sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
     sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
     // value codes for the Taylor tile kernels, produced by the compaction itself (no pass of their own)

@@ -214,6 +214,22 @@ static __global__ void __launch_bounds__(NT) answer_requests_kernel(const uint32
     if (blockIdx.x == 0 && threadIdx.x == 0) found[nr] = 0;
 }
 
+/// Per-peer bucket boundaries of an exclusive scan, picked on the device: out[p] = scan[offs.v[p]] for p = 0..P (the
+/// requests of peer p occupy [offs.v[p], offs.v[p+1]) of the bucketed list); extra != nullptr: out[65] = *extra.
+/// Replaces P + 1 four-byte copies to the host per list.
+struct PeerOffsets {
+    uint32_t v[65];
+};
+struct ShardAsmInfo {
+    uint32_t found_at[66];  // [0..P] scan of the found flags at the requesters' bucket boundaries
+    uint32_t halo_at[66];   // [0..P] scan of the reply flags at the owners' bucket boundaries; [65] = nnz
+};
+static __global__ void pick_boundaries_kernel(const uint32_t* __restrict__ scan, PeerOffsets offs, uint32_t P,
+                                              const uint32_t* __restrict__ extra, uint32_t* __restrict__ out) {
+    if (threadIdx.x <= P) out[threadIdx.x] = scan[offs.v[threadIdx.x]];
+    if (threadIdx.x == 0 && extra != nullptr) out[65] = *extra;
+}
+
 /// send_idx[found_pos[j]] = answer[j] for found requests (order preserving).
 static __global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __restrict__ answer,
                                                              const uint32_t* __restrict__ found_pos, uint32_t nr,
