@@ -637,21 +637,32 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
             e.aux_words.ensure(rows * W * 4 + 16);
             // both uploads and comparisons on their own stream: the step itself starts at once on the resident data
             e.sync();  // the resident buffers they read are final
-            auto upload = [&e, flags, coeff, words, rows, W, &res]() {
+            // uploads first, both on the io stream; the two comparison kernels follow once the Taylor phase is enqueued
+            // and wait for its end: the GPU is idle then (the coefficient download is the critical path), while beside
+            // the Taylor launches they would take SM slots from the persistent tile kernels
+            auto upload = [&e, flags, coeff, words, rows, W]() {
                 PB_CUDA(cudaMemsetAsync(flags, 0, 8, e.io_stream));
                 PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
-                words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(
-                    e.aux_coeff.as<uint32_t>(), e.coeff[e.ccur].as<uint32_t>(), rows * 4, flags);
-                e.check_launch();
                 PB_CUDA(cudaMemcpyAsync(e.aux_words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.io_stream));
-                words_differ_kernel<<<e.grid_for(rows * W), NT, 0, e.io_stream>>>(
-                    e.aux_words.as<uint32_t>(), res.words.as<uint32_t>(), rows * W, flags + 1);
+            };
+            const uint32_t* res_words = res.words.as<uint32_t>();
+            const uint32_t* res_coeff = e.coeff[e.ccur].as<uint32_t>();
+            auto compare = [&e, flags, rows, W, res_words, res_coeff](cudaEvent_t after) {
+                if (after) PB_CUDA(cudaStreamWaitEvent(e.io_stream, after, 0));
+                words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(e.aux_coeff.as<uint32_t>(), res_coeff,
+                                                                                  rows * 4, flags);
+                e.check_launch();
+                words_differ_kernel<<<e.grid_for(rows * W), NT, 0, e.io_stream>>>(e.aux_words.as<uint32_t>(), res_words,
+                                                                                  rows * W, flags + 1);
                 e.check_launch();
             };
-            if (std::getenv("PB200_EAGER_UPLOAD"))
+            if (std::getenv("PB200_EAGER_UPLOAD")) {
                 upload();
-            else
+                compare(nullptr);
+            } else {
                 io.start_upload = upload;
+                io.start_compare = compare;
+            }
             {
                 const pb200_run_cfg saved = e.cfg;
                 e.cfg = c;

@@ -1105,6 +1105,10 @@ void Engine::run_step(pb200_diag* out) {
         rec.q_true = sharded ? next.n_global : next.n;
         rec.energy = e;
         PB_CUDA(cudaEventRecord(ev[6], stream));
+        if (io && io->start_compare) {
+            io->start_compare(ev[6]);
+            io->start_compare = nullptr;
+        }
         if (io && next.n)
             PB_CUDA(cudaMemcpyAsync(io->out_coeff, psi, size_t(next.n) * 16, cudaMemcpyDeviceToHost, stream));
         sync();

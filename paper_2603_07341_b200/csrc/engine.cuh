@@ -208,6 +208,9 @@ struct Engine {
         // phase is ~40 short kernels whose launches (command fetches over PCIe) crawl while 100 MB of upload
         // saturate the same link direction; the Taylor kernels behind it are long and enqueued ahead.
         mutable std::function<void()> start_upload;
+        // Enqueues the two comparison kernels behind the uploads; run_step calls it with the event that marks the end
+        // of the Taylor phase (they run while the coefficients travel to the host, on an otherwise idle GPU).
+        mutable std::function<void(cudaEvent_t)> start_compare;
     };
     /// thrown by run_step when the deferred key comparison of a cached host-buffer step fails
     struct CacheMiss {};

@@ -18,7 +18,18 @@ cases = [
     (dict(kind=0, extents=(31,), eps=(0.0,), hop=(1.0,)),
      dict(init="localized", site=-1, m_init=3, m=2, q_nom=9, dt=0.05, rtol=1e-15, t_max=5.0, seed=1), 10),
 ]
+SHARDED = bool(os.environ.get("PB200_SANITIZE_SHARDED"))  # the sharded algorithms over a one-rank NCCL communicator
 for model, run_kw, steps in cases:
+    if SHARDED:
+        from paper_2603_07341_b200.dist import NcclComm
+        ctx = pb.Context(pb.ModelDef(**model), comm=NcclComm(device=0, rank=0, world=1))
+        run = ctx.run(**run_kw)
+        for s in range(steps):
+            d = run.step()
+        o = run.observe()
+        print("sharded", model["extents"], "q_true", d["q_true"], "order", d["taylor_order"], flush=True)
+        ctx.close()
+        continue
     ctx = pb.Context(pb.ModelDef(**model))
     run = ctx.run(**run_kw)
     for s in range(steps):
