@@ -1032,8 +1032,14 @@ void Engine::run_step(pb200_diag* out) {
         if (incremental) {
             PB_CUDA(cudaEventRecord(ev[2], stream));
         } else if (sharded) {
-            // grow() = expansion + assembly; split the timer inside via ev[2]
-            grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
+            // grow() = expansion + assembly; split the timer inside via ev[2].  The table grows incrementally from the
+            // previous space when it can (sharded.cu); a buffer bound hit on any rank sends every rank to the full path
+            const bool inc_shard = old.has_h && old.has_full && cfg.m >= 1 && cfg.m <= INC_MAX_ORDER && md.max_deg + md.kind > 0 &&
+                                   memory_cap_bytes() == 0 && std::getenv("PB200_NO_INCREMENTAL") == nullptr;
+            if (!(inc_shard && grow_incremental_sharded(old, last_kept_global, cfg.m, next))) {
+                if (inc_shard) ++inc_fallbacks;
+                grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
+            }
         } else {
             grow(seeds.as<uint32_t>(), kept, cfg.m, next);
         }

@@ -263,6 +263,9 @@ struct Engine {
     void classify_rows(Space& sp);
     void grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out);
     void assemble_sharded(Space& sp);
+    /// incremental table growth on shards (sharded.cu); collective, false on every rank = take the full path
+    bool grow_incremental_sharded(const Space& old, uint64_t kept_global, int m, Space& next);
+    uint64_t last_kept_global = 0;  // rows select_sharded kept over all ranks
     uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
                             double* norm2_out);
     /// fuse_first (tile kernels only): the first order also yields <x|H|x>, |x|^2 and the non-finite count of the input

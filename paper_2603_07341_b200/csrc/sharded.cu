@@ -164,7 +164,8 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
     Ctl* c = dctl();
     ShardCounters* dsc = &route_block()->sc;
 
-    for (int k = 0; k < order; ++k) {
+    int levels_done = 0;
+    for (int k = 0; k < order; ++k, ++levels_done) {
         if (allreduce_host_u64(nf) == 0) break;  // every frontier is empty: the ball is complete
         const uint64_t cap64 = uint64_t(nf) * uint64_t(nmoves) + 1;
         if (cap64 > 0x7ffffff0ull) throw PacesError("subspace growth: candidate count exceeds 32-bit indexing");
@@ -228,8 +229,179 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
     out.n = n;
     out.q_nom = ns_global;
     out.order = order;
+    // which rows had their neighbourhood generated (remote neighbours included: they went to their owners): all but the
+    // last frontier, when every order ran (the incremental growth of the next step needs it)
+    out.full.ensure(size_t(n) + 1);
+    PB_CUDA(cudaMemsetAsync(out.full.p, order == 0 ? 0 : 1, n, stream));
+    if (order > 0 && levels_done == order && nf > 0 && !identity_frontier) {
+        inc_clear_full_kernel<<<grid_for(nf), NT, 0, stream>>>(frontier[fcur].as<uint32_t>(), nf, out.full.as<uint8_t>());
+        check_launch();
+    }
+    out.has_full = true;
     PB_CUDA(cudaEventRecord(ev[2], stream));
     assemble_sharded(out);
+}
+
+// ------------------------------------------------------------------------------------------------
+// grow_subspace on shards, incremental: the new TABLE from the previous space (sharded.cuh, "Incremental TABLE growth
+// on a shard"); H_eff of the new table is then assembled the usual way.  Collective; returns false on every rank when
+// any rank hit a buffer bound (the caller then runs grow_sharded from the kept keys).
+// ------------------------------------------------------------------------------------------------
+bool Engine::grow_incremental_sharded(const Space& old, uint64_t kept_global, int m, Space& next) {
+    const int W = md.W;
+    const uint32_t P = uint32_t(world);
+    const uint32_t n = old.n;
+    const int nmoves = md.max_deg + (md.kind == 1 ? 2 : 0);
+    Ctl* c = dctl();
+    inc_ctr.ensure(sizeof(IncCounters));
+    IncCounters* ictr = inc_ctr.as<IncCounters>();
+    PB_CUDA(cudaMemsetAsync(ictr, 0, sizeof(IncCounters), stream));
+    ShardCounters* dsc = &route_block()->sc;
+
+    // capacities (as incremental.cu): nothing is sized by a count the host would have to read first; a bound that is
+    // hit only raises `overflow`
+    const uint32_t side_cap = n / 4 + (1u << 16);
+    const uint64_t n_bound = uint64_t(n) + side_cap;
+    bool local_fail = n_bound > 0x7fffffffull;
+    {
+        const uint64_t want = std::max<uint64_t>(uint64_t(n / 8 + 1024) * uint64_t(std::max(nmoves, 1)), 1u << 16);
+        cand_keys.ensure(size_t(want) * W * 4);
+        cand_gap.ensure(size_t(want) * 4);
+    }
+    const uint32_t cand_cap =
+        uint32_t(std::min<uint64_t>({cand_keys.cap / (size_t(W) * 4), cand_gap.cap / 4, 0x7ffffff0ull}));
+    const uint32_t out_cap = cand_cap;
+    out_keys.ensure(size_t(out_cap) * W * 4);
+    out_dest.ensure(size_t(out_cap) * 4);
+    route_pos.ensure(size_t(out_cap) * 4);
+    sendbuf.ensure(size_t(out_cap) * W * 4 + 16);
+    perm.ensure(size_t(cand_cap) * 4 + 4);
+    seg_rank.ensure(size_t(cand_cap) * 4 + 4);
+    for (int i = 0; i < 2; ++i) {
+        inc_side_keys[i].ensure(size_t(side_cap) * W * 4 + 64);
+        inc_side_gap[i].ensure(size_t(side_cap) * 4 + 64);
+        inc_side_dist[i].ensure(size_t(side_cap) + 64);
+    }
+    inc_new_keys.ensure(size_t(cand_cap) * W * 4 + 64);
+    inc_new_gap.ensure(size_t(cand_cap) * 4 + 64);
+    inc_elist.ensure(size_t(n) * 4 + 4);
+    int sh = 0;
+    while ((uint64_t(n) >> sh) > (1u << 16)) ++sh;
+    const uint32_t nbuckets = uint32_t(uint64_t(n) >> sh) + 1;  // gaps run over [0, n]
+    const size_t bstride = (size_t(nbuckets) + 2 + 3) & ~size_t(3);
+    inc_buckets.ensure(3 * bstride * 4);
+    uint32_t* b_start = inc_buckets.as<uint32_t>();
+    uint32_t* b_fill = b_start + bstride;
+    uint32_t* b_kept = b_fill + bstride;
+    const int small_grid = sm_count * 4;
+
+    // distances: 0 on the kept rows (select_sharded's flags), the halo slots behind the local rows
+    const uint32_t n_ext = n + old.halo_n;
+    inc_dist.ensure(size_t(n_ext) + 16);
+    uint8_t* dist = inc_dist.as<uint8_t>();
+    inc_dist_from_keep_kernel<<<grid_for(n_ext), NT, 0, stream>>>(flag_keep.as<uint32_t>(), n, n_ext, dist);
+    check_launch();
+    halo_stage.ensure(size_t(old.send_total) + 16);
+
+    int scur = 0;
+    for (int k = 0; k < m; ++k) {
+        // the owners' distances of my halo rows (one byte per halo entry; the SpMV's pack lists carry them)
+        if (old.send_total) {
+            halo_pack_u8_kernel<<<grid_for(old.send_total), NT, 0, stream>>>(dist, old.send_idx.as<uint32_t>(), old.send_total,
+                                                                             halo_stage.as<uint8_t>());
+            check_launch();
+        }
+        comm_check(ops.alltoallv_dev(ops.user, halo_stage.p, old.halo_send.data(), dist + n, old.halo_recv.data(), 1, stream),
+                   "alltoallv_dev(distances)");
+        inc_level_kernel<<<grid_for(n), NT, 0, stream>>>(n, k, old.full.as<uint8_t>(), old.row_ptr.as<uint32_t>(),
+                                                          old.col.as<int32_t>(), dist, inc_elist.as<uint32_t>(), ictr);
+        check_launch();
+        PB_CUDA(cudaMemsetAsync(b_start, 0, 3 * bstride * 4, stream));
+        PB_CUDA(cudaMemsetAsync(dsc, 0, sizeof(ShardCounters), stream));
+        PB_DISPATCH_WS(W, inc_expand_sharded_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              md, uint32_t(rank), P, old.words.as<uint32_t>(), n, inc_elist.as<uint32_t>(),
+                              inc_side_keys[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), k, nmoves, dist,
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cand_cap, sh, b_start, ictr,
+                              out_keys.as<uint32_t>(), out_dest.as<uint32_t>(), out_cap, dsc));
+        check_launch();
+        // neighbours owned elsewhere -> their owners (device-side count, one read-back)
+        route_async(out_dest.as<uint32_t>(), &dsc->n_out, out_cap, route_pos.as<uint32_t>());
+        PB_DISPATCH_WS(W, route_scatter_keys_kernel<W><<<grid_for(out_cap), NT, 0, stream>>>(
+                              out_keys.as<uint32_t>(), route_pos.as<uint32_t>(), &dsc->n_out, out_cap, sendbuf.as<uint32_t>()));
+        check_launch();
+        const ShardCounters hsc = route_finish();
+        if (hsc.overflow) local_fail = true;  // (the exchange still runs: every rank keeps the same sequence of collectives)
+        const uint64_t nr = exchange_known(sendbuf.p, recvbuf, uint64_t(W) * 4);
+        if (nr) {
+            PB_DISPATCH_WS(W, inc_classify_received_kernel<W><<<grid_for(nr), NT, 0, stream>>>(
+                                  old.words.as<uint32_t>(), n, inc_side_keys[scur].as<uint32_t>(), k, recvbuf.as<uint32_t>(),
+                                  uint32_t(nr), dist, cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), cand_cap, sh, b_start,
+                                  ictr));
+            check_launch();
+        }
+        // unique new keys of this level in canonical order, merged into the side list (incremental.cu's chain)
+        const uint32_t* nc_ptr = &ictr->n_cand[k];
+        exclusive_scan(b_start, uint64_t(nbuckets) + 1);
+        place_candidates_kernel<<<small_grid, NT, 0, stream>>>(cand_gap.as<uint32_t>(), nc_ptr, cand_cap, sh, b_start,
+                                                               b_fill, perm.as<uint32_t>());
+        check_launch();
+        PB_DISPATCH_WS(W, segment_dedup_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, cand_cap, sh,
+                              b_start, seg_rank.as<uint32_t>(), b_kept, nullptr));
+        check_launch();
+        PB_DISPATCH_WS(W, segment_rank_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(), nc_ptr, cand_cap, sh,
+                              b_start, seg_rank.as<uint32_t>()));
+        check_launch();
+        exclusive_scan(b_kept, uint64_t(nbuckets) + 1);
+        PB_DISPATCH_WS(W, inc_emit_unique_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              cand_keys.as<uint32_t>(), cand_gap.as<uint32_t>(), perm.as<uint32_t>(),
+                              seg_rank.as<uint32_t>(), k, cand_cap, sh, b_kept, nbuckets, inc_new_keys.as<uint32_t>(),
+                              inc_new_gap.as<uint32_t>(), ictr));
+        check_launch();
+        PB_DISPATCH_WS(W, inc_side_merge_kernel<W><<<small_grid, NT, 0, stream>>>(
+                              inc_side_keys[scur].as<uint32_t>(), inc_side_gap[scur].as<uint32_t>(),
+                              inc_side_dist[scur].as<uint8_t>(), inc_new_keys.as<uint32_t>(), inc_new_gap.as<uint32_t>(), k,
+                              side_cap, inc_side_keys[scur ^ 1].as<uint32_t>(), inc_side_gap[scur ^ 1].as<uint32_t>(),
+                              inc_side_dist[scur ^ 1].as<uint8_t>(), ictr));
+        check_launch();
+        scur ^= 1;
+    }
+
+    // ---- the new table: survivors (distance <= m) and side keys at their merged positions
+    inc_newidx.ensure((size_t(n) + 2) * 4);  // add[]
+    pos_a.ensure((size_t(n) + 2) * 4);       // v[] -> its exclusive scan
+    uint32_t* add = inc_newidx.as<uint32_t>();
+    uint32_t* vs = pos_a.as<uint32_t>();
+    inc_shard_count_kernel<<<grid_for(uint64_t(n) + 1), NT, 0, stream>>>(n, m, dist, inc_side_gap[scur].as<uint32_t>(), m, ictr,
+                                                                         add, vs);
+    check_launch();
+    exclusive_scan(vs, uint64_t(n) + 2);
+    inc_shard_head_kernel<<<1, 32, 0, stream>>>(n, vs, m, ictr);
+    check_launch();
+    const IncHead fin = read_back<IncHead>(&ictr->h);
+    if (fin.overflow) local_fail = true;
+    // any rank's overflow sends every rank to the full path
+    if (allreduce_host_u64(local_fail ? 1 : 0) != 0) return false;
+    if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
+    next.words.ensure(size_t(fin.n_new) * W * 4 + 64);
+    next.full.ensure(size_t(fin.n_new) + 64);
+    PB_DISPATCH_WS(W, inc_shard_table_kernel<W><<<grid_for(uint64_t(n) + fin.side_total), NT, 0, stream>>>(
+                          n, m, m, dist, old.words.as<uint32_t>(), inc_side_keys[scur].as<uint32_t>(),
+                          inc_side_gap[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), add, vs, ictr,
+                          next.words.as<uint32_t>(), next.full.as<uint8_t>()));
+    check_launch();
+    next.n = fin.n_new;
+    next.q_nom = kept_global;
+    next.order = m;
+    next.has_full = true;
+    ++inc_steps;
+    inc_side_keys_total += fin.side_total;
+    inc_expanded_total += fin.expanded_total;
+    (void)c;
+    PB_CUDA(cudaEventRecord(ev[2], stream));
+    assemble_sharded(next);
+    return true;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -425,6 +597,7 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
     const uint64_t support = sc.support;
     if (norm2_out) *norm2_out = norm2;
     if (support == 0) throw PacesError("truncate_select: state has no support");
+    last_kept_global = std::min<uint64_t>(support, q_nom);
 
     uint32_t* keep = flag_keep.as<uint32_t>();
     if (support <= q_nom) {

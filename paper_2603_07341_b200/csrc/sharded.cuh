@@ -5,6 +5,7 @@
 // reductions whose global value needs an all-reduce.
 #pragma once
 #include "kernels.cuh"
+#include "incremental.cuh"
 
 namespace pb {
 
@@ -329,6 +330,170 @@ static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uin
                     }
                 }
             }
+        }
+    }
+}
+
+// ================================================================================================
+// Incremental TABLE growth on a shard (the expansion half of incremental.cuh, across ranks).  T_new = {k : dist(k, S)
+// <= m}: the kept keys S are a subset of the previous table and the previous H_eff lists every edge among its keys on
+// BOTH ranks of an edge, so the ball is grown in old index space: a row pulls through its CSR columns, halo columns
+// included -- the owners' distances of the halo rows travel over the SpMV's halo lists, one byte per entry and level.
+// Only the rows whose neighbourhood was not complete in the previous space and the keys they bring in ("side" keys)
+// are expanded by key; a neighbour owned by another rank is routed to its owner, which lowers the distance of the
+// row it finds (a push: the edge of a side key is not in the old H_eff) or takes the key as a candidate.
+// ================================================================================================
+
+/// dist[i] = 0 for kept rows, DIST_INF elsewhere (n local rows + the halo slots behind them).
+static __global__ void __launch_bounds__(NT) inc_dist_from_keep_kernel(const uint32_t* __restrict__ keep, uint32_t n,
+                                                                       uint32_t n_ext, uint8_t* __restrict__ dist) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n_ext; i += gridDim.x * NT)
+        dist[i] = (i < n && keep[i]) ? uint8_t(0) : DIST_INF;
+}
+
+/// Halo pack of the distances: send[j] = dist[send_idx[j]].
+static __global__ void __launch_bounds__(NT) halo_pack_u8_kernel(const uint8_t* __restrict__ dist,
+                                                                 const uint32_t* __restrict__ send_idx, uint32_t cnt,
+                                                                 uint8_t* __restrict__ send) {
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < cnt; j += gridDim.x * NT) send[j] = dist[send_idx[j]];
+}
+
+/// inc_expand_kernel on a shard: a neighbour owned by this rank takes the local path (old table -> distance k+1; side
+/// list -> known; else candidate with its insertion gap), one owned elsewhere is appended to the outgoing list.
+template <int W>
+static __global__ void __launch_bounds__(NT) inc_expand_sharded_kernel(
+    ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n,
+    const uint32_t* __restrict__ elist, const uint32_t* __restrict__ side_keys, const uint8_t* __restrict__ side_dist, int k,
+    int nslots, uint8_t* dist, uint32_t* __restrict__ cand_keys, uint32_t* __restrict__ cand_gap, uint32_t cand_cap, int sh,
+    uint32_t* __restrict__ bucket_count, IncCounters* ctr, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_dest,
+    uint32_t out_cap, ShardCounters* sc) {
+    const uint32_t n_elist = ctr->n_expand[k], side_n = ctr->side_n[k];
+    const uint64_t total = (uint64_t(n_elist) + side_n) * uint64_t(nslots);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctr->h.expanded_total, n_elist);
+    for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
+        const uint32_t src = uint32_t(t / uint32_t(nslots));
+        const int slot = int(t - uint64_t(src) * uint32_t(nslots));
+        Key<W> key;
+        if (src < n_elist) {
+            key = load_key<W>(table + size_t(__ldg(elist + src)) * W);
+        } else {
+            const uint32_t j = src - n_elist;
+            if (side_dist[j] != uint8_t(k)) continue;
+            key = load_key<W>(side_keys + size_t(j) * W);
+        }
+        int idx = 0;
+        for_each_neighbor<W>(m, key, false, [&](int, const Key<W>& kk, double, bool) {
+            if (idx++ != slot) return;
+            const uint32_t dest = owner_of<W>(m, kk, P);
+            if (dest != rank) {
+                const uint32_t o = append_slot(&sc->n_out);
+                if (o < out_cap) {
+                    store_key<W>(out_keys + size_t(o) * W, kk);
+                    out_dest[o] = dest;
+                } else {
+                    sc->overflow = 1;
+                }
+                return;
+            }
+            uint32_t pos, spos;
+            if (find_row_in4<W>(table, 0, n, kk, pos)) {
+                if (dist[pos] > uint8_t(k + 1)) dist[pos] = uint8_t(k + 1);
+            } else if (!side_find<W>(side_keys, side_n, kk, spos)) {
+                const uint32_t c = append_slot(&ctr->n_cand[k]);
+                if (c < cand_cap) {
+                    store_key<W>(cand_keys + size_t(c) * W, kk);
+                    cand_gap[c] = pos;
+                    atomicAdd(bucket_count + (pos >> sh), 1u);
+                } else {
+                    ctr->h.overflow = 1;
+                }
+            }
+        });
+    }
+}
+
+/// Keys another rank generated at level k and this rank owns: in the old table -> that row is within k+1; in the side
+/// list -> known; else a candidate of this level.
+template <int W>
+static __global__ void __launch_bounds__(NT) inc_classify_received_kernel(
+    const uint32_t* __restrict__ table, uint32_t n, const uint32_t* __restrict__ side_keys, int k,
+    const uint32_t* __restrict__ recv, uint32_t nr, uint8_t* dist, uint32_t* __restrict__ cand_keys,
+    uint32_t* __restrict__ cand_gap, uint32_t cand_cap, int sh, uint32_t* __restrict__ bucket_count, IncCounters* ctr) {
+    const uint32_t side_n = ctr->side_n[k];
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < nr; i += gridDim.x * NT) {
+        const Key<W> kk = load_key<W>(recv + size_t(i) * W);
+        uint32_t pos, spos;
+        if (find_row_in4<W>(table, 0, n, kk, pos)) {
+            if (dist[pos] > uint8_t(k + 1)) dist[pos] = uint8_t(k + 1);
+        } else if (!side_find<W>(side_keys, side_n, kk, spos)) {
+            const uint32_t c = append_slot(&ctr->n_cand[k]);
+            if (c < cand_cap) {
+                store_key<W>(cand_keys + size_t(c) * W, kk);
+                cand_gap[c] = pos;
+                atomicAdd(bucket_count + (pos >> sh), 1u);
+            } else {
+                ctr->h.overflow = 1;
+            }
+        }
+    }
+}
+
+/// v[i] = [old row i survives] + [side keys inserted right before old row i] over i = 0..n (slot n: the side keys behind
+/// the last row); add[] keeps the second term.  The exclusive scan of v numbers the new table.
+static __global__ void __launch_bounds__(NT) inc_shard_count_kernel(uint32_t n, int m, const uint8_t* __restrict__ dist,
+                                                                    const uint32_t* __restrict__ side_gap, int levels,
+                                                                    const IncCounters* __restrict__ ctr,
+                                                                    uint32_t* __restrict__ add, uint32_t* __restrict__ v) {
+    const uint32_t side_n = ctr->side_n[levels];
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i <= n; i += gridDim.x * NT) {
+        // side keys with gap == i: [lower_bound(i), lower_bound(i + 1))
+        const uint32_t a = lower_bound_u32(side_gap, side_n, i), b = lower_bound_u32(side_gap, side_n, i + 1);
+        add[i] = b - a;
+        v[i] = (b - a) + ((i < n && dist[i] <= uint8_t(m)) ? 1u : 0u);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) v[n + 1] = 0;
+}
+
+/// Head of the counter block after the scan (over n + 2 slots, the last one zero: vscan[n + 1] is the total).
+static __global__ void inc_shard_head_kernel(uint32_t n, const uint32_t* __restrict__ vscan, int levels, IncCounters* ctr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t side_n = ctr->side_n[levels];
+    const uint32_t n_new = vscan[n + 1];
+    ctr->h.side_total = side_n;
+    ctr->h.n_new = n_new;
+    ctr->h.n_keep = n_new - side_n;
+}
+
+/// The new table: surviving old rows and side keys at their merged positions; full = the row's neighbourhood was
+/// generated (distance < m).  Old row i -> S[i] + add[i]; side key j with gap g -> S[g] + (j - first side key of gap g).
+template <int W>
+static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, int m, int levels,
+                                                                    const uint8_t* __restrict__ dist,
+                                                                    const uint32_t* __restrict__ table,
+                                                                    const uint32_t* __restrict__ side_keys,
+                                                                    const uint32_t* __restrict__ side_gap,
+                                                                    const uint8_t* __restrict__ side_dist,
+                                                                    const uint32_t* __restrict__ add,
+                                                                    const uint32_t* __restrict__ S,
+                                                                    const IncCounters* __restrict__ ctr,
+                                                                    uint32_t* __restrict__ words_new,
+                                                                    uint8_t* __restrict__ full_new) {
+    const uint32_t side_n = ctr->side_n[levels];
+    const uint64_t total = uint64_t(n) + side_n;
+    for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
+        if (t < n) {
+            const uint32_t i = uint32_t(t);
+            const uint8_t d = dist[i];
+            if (d > uint8_t(m)) continue;
+            const uint32_t o = S[i] + add[i];
+            store_key<W>(words_new + size_t(o) * W, load_key<W>(table + size_t(i) * W));
+            full_new[o] = d < uint8_t(m) ? 1 : 0;
+        } else {
+            const uint32_t j = uint32_t(t - n);
+            const uint32_t g = side_gap[j];
+            const uint32_t o = S[g] + (j - lower_bound_u32(side_gap, side_n, g));
+            store_key<W>(words_new + size_t(o) * W, load_key<W>(side_keys + size_t(j) * W));
+            full_new[o] = side_dist[j] < uint8_t(m) ? 1 : 0;
         }
     }
 }

@@ -79,7 +79,8 @@ def main():
         allsizes = [None] * world
         dist.all_gather_object(allsizes, sizes[-1] if sizes else 0)
         report[name] = dict(steps=len(sizes), shard_rows=allsizes, transport=ctx.comm_describe(),
-                            calls=dict(getattr(comm, "calls", {})), deferred=run.times()["taylor_deferred"])
+                            calls=dict(getattr(comm, "calls", {})), deferred=run.times()["taylor_deferred"],
+                            adapt=ctx.adapt_stats())
     if rank == 0:
         print("SHARDED_OK " + json.dumps(report), flush=True)
     dist.barrier()

@@ -34,6 +34,17 @@ def test_two_ranks_selection_full_pass_fallback():
 
 
 @pytest.mark.gpu
+def test_two_ranks_full_expansion_equals_incremental_growth():
+    """PB200_NO_INCREMENTAL=1: every step grows its table by the full expansion from the kept keys (the path a buffer
+    overflow of the incremental growth falls back to); same trajectories."""
+    out = _launch(2, "cfg1_holstein_L4_d8,cube_2x2x2_d16", 12, 29618, env={"PB200_NO_INCREMENTAL": "1"})
+    import json
+
+    rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
+    assert all(v["adapt"]["incremental_steps"] == 0 for v in rep.values()), rep
+
+
+@pytest.mark.gpu
 def test_three_and_four_ranks_match_oracle():
     _launch(3, "ties_holstein_L5_d6,square_3x3_d5", 25, 29612)
     _launch(4, "cfg2_layout_L16_d16_small,substeps_L4_d4_m1,tb_chain_31", 20, 29613)
@@ -49,6 +60,9 @@ def test_eight_ranks_match_oracle():
     rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
     assert all(len(v["shard_rows"]) == 8 for v in rep.values())
     assert any(v["deferred"] > 0 for v in rep.values()), rep
+    # the table of every step after the first grew incrementally from the previous space (no fallback to the full path)
+    for v in rep.values():
+        assert v["adapt"]["incremental_steps"] >= v["steps"] - 1 and v["adapt"]["fallbacks"] == 0, rep
 
 
 @pytest.mark.gpu
