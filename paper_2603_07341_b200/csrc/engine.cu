@@ -1018,6 +1018,7 @@ void Engine::run_step(pb200_diag* out) {
                                   : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
                                            !incremental);
         rec.norm_pre = std::sqrt(n2_pre);
+        bool shard_remapped = false;  // shards: the incremental table growth also remapped the coefficients (into term[0])
         PB_CUDA(cudaEventRecord(ev[1], stream));
         // (the incremental path remaps the coefficients straight into term[0], the first Taylor order's input)
         if (incremental && !grow_incremental(old, c_old, kept, cfg.m, next, term[0])) {
@@ -1036,7 +1037,8 @@ void Engine::run_step(pb200_diag* out) {
             // previous space when it can (sharded.cu); a buffer bound hit on any rank sends every rank to the full path
             const bool inc_shard = old.has_h && old.has_full && cfg.m >= 1 && cfg.m <= INC_MAX_ORDER && md.max_deg + md.kind > 0 &&
                                    memory_cap_bytes() == 0 && std::getenv("PB200_NO_INCREMENTAL") == nullptr;
-            if (!(inc_shard && grow_incremental_sharded(old, last_kept_global, cfg.m, next))) {
+            shard_remapped = inc_shard && grow_incremental_sharded(old, c_old, last_kept_global, cfg.m, next, term[0]);
+            if (!shard_remapped) {
                 if (inc_shard) ++inc_fallbacks;
                 grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
             }
@@ -1073,14 +1075,27 @@ void Engine::run_step(pb200_diag* out) {
             // which also yields <H>, the norm and the finiteness check (no separate SpMV + halo exchange for <H>, no
             // copy of the state)
             shard_fused = true;
-            term[0].ensure((size_t(next.n) + next.halo_n) * 16 + 16);
-            rec.discarded_weight = remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n,
-                                         term[0].as<double2>());
+            if (shard_remapped) {
+                // the incremental table growth already moved the coefficients into term[0] (index map, no key search)
+                const size_t ext_bytes = (size_t(next.n) + next.halo_n) * 16 + 16;
+                if (ext_bytes > term[0].cap) sync();  // (the copy of a growing buffer is not stream-ordered)
+                term[0].ensure_keep(ext_bytes, size_t(next.n) * 16);
+                rec.discarded_weight = allreduce_host(read_back<double>(dctl()->out));
+            } else {
+                term[0].ensure((size_t(next.n) + next.halo_n) * 16 + 16);
+                rec.discarded_weight = remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n,
+                                             term[0].as<double2>());
+            }
             PB_CUDA(cudaEventRecord(ev[4], stream));
             PB_CUDA(cudaEventRecord(ev[5], stream));
         } else {
-            rec.discarded_weight =
-                remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+            if (shard_remapped) {  // (row-list Taylor kernels: the state is expected in psi)
+                PB_CUDA(cudaMemcpyAsync(psi, term[0].p, size_t(next.n) * 16, cudaMemcpyDeviceToDevice, stream));
+                rec.discarded_weight = allreduce_host(read_back<double>(dctl()->out));
+            } else {
+                rec.discarded_weight =
+                    remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n, psi);
+            }
             PB_CUDA(cudaEventRecord(ev[4], stream));
             expectation(next, psi, &e, &n2, true);
             PB_CUDA(cudaEventRecord(ev[5], stream));

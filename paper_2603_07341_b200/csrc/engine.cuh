@@ -264,7 +264,9 @@ struct Engine {
     void grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out);
     void assemble_sharded(Space& sp);
     /// incremental table growth on shards (sharded.cu); collective, false on every rank = take the full path
-    bool grow_incremental_sharded(const Space& old, uint64_t kept_global, int m, Space& next);
+    /// (the coefficients are remapped into c_new on the way, discarded weight -> Ctl::out[0])
+    bool grow_incremental_sharded(const Space& old, const double2* c_old, uint64_t kept_global, int m, Space& next,
+                                  DevBuf& c_new);
     uint64_t last_kept_global = 0;  // rows select_sharded kept over all ranks
     uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
                             double* norm2_out);

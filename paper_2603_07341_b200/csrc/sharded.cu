@@ -247,7 +247,8 @@ void Engine::grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space
 // on a shard"); H_eff of the new table is then assembled the usual way.  Collective; returns false on every rank when
 // any rank hit a buffer bound (the caller then runs grow_sharded from the kept keys).
 // ------------------------------------------------------------------------------------------------
-bool Engine::grow_incremental_sharded(const Space& old, uint64_t kept_global, int m, Space& next) {
+bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, uint64_t kept_global, int m, Space& next,
+                                      DevBuf& c_new) {
     const int W = md.W;
     const uint32_t P = uint32_t(world);
     const uint32_t n = old.n;
@@ -391,6 +392,16 @@ bool Engine::grow_incremental_sharded(const Space& old, uint64_t kept_global, in
                           inc_side_gap[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), add, vs, ictr,
                           next.words.as<uint32_t>(), next.full.as<uint8_t>()));
     check_launch();
+    // the coefficients move with their rows (remap_state); the discarded weight lands in Ctl::out[0].  Room for a halo
+    // of the previous size behind the rows: the first Taylor order reads the vector from here
+    c_new.ensure((size_t(fin.n_new) + old.halo_n + old.halo_n / 4 + 1024) * 16 + 16);
+    {
+        const int rg = grid_for(uint64_t(n) + fin.side_total);
+        if (size_t(rg) * 8 > partials.cap) throw CudaFail("internal error: reduction scratch too small for the grid");
+        inc_shard_remap_kernel<<<rg, NT, 0, stream>>>(n, m, m, dist, inc_side_gap[scur].as<uint32_t>(), add, vs, ictr, c_old,
+                                                      c_new.as<double2>(), partials.as<double>(), &c->ticket, c->out);
+        check_launch();
+    }
     next.n = fin.n_new;
     next.q_nom = kept_global;
     next.order = m;
@@ -398,7 +409,6 @@ bool Engine::grow_incremental_sharded(const Space& old, uint64_t kept_global, in
     ++inc_steps;
     inc_side_keys_total += fin.side_total;
     inc_expanded_total += fin.expanded_total;
-    (void)c;
     PB_CUDA(cudaEventRecord(ev[2], stream));
     assemble_sharded(next);
     return true;

@@ -498,6 +498,41 @@ static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, 
     }
 }
 
+/// remap_state (subspace.hpp:281-305) through the same index arithmetic: the coefficient of a surviving old row moves
+/// to its new position, a side key starts at zero, a dropped row adds |c|^2 to the discarded weight (per-CTA partials
+/// combined in CTA order -> out[0]).
+static __global__ void __launch_bounds__(NT) inc_shard_remap_kernel(uint32_t n, int m, int levels,
+                                                                    const uint8_t* __restrict__ dist,
+                                                                    const uint32_t* __restrict__ side_gap,
+                                                                    const uint32_t* __restrict__ add,
+                                                                    const uint32_t* __restrict__ S,
+                                                                    const IncCounters* __restrict__ ctr,
+                                                                    const double2* __restrict__ c_old,
+                                                                    double2* __restrict__ c_new,
+                                                                    double* __restrict__ partials, unsigned* ticket,
+                                                                    double* __restrict__ out) {
+    __shared__ double smem[NT / 32];
+    const uint32_t side_n = ctr->side_n[levels];
+    const uint64_t total = uint64_t(n) + side_n;
+    double acc[1] = {0.0};
+    for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
+        if (t < n) {
+            const uint32_t i = uint32_t(t);
+            const double2 x = c_old[i];
+            if (dist[i] <= uint8_t(m))
+                c_new[S[i] + add[i]] = x;
+            else
+                acc[0] = __dadd_rn(acc[0], __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)));
+        } else {
+            const uint32_t j = uint32_t(t - n);
+            const uint32_t g = side_gap[j];
+            c_new[S[g] + (j - lower_bound_u32(side_gap, side_n, g))] = make_double2(0.0, 0.0);
+        }
+    }
+    double tot[1];
+    if (grid_sum<1>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) out[0] = tot[0];
+}
+
 /// Halo pack: send[j] = x[send_idx[j]].
 static __global__ void __launch_bounds__(NT) halo_pack_kernel(const double2* __restrict__ x,
                                                        const uint32_t* __restrict__ send_idx, uint32_t cnt,
