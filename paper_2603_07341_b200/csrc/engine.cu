@@ -300,6 +300,7 @@ void Engine::set_model(const HostModel& m) {
     space[0].n = space[1].n = 0;
     space[0].has_h = space[1].has_h = false;
     space[0].has_full = space[1].has_full = false;
+    space[0].has_move = space[1].has_move = false;
     if (m.W > 16) throw PacesError("basis keys wider than 16 words (512 bits) are not supported by this build");
 }
 

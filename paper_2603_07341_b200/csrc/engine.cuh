@@ -141,6 +141,9 @@ struct Space {
     uint32_t n_interior = 0, n_boundary = 0;
     DevBuf rows_int, rows_bnd;
     bool row_lists = false;
+    // sharded assembly: the neighbour generator's move id of every CSR entry (the hint of the next step's assembly)
+    DevBuf move;
+    bool has_move = false;
 };
 
 struct Engine {
@@ -227,7 +230,7 @@ struct Engine {
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     DevBuf row_class, scan_aligned;
     DevBuf out_keys, out_dest, route_pos, route_ctr, sendbuf, recvbuf, req_keys, req_dest, req_pos, reply, answer,
-        found, halo_flag, tmp_cnt, halo_stage, sel_keys, sel_stage, asm_info;
+        found, halo_flag, tmp_cnt, tmp_move, halo_stage, sel_keys, sel_stage, asm_info;
     std::vector<uint64_t> h_send, h_recv;
 
     explicit Engine(int dev);
@@ -262,7 +265,8 @@ struct Engine {
     void halo_wait();
     void classify_rows(Space& sp);
     void grow_sharded(const uint32_t* d_seeds, uint32_t ns, int order, Space& out);
-    void assemble_sharded(Space& sp);
+    /// hint != nullptr: the table grew incrementally from the previous space (sharded.cuh, AsmHint)
+    void assemble_sharded(Space& sp, const AsmHint* hint = nullptr);
     /// incremental table growth on shards (sharded.cu); collective, false on every rank = take the full path
     /// (the coefficients are remapped into c_new on the way, discarded weight -> Ctl::out[0])
     bool grow_incremental_sharded(const Space& old, const double2* c_old, uint64_t kept_global, int m, Space& next,

@@ -387,11 +387,33 @@ bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, ui
     if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     next.words.ensure(size_t(fin.n_new) * W * 4 + 64);
     next.full.ensure(size_t(fin.n_new) + 64);
+    inc_inv.ensure(size_t(fin.n_new) * 4 + 4);  // origin of every new row
     PB_DISPATCH_WS(W, inc_shard_table_kernel<W><<<grid_for(uint64_t(n) + fin.side_total), NT, 0, stream>>>(
                           n, m, m, dist, old.words.as<uint32_t>(), inc_side_keys[scur].as<uint32_t>(),
                           inc_side_gap[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), add, vs, ictr,
-                          next.words.as<uint32_t>(), next.full.as<uint8_t>()));
+                          next.words.as<uint32_t>(), next.full.as<uint8_t>(), inc_inv.as<uint32_t>()));
     check_launch();
+    // the assembly hint: surviving rows next to a local side key are searched, the others read the previous H_eff
+    AsmHint hint{};
+    const bool hinted = old.has_move && std::getenv("PB200_NO_ASSEMBLY_HINT") == nullptr;
+    if (hinted) {
+        inc_has_extra.ensure(size_t(n) + 64);
+        uint8_t* touched = inc_has_extra.as<uint8_t>();
+        PB_CUDA(cudaMemsetAsync(touched, 0, size_t(n) + 1, stream));
+        if (fin.side_total && nmoves) {
+            PB_DISPATCH_WS(W, inc_shard_touch_kernel<W><<<small_grid, NT, 0, stream>>>(
+                                  md, uint32_t(rank), P, old.words.as<uint32_t>(), n, m, m, dist,
+                                  inc_side_keys[scur].as<uint32_t>(), nmoves, touched, ictr));
+            check_launch();
+        }
+        hint.origin = inc_inv.as<uint32_t>();
+        hint.touched = touched;
+        hint.newidx = add;  // (converted in place once the remap below has used the counts)
+        hint.row_ptr = old.row_ptr.as<uint32_t>();
+        hint.col = old.col.as<int32_t>();
+        hint.move = old.move.as<uint8_t>();
+        hint.n_old = n;
+    }
     // the coefficients move with their rows (remap_state); the discarded weight lands in Ctl::out[0].  Room for a halo
     // of the previous size behind the rows: the first Taylor order reads the vector from here
     c_new.ensure((size_t(fin.n_new) + old.halo_n + old.halo_n / 4 + 1024) * 16 + 16);
@@ -402,6 +424,10 @@ bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, ui
                                                       c_new.as<double2>(), partials.as<double>(), &c->ticket, c->out);
         check_launch();
     }
+    if (hinted && n) {
+        inc_shard_newidx_kernel<<<grid_for(n), NT, 0, stream>>>(n, m, dist, vs, add);
+        check_launch();
+    }
     next.n = fin.n_new;
     next.q_nom = kept_global;
     next.order = m;
@@ -410,14 +436,14 @@ bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, ui
     inc_side_keys_total += fin.side_total;
     inc_expanded_total += fin.expanded_total;
     PB_CUDA(cudaEventRecord(ev[2], stream));
-    assemble_sharded(next);
+    assemble_sharded(next, hinted ? &hint : nullptr);
     return true;
 }
 
 // ------------------------------------------------------------------------------------------------
 // row-wise assembly on shards + halo plan
 // ------------------------------------------------------------------------------------------------
-void Engine::assemble_sharded(Space& sp) {
+void Engine::assemble_sharded(Space& sp, const AsmHint* hint) {
     const int W = md.W;
     const uint32_t P = uint32_t(world);
     const uint32_t n = sp.n;
@@ -426,6 +452,7 @@ void Engine::assemble_sharded(Space& sp) {
     tmp_col.ensure(size_t(n) * width * 4 + 4);
     tmp_val.ensure(size_t(n) * width * 8 + 8);
     tmp_cnt.ensure(size_t(n) * 4 + 4);
+    tmp_move.ensure(size_t(n) * width + 4);
     sp.row_ptr.ensure((size_t(n) + 1) * 4 + CSR_PAD);
     const uint64_t req_cap64 = uint64_t(n) * uint64_t(width) + 1;
     if (req_cap64 > 0x7ffffff0ull) throw PacesError("assembly: request count exceeds 31-bit indexing");
@@ -437,10 +464,17 @@ void Engine::assemble_sharded(Space& sp) {
     ShardCounters* dsc = &route_block()->sc;
     PB_CUDA(cudaMemsetAsync(dsc, 0, sizeof(ShardCounters), stream));
     const uint32_t achunk = chunk_for(n);
-    if (n) {
+    if (n && hint != nullptr) {
+        // the table grew incrementally: rows that survived untouched take their local columns from the previous H_eff
+        PB_DISPATCH_WS(W, assemble_rows_hinted_sharded_kernel<W><<<grid_for(n), NT, 0, stream>>>(
+                              md, uint32_t(rank), P, sp.words.as<uint32_t>(), n, width, *hint, tmp_col.as<uint32_t>(),
+                              tmp_val.as<double>(), tmp_move.as<uint8_t>(), tmp_cnt.as<uint32_t>(), req_keys.as<uint32_t>(),
+                              req_dest.as<uint32_t>(), req_cap, dsc));
+        check_launch();
+    } else if (n) {
         PB_DISPATCH_WS(W, assemble_rows_sharded_kernel<W><<<grid_chunked(n, achunk), NT, 0, stream>>>(
                               md, uint32_t(rank), P, sp.words.as<uint32_t>(), n, achunk, width, tmp_col.as<uint32_t>(),
-                              tmp_val.as<double>(), tmp_cnt.as<uint32_t>(), req_keys.as<uint32_t>(),
+                              tmp_val.as<double>(), tmp_move.as<uint8_t>(), tmp_cnt.as<uint32_t>(), req_keys.as<uint32_t>(),
                               req_dest.as<uint32_t>(), req_cap, dsc));
         check_launch();
     }
@@ -494,7 +528,8 @@ void Engine::assemble_sharded(Space& sp) {
     check_launch();
     exclusive_scan(halo_flag.as<uint32_t>(), uint64_t(nreq) + 1);
     resolve_requests_kernel<<<grid_for(n), NT, 0, stream>>>(n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(),
-                                                            tmp_cnt.as<uint32_t>(), req_pos.as<uint32_t>(),
+                                                            tmp_move.as<uint8_t>(), tmp_cnt.as<uint32_t>(),
+                                                            req_pos.as<uint32_t>(),
                                                             reply.as<uint32_t>(), halo_flag.as<uint32_t>(),
                                                             sp.row_ptr.as<uint32_t>());
     check_launch();
@@ -516,6 +551,7 @@ void Engine::assemble_sharded(Space& sp) {
     const uint32_t nnz = info.halo_at[65];
     sp.col.ensure(size_t(nnz) * 4 + CSR_PAD);
     sp.val.ensure(size_t(nnz) * 8 + CSR_PAD);
+    sp.move.ensure(size_t(nnz) + CSR_PAD);  // the generator's move id of every entry (the next step's assembly hint)
     // value codes for the Taylor tile kernels, produced by the compaction itself (no pass of their own)
     const bool tiles = taylor_tiles_usable(width);
     const bool want_codes = tiles && use_codes && md.vt_n > 0;
@@ -526,8 +562,8 @@ void Engine::assemble_sharded(Space& sp) {
         PB_CUDA(cudaMemsetAsync(fail, 0, 4, stream));
     }
     assemble_compact_sharded_kernel<<<grid_for(n), NT, 0, stream>>>(
-        n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(), sp.row_ptr.as<uint32_t>(), sp.col.as<int32_t>(),
-        sp.val.as<double>(), md.vtab, md.vt_n, md.vt_diag,
+        n, width, tmp_col.as<uint32_t>(), tmp_val.as<double>(), tmp_move.as<uint8_t>(), sp.row_ptr.as<uint32_t>(),
+        sp.col.as<int32_t>(), sp.val.as<double>(), sp.move.as<uint8_t>(), md.vtab, md.vt_n, md.vt_diag,
         want_codes ? sp.code.as<uint16_t>() : nullptr, sp.diag.as<double>(), fail);
     check_launch();
     sp.nnz = nnz;
@@ -535,6 +571,7 @@ void Engine::assemble_sharded(Space& sp) {
     sp.has_h = true;
     sp.val_valid = true;
     sp.has_code = want_codes && read_back<uint32_t>(fail) == 0;
+    sp.has_move = true;
     // the tile kernels tell rows without / with halo columns apart themselves; the row-list kernels need the lists
     sp.n_interior = sp.n_boundary = 0;
     sp.row_lists = false;

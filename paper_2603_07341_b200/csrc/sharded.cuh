@@ -19,6 +19,13 @@ struct ShardCounters {
     uint32_t pad;
 };
 
+/// Owner of a neighbour generated from a key THIS rank owns: a hop only rewrites the exciton register, which the
+/// ownership hash ignores (owner_of, keys.cuh), so the neighbour stays here; only the ladder moves need the hash.
+template <int W>
+__device__ __forceinline__ uint32_t neighbor_owner(const ModelDev& m, int move, const Key<W>& kk, uint32_t rank, uint32_t P) {
+    return move < MAX_NB ? rank : owner_of<W>(m, kk, P);
+}
+
 /// Expansion of one BFS order on a shard.  Neighbours owned by this rank take the local path of
 /// expand_window_kernel (look-up, candidate + gap when absent); the others are appended to the outgoing list
 /// with their destination rank.
@@ -37,7 +44,7 @@ static __global__ void __launch_bounds__(NT) expand_level_sharded_kernel(
         const uint32_t e = exciton_site<W>(m, k);
         if (e != cur.site) cur.reset(e);
         for_each_neighbor<W>(m, k, false, [&](int move, const Key<W>& kk, double, bool) {
-            const uint32_t dest = owner_of<W>(m, kk, P);
+            const uint32_t dest = neighbor_owner<W>(m, move, kk, rank, P);
             if (dest == rank) {
                 uint32_t pos;
                 if (!cursor_find<W>(table, n, cur, move, kk, pos)) {
@@ -157,8 +164,9 @@ static __global__ void __launch_bounds__(NT) classify_received_kernel(const uint
 template <int W>
 static __global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
     ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n, uint32_t chunk, int width,
-    uint32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, uint32_t* __restrict__ tmp_cnt,
-    uint32_t* __restrict__ req_keys, uint32_t* __restrict__ req_dest, uint32_t req_cap, ShardCounters* sc) {
+    uint32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, uint8_t* __restrict__ tmp_move,
+    uint32_t* __restrict__ tmp_cnt, uint32_t* __restrict__ req_keys, uint32_t* __restrict__ req_dest, uint32_t req_cap,
+    ShardCounters* sc) {
     const uint64_t wbase = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32ull * chunk + (threadIdx.x & 31);
     MoveCursors cur;
     cur.reset(0xffffffffu);
@@ -170,11 +178,12 @@ static __global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
         int len = 0;
         uint32_t* tc = tmp_col + size_t(i) * width;
         double* tv = tmp_val + size_t(i) * width;
+        uint8_t* tm = tmp_move + size_t(i) * width;
         for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
             uint32_t pos = i;
             bool keep = true;
             if (!is_diag) {
-                const uint32_t dest = owner_of<W>(m, kk, P);
+                const uint32_t dest = neighbor_owner<W>(m, move, kk, rank, P);
                 if (dest == rank) {
                     keep = cursor_find<W>(table, n, cur, move, kk, pos);
                 } else {
@@ -191,6 +200,117 @@ static __global__ void __launch_bounds__(NT) assemble_rows_sharded_kernel(
             if (keep) {
                 tc[len] = pos;
                 tv[len] = amp;
+                tm[len] = uint8_t(move);
+                ++len;
+            }
+        });
+        tmp_cnt[i] = uint32_t(len);
+    }
+}
+
+/// What the incremental table growth leaves behind for the assembly of the new table (Engine::grow_incremental_sharded):
+/// where every new row came from, the previous space's CSR with the generator's move id of every entry, and the index
+/// arithmetic old row -> new row.
+struct AsmHint {
+    const uint32_t* origin;    // [n_new] old row index, or ORIGIN_SIDE | side index
+    const uint8_t* touched;    // [n_old] 1: the row has a local side key among its neighbours (its row is searched)
+    const uint32_t* newidx;    // [n_old] new index of a surviving old row, IDX_NONE for a dropped one
+    const uint32_t* row_ptr;   // previous space: CSR of the local rows ...
+    const int32_t* col;
+    const uint8_t* move;       // ... and the move id of every entry
+    uint32_t n_old;
+};
+constexpr uint32_t ORIGIN_SIDE = 0x80000000u;
+
+/// Marks the surviving old rows that have a LOCAL side key among their neighbours: one thread per (side key, move).
+/// (Side keys of other ranks reach a row through the look-up requests, which every row issues for all its remote
+/// neighbours anyway.)
+template <int W>
+static __global__ void __launch_bounds__(NT) inc_shard_touch_kernel(ModelDev m, uint32_t rank, uint32_t P,
+                                                                    const uint32_t* __restrict__ table, uint32_t n, int order,
+                                                                    int levels, const uint8_t* __restrict__ dist,
+                                                                    const uint32_t* __restrict__ side_keys, int nslots,
+                                                                    uint8_t* __restrict__ touched,
+                                                                    const IncCounters* __restrict__ ctr) {
+    const uint32_t side_n = ctr->side_n[levels];
+    const uint64_t total = uint64_t(side_n) * uint32_t(nslots);
+    for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
+        const uint32_t j = uint32_t(t / uint32_t(nslots));
+        const int slot = int(t - uint64_t(j) * uint32_t(nslots));
+        const Key<W> key = load_key<W>(side_keys + size_t(j) * W);
+        int idx = 0;
+        for_each_neighbor<W>(m, key, false, [&](int move, const Key<W>& kk, double, bool) {
+            if (idx++ != slot) return;
+            if (neighbor_owner<W>(m, move, kk, rank, P) != rank) return;
+            uint32_t pos;
+            if (find_row_in4<W>(table, 0, n, kk, pos) && dist[pos] <= uint8_t(order)) touched[pos] = 1;
+        });
+    }
+}
+
+/// Assembly pass 1 on a shard WITH the previous space as a hint, one thread per row of the new table.  A row that
+/// survived from the previous table and has no local side key among its neighbours needs NO search: the previous
+/// H_eff lists every local neighbour it had, tagged with the generator's move id, and the neighbour's new index is
+/// index arithmetic (S[j] + add[j] when it survived).  Side keys and touched rows search the new table.  Neighbours
+/// owned by other ranks become look-up requests exactly as in assemble_rows_sharded_kernel; same scratch layout.
+template <int W>
+static __global__ void __launch_bounds__(NT) assemble_rows_hinted_sharded_kernel(
+    ModelDev m, uint32_t rank, uint32_t P, const uint32_t* __restrict__ table, uint32_t n, int width, AsmHint h,
+    uint32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, uint8_t* __restrict__ tmp_move,
+    uint32_t* __restrict__ tmp_cnt, uint32_t* __restrict__ req_keys, uint32_t* __restrict__ req_dest, uint32_t req_cap,
+    ShardCounters* sc) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+        const Key<W> k = load_key<W>(table + size_t(i) * W);
+        const uint32_t org = __ldg(h.origin + i);
+        const bool hinted = !(org & ORIGIN_SIDE) && !__ldg(h.touched + org);
+        // the previous row lists, in generator order, the neighbours that were in the previous table (any rank): one
+        // cursor walks it beside the generator
+        uint32_t oe = 0, oend = 0;
+        if (hinted) {
+            oe = __ldg(h.row_ptr + org);
+            oend = __ldg(h.row_ptr + org + 1);
+        }
+        int len = 0;
+        uint32_t* tc = tmp_col + size_t(i) * width;
+        double* tv = tmp_val + size_t(i) * width;
+        uint8_t* tm = tmp_move + size_t(i) * width;
+        for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
+            uint32_t pos = i;
+            bool keep = true;
+            bool was = false;  // hinted rows: this neighbour had an entry in the previous row
+            uint32_t ocol = 0;
+            if (hinted && oe < oend && int(__ldg(h.move + oe)) == move) {
+                was = true;
+                ocol = uint32_t(__ldg(h.col + oe));
+                ++oe;
+            }
+            if (!is_diag) {
+                const uint32_t dest = neighbor_owner<W>(m, move, kk, rank, P);
+                if (dest == rank) {
+                    if (hinted) {
+                        keep = false;
+                        if (was) {
+                            pos = __ldg(h.newidx + ocol);
+                            keep = pos != IDX_NONE;
+                        }
+                    } else {
+                        keep = find_row_in4<W>(table, 0, n, kk, pos);
+                    }
+                } else {
+                    const uint32_t r = append_slot(&sc->n_req);
+                    if (r < req_cap) {
+                        store_key<W>(req_keys + size_t(r) * W, kk);
+                        req_dest[r] = dest;
+                    } else {
+                        sc->overflow = 1;
+                    }
+                    pos = COL_REQ | r;
+                }
+            }
+            if (keep) {
+                tc[len] = pos;
+                tv[len] = amp;
+                tm[len] = uint8_t(move);
                 ++len;
             }
         });
@@ -251,6 +371,7 @@ static __global__ void __launch_bounds__(NT) reply_flags_kernel(const uint32_t* 
 /// row's scratch: afterwards the first row_len[i] scratch entries of row i are its CSR entries, in neighbour-key order.
 static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n, int width, uint32_t* __restrict__ tmp_col,
                                                               double* __restrict__ tmp_val,
+                                                              uint8_t* __restrict__ tmp_move,
                                                               const uint32_t* __restrict__ tmp_cnt,
                                                               const uint32_t* __restrict__ req_pos,
                                                               const uint32_t* __restrict__ reply,
@@ -259,17 +380,22 @@ static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n,
     for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
         uint32_t* tc = tmp_col + size_t(i) * width;
         double* tv = tmp_val + size_t(i) * width;
+        uint8_t* tm = tmp_move + size_t(i) * width;
         const uint32_t cnt = tmp_cnt[i];
         uint32_t len = 0;
         for (uint32_t s = 0; s < cnt; ++s) {
-            uint32_t c = tc[s];
+            const uint32_t c0 = tc[s];
+            uint32_t c = c0;
             if (c != COL_ABSENT && (c & COL_REQ)) {
                 const uint32_t p = req_pos[c & ~COL_REQ];
                 c = (reply[p] != COL_ABSENT) ? n + halo_slot[p] : COL_ABSENT;
             }
             if (c != COL_ABSENT) {
-                tc[len] = c;
-                if (len != s) tv[len] = tv[s];
+                if (c != c0 || len != s) tc[len] = c;
+                if (len != s) {
+                    tv[len] = tv[s];
+                    tm[len] = tm[s];
+                }
                 ++len;
             }
         }
@@ -285,9 +411,11 @@ static __global__ void __launch_bounds__(NT) resolve_requests_kernel(uint32_t n,
 static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uint32_t n, int width,
                                                                       const uint32_t* __restrict__ tmp_col,
                                                                       const double* __restrict__ tmp_val,
+                                                                      const uint8_t* __restrict__ tmp_move,
                                                                       const uint32_t* __restrict__ row_ptr,
                                                                       int32_t* __restrict__ col,
                                                                       double* __restrict__ val,
+                                                                      uint8_t* __restrict__ move,
                                                                       const double* __restrict__ vtab, int vt_n,
                                                                       int vt_diag, uint16_t* __restrict__ code,
                                                                       double* __restrict__ diag,
@@ -316,6 +444,7 @@ static __global__ void __launch_bounds__(NT) assemble_compact_sharded_kernel(uin
                 const double v = __ldg(tmp_val + src);
                 col[target] = int32_t(cc);
                 val[target] = v;
+                move[target] = __ldg(tmp_move + src);
                 if (code != nullptr) {
                     if (!vt_diag && cc == uint32_t(base + r)) {
                         diag[base + r] = v;
@@ -382,9 +511,9 @@ static __global__ void __launch_bounds__(NT) inc_expand_sharded_kernel(
             key = load_key<W>(side_keys + size_t(j) * W);
         }
         int idx = 0;
-        for_each_neighbor<W>(m, key, false, [&](int, const Key<W>& kk, double, bool) {
+        for_each_neighbor<W>(m, key, false, [&](int move, const Key<W>& kk, double, bool) {
             if (idx++ != slot) return;
-            const uint32_t dest = owner_of<W>(m, kk, P);
+            const uint32_t dest = neighbor_owner<W>(m, move, kk, rank, P);
             if (dest != rank) {
                 const uint32_t o = append_slot(&sc->n_out);
                 if (o < out_cap) {
@@ -477,7 +606,8 @@ static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, 
                                                                     const uint32_t* __restrict__ S,
                                                                     const IncCounters* __restrict__ ctr,
                                                                     uint32_t* __restrict__ words_new,
-                                                                    uint8_t* __restrict__ full_new) {
+                                                                    uint8_t* __restrict__ full_new,
+                                                                    uint32_t* __restrict__ origin) {
     const uint32_t side_n = ctr->side_n[levels];
     const uint64_t total = uint64_t(n) + side_n;
     for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
@@ -488,12 +618,14 @@ static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, 
             const uint32_t o = S[i] + add[i];
             store_key<W>(words_new + size_t(o) * W, load_key<W>(table + size_t(i) * W));
             full_new[o] = d < uint8_t(m) ? 1 : 0;
+            origin[o] = i;
         } else {
             const uint32_t j = uint32_t(t - n);
             const uint32_t g = side_gap[j];
             const uint32_t o = S[g] + (j - lower_bound_u32(side_gap, side_n, g));
             store_key<W>(words_new + size_t(o) * W, load_key<W>(side_keys + size_t(j) * W));
             full_new[o] = side_dist[j] < uint8_t(m) ? 1 : 0;
+            origin[o] = ORIGIN_SIDE | j;
         }
     }
 }
@@ -531,6 +663,13 @@ static __global__ void __launch_bounds__(NT) inc_shard_remap_kernel(uint32_t n, 
     }
     double tot[1];
     if (grid_sum<1>(acc, partials, ticket, tot, smem) && threadIdx.x == 0) out[0] = tot[0];
+}
+
+/// add[i] -> new index of old row i (IDX_NONE when it was dropped): the assembly hint needs one gather per column.
+static __global__ void __launch_bounds__(NT) inc_shard_newidx_kernel(uint32_t n, int m, const uint8_t* __restrict__ dist,
+                                                                     const uint32_t* __restrict__ S, uint32_t* add) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT)
+        add[i] = dist[i] <= uint8_t(m) ? S[i] + add[i] : IDX_NONE;
 }
 
 /// Halo pack: send[j] = x[send_idx[j]].
