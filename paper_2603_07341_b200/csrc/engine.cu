@@ -1014,10 +1014,14 @@ void Engine::run_step(pb200_diag* out) {
         bool incremental = !sharded && (!io || io->cached) && old.has_h && old.has_full && cfg.m >= 1 &&
                            cfg.m <= INC_MAX_ORDER && memory_cap_bytes() == 0 &&
                            std::getenv("PB200_NO_INCREMENTAL") == nullptr;
-        const uint32_t kept = sharded
-                                  ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre)
-                                  : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
-                                           !incremental);
+        // (shards: the table grows incrementally from the previous space when it can -- sharded.cu; the same on every rank)
+        const bool inc_shard = sharded && old.has_h && old.has_full && cfg.m >= 1 && cfg.m <= INC_MAX_ORDER &&
+                               md.max_deg + md.kind > 0 && memory_cap_bytes() == 0 &&
+                               std::getenv("PB200_NO_INCREMENTAL") == nullptr;
+        uint32_t kept = sharded ? select_sharded(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
+                                                 !inc_shard)
+                                : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
+                                         !incremental);
         rec.norm_pre = std::sqrt(n2_pre);
         bool shard_remapped = false;  // shards: the incremental table growth also remapped the coefficients (into term[0])
         PB_CUDA(cudaEventRecord(ev[1], stream));
@@ -1036,11 +1040,12 @@ void Engine::run_step(pb200_diag* out) {
         } else if (sharded) {
             // grow() = expansion + assembly; split the timer inside via ev[2].  The table grows incrementally from the
             // previous space when it can (sharded.cu); a buffer bound hit on any rank sends every rank to the full path
-            const bool inc_shard = old.has_h && old.has_full && cfg.m >= 1 && cfg.m <= INC_MAX_ORDER && md.max_deg + md.kind > 0 &&
-                                   memory_cap_bytes() == 0 && std::getenv("PB200_NO_INCREMENTAL") == nullptr;
             shard_remapped = inc_shard && grow_incremental_sharded(old, c_old, last_kept_global, cfg.m, next, term[0]);
             if (!shard_remapped) {
-                if (inc_shard) ++inc_fallbacks;
+                if (inc_shard) {  // a buffer bound was hit on some rank: every rank takes the full expansion
+                    ++inc_fallbacks;
+                    kept = compact_kept_counted(old.words.as<uint32_t>(), old.n);
+                }
                 grow_sharded(seeds.as<uint32_t>(), kept, cfg.m, next);
             }
         } else {

@@ -272,8 +272,11 @@ struct Engine {
     bool grow_incremental_sharded(const Space& old, const double2* c_old, uint64_t kept_global, int m, Space& next,
                                   DevBuf& c_new);
     uint64_t last_kept_global = 0;  // rows select_sharded kept over all ranks
+    /// compact = false: only the keep flags (flag_keep) are produced and 0 is returned; compact_kept_counted() gathers
+    /// the kept keys later if the full expansion needs them
     uint32_t select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
-                            double* norm2_out);
+                            double* norm2_out, bool compact = true);
+    uint32_t compact_kept_counted(const uint32_t* d_words, uint32_t n);
     /// fuse_first (tile kernels only): the first order also yields <x|H|x>, |x|^2 and the non-finite count of the input
     /// state (*exp_out, *norm2_out; a non-finite coefficient throws) and takes that state from term[0], writing c only
     void expmv_sharded(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps,

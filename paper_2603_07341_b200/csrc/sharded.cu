@@ -374,21 +374,28 @@ bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, ui
     pos_a.ensure((size_t(n) + 2) * 4);       // v[] -> its exclusive scan
     uint32_t* add = inc_newidx.as<uint32_t>();
     uint32_t* vs = pos_a.as<uint32_t>();
-    inc_shard_count_kernel<<<grid_for(uint64_t(n) + 1), NT, 0, stream>>>(n, m, dist, inc_side_gap[scur].as<uint32_t>(), m, ictr,
-                                                                         add, vs);
+    PB_CUDA(cudaMemsetAsync(add, 0, (size_t(n) + 2) * 4, stream));
+    inc_shard_mark_kernel<<<small_grid, NT, 0, stream>>>(inc_side_gap[scur].as<uint32_t>(), m, ictr, add);
+    check_launch();
+    inc_shard_count_kernel<<<grid_for(uint64_t(n) + 1), NT, 0, stream>>>(n, m, dist, add, vs);
     check_launch();
     exclusive_scan(vs, uint64_t(n) + 2);
     inc_shard_head_kernel<<<1, 32, 0, stream>>>(n, vs, m, ictr);
     check_launch();
     const IncHead fin = read_back<IncHead>(&ictr->h);
     if (fin.overflow) local_fail = true;
+    {
+        // test hook: rank 0 pretends to have hit a bound on every k-th step (the other ranks must follow it)
+        static const char* fe = std::getenv("PB200_SHARD_INC_FAIL_EVERY");
+        if (fe != nullptr && rank == 0 && std::atoi(fe) > 0 && steps_done % uint64_t(std::atoi(fe)) == 0) local_fail = true;
+    }
     // any rank's overflow sends every rank to the full path
     if (allreduce_host_u64(local_fail ? 1 : 0) != 0) return false;
     if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     next.words.ensure(size_t(fin.n_new) * W * 4 + 64);
     next.full.ensure(size_t(fin.n_new) + 64);
     inc_inv.ensure(size_t(fin.n_new) * 4 + 4);  // origin of every new row
-    PB_DISPATCH_WS(W, inc_shard_table_kernel<W><<<grid_for(uint64_t(n) + fin.side_total), NT, 0, stream>>>(
+    PB_DISPATCH_WS(W, inc_shard_table_kernel<W><<<grid_for(std::max<uint64_t>(n, fin.side_total)), NT, 0, stream>>>(
                           n, m, m, dist, old.words.as<uint32_t>(), inc_side_keys[scur].as<uint32_t>(),
                           inc_side_gap[scur].as<uint32_t>(), inc_side_dist[scur].as<uint8_t>(), add, vs, ictr,
                           next.words.as<uint32_t>(), next.full.as<uint8_t>(), inc_inv.as<uint32_t>()));
@@ -588,7 +595,7 @@ void Engine::assemble_sharded(Space& sp, const AsmHint* hint) {
 // truncate_select on shards: global k-th largest weight, ties drawn identically on every rank
 // ------------------------------------------------------------------------------------------------
 uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uint32_t n, uint64_t q_nom, uint64_t seed,
-                                double* norm2_out) {
+                                double* norm2_out, bool compact) {
     require_model();
     if (q_nom < 1) throw PacesError("truncate_select: q_nom must be >= 1");
     const int W = md.W;
@@ -724,7 +731,20 @@ uint32_t Engine::select_sharded(const uint32_t* d_words, const double2* d_c, uin
             sync();
         }
     }
-    pos_a.ensure((size_t(n) + 1) * 4);
+    // the kept keys themselves are only needed by the full expansion; the incremental growth works on the flags
+    if (!compact) {
+        n_seeds = 0;
+        return 0;
+    }
+    return compact_kept_counted(d_words, n);
+}
+
+/// The rows flagged in flag_keep -> this->seeds (order preserving); returns their number (one read-back).
+uint32_t Engine::compact_kept_counted(const uint32_t* d_words, uint32_t n) {
+    const int W = md.W;
+    const int g = grid_for(n);
+    uint32_t* keep = flag_keep.as<uint32_t>();
+    pos_a.ensure((size_t(n) + 2) * 4);
     PB_CUDA(cudaMemcpyAsync(pos_a.p, keep, (size_t(n) + 1) * 4, cudaMemcpyDeviceToDevice, stream));
     exclusive_scan(pos_a.as<uint32_t>(), uint64_t(n) + 1);
     if (pending_words) {

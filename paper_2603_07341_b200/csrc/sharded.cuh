@@ -567,19 +567,21 @@ static __global__ void __launch_bounds__(NT) inc_classify_received_kernel(
     }
 }
 
-/// v[i] = [old row i survives] + [side keys inserted right before old row i] over i = 0..n (slot n: the side keys behind
-/// the last row); add[] keeps the second term.  The exclusive scan of v numbers the new table.
-static __global__ void __launch_bounds__(NT) inc_shard_count_kernel(uint32_t n, int m, const uint8_t* __restrict__ dist,
-                                                                    const uint32_t* __restrict__ side_gap, int levels,
-                                                                    const IncCounters* __restrict__ ctr,
-                                                                    uint32_t* __restrict__ add, uint32_t* __restrict__ v) {
+/// add[g] = number of side keys whose insertion gap is old row g (g = 0..n; slot n: behind the last row); add[] starts
+/// at zero.
+static __global__ void __launch_bounds__(NT) inc_shard_mark_kernel(const uint32_t* __restrict__ side_gap, int levels,
+                                                                   const IncCounters* __restrict__ ctr,
+                                                                   uint32_t* __restrict__ add) {
     const uint32_t side_n = ctr->side_n[levels];
-    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i <= n; i += gridDim.x * NT) {
-        // side keys with gap == i: [lower_bound(i), lower_bound(i + 1))
-        const uint32_t a = lower_bound_u32(side_gap, side_n, i), b = lower_bound_u32(side_gap, side_n, i + 1);
-        add[i] = b - a;
-        v[i] = (b - a) + ((i < n && dist[i] <= uint8_t(m)) ? 1u : 0u);
-    }
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < side_n; j += gridDim.x * NT) atomicAdd(add + side_gap[j], 1u);
+}
+
+/// v[i] = [old row i survives] + add[i] over i = 0..n, v[n + 1] = 0.  The exclusive scan of v numbers the new table.
+static __global__ void __launch_bounds__(NT) inc_shard_count_kernel(uint32_t n, int m, const uint8_t* __restrict__ dist,
+                                                                    const uint32_t* __restrict__ add,
+                                                                    uint32_t* __restrict__ v) {
+    for (uint32_t i = blockIdx.x * NT + threadIdx.x; i <= n; i += gridDim.x * NT)
+        v[i] = add[i] + ((i < n && dist[i] <= uint8_t(m)) ? 1u : 0u);
     if (blockIdx.x == 0 && threadIdx.x == 0) v[n + 1] = 0;
 }
 
@@ -594,7 +596,9 @@ static __global__ void inc_shard_head_kernel(uint32_t n, const uint32_t* __restr
 }
 
 /// The new table: surviving old rows and side keys at their merged positions; full = the row's neighbourhood was
-/// generated (distance < m).  Old row i -> S[i] + add[i]; side key j with gap g -> S[g] + (j - first side key of gap g).
+/// generated (distance < m); origin = where the row came from (the assembly hint).  Old row i -> S[i] + add[i]; side
+/// key j with gap g -> S[g] + (j - first side key of gap g).  A warp moves the keys of 32 consecutive old rows word by
+/// word (coalesced reads; surviving neighbours land next to each other); the few side keys follow one per thread.
 template <int W>
 static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, int m, int levels,
                                                                     const uint8_t* __restrict__ dist,
@@ -608,25 +612,36 @@ static __global__ void __launch_bounds__(NT) inc_shard_table_kernel(uint32_t n, 
                                                                     uint32_t* __restrict__ words_new,
                                                                     uint8_t* __restrict__ full_new,
                                                                     uint32_t* __restrict__ origin) {
-    const uint32_t side_n = ctr->side_n[levels];
-    const uint64_t total = uint64_t(n) + side_n;
-    for (uint64_t t = uint64_t(blockIdx.x) * NT + threadIdx.x; t < total; t += uint64_t(gridDim.x) * NT) {
-        if (t < n) {
-            const uint32_t i = uint32_t(t);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (NT / 32);
+    for (uint64_t base = (uint64_t(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        uint32_t o = IDX_NONE;
+        if (i < n) {
             const uint8_t d = dist[i];
-            if (d > uint8_t(m)) continue;
-            const uint32_t o = S[i] + add[i];
-            store_key<W>(words_new + size_t(o) * W, load_key<W>(table + size_t(i) * W));
-            full_new[o] = d < uint8_t(m) ? 1 : 0;
-            origin[o] = i;
-        } else {
-            const uint32_t j = uint32_t(t - n);
-            const uint32_t g = side_gap[j];
-            const uint32_t o = S[g] + (j - lower_bound_u32(side_gap, side_n, g));
-            store_key<W>(words_new + size_t(o) * W, load_key<W>(side_keys + size_t(j) * W));
-            full_new[o] = side_dist[j] < uint8_t(m) ? 1 : 0;
-            origin[o] = ORIGIN_SIDE | j;
+            if (d <= uint8_t(m)) {
+                o = S[i] + add[i];
+                full_new[o] = d < uint8_t(m) ? 1 : 0;
+                origin[o] = uint32_t(i);
+            }
         }
+        const uint32_t rows = uint32_t(min(uint64_t(32), uint64_t(n) - base));
+        const uint32_t* src = table + size_t(base) * W;
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+            const uint32_t q = uint32_t(t) * 32 + lane;  // word q of the run of 32 keys
+            const uint32_t r = q / uint32_t(W);
+            const uint32_t dst_row = __shfl_sync(0xffffffffu, o, int(r));
+            if (r < rows && dst_row != IDX_NONE) words_new[size_t(dst_row) * W + (q - r * uint32_t(W))] = __ldg(src + q);
+        }
+    }
+    const uint32_t side_n = ctr->side_n[levels];
+    for (uint32_t j = blockIdx.x * NT + threadIdx.x; j < side_n; j += gridDim.x * NT) {
+        const uint32_t g = side_gap[j];
+        const uint32_t o = S[g] + (j - lower_bound_u32(side_gap, side_n, g));
+        store_key<W>(words_new + size_t(o) * W, load_key<W>(side_keys + size_t(j) * W));
+        full_new[o] = side_dist[j] < uint8_t(m) ? 1 : 0;
+        origin[o] = ORIGIN_SIDE | j;
     }
 }
 

@@ -45,6 +45,18 @@ def test_two_ranks_full_expansion_equals_incremental_growth():
 
 
 @pytest.mark.gpu
+def test_incremental_growth_falls_back_collectively():
+    """A buffer bound hit on ONE rank sends every rank to the full expansion for that step (forced on rank 0 every third
+    step); the next step grows incrementally again from the fully assembled space.  Same trajectories."""
+    import json
+
+    out = _launch(3, "cfg1_holstein_L4_d8,square_3x3_d5", 14, 29619, env={"PB200_SHARD_INC_FAIL_EVERY": "3"})
+    rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
+    for v in rep.values():
+        assert v["adapt"]["fallbacks"] >= 3 and v["adapt"]["incremental_steps"] >= 6, rep
+
+
+@pytest.mark.gpu
 def test_three_and_four_ranks_match_oracle():
     _launch(3, "ties_holstein_L5_d6,square_3x3_d5", 25, 29612)
     _launch(4, "cfg2_layout_L16_d16_small,substeps_L4_d4_m1,tb_chain_31", 20, 29613)
