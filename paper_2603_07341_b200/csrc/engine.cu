@@ -1023,6 +1023,7 @@ void Engine::run_step(pb200_diag* out) {
                                 : select(old.words.as<uint32_t>(), c_old, old.n, cfg.q_nom, sel_seed, &n2_pre,
                                          !incremental);
         rec.norm_pre = std::sqrt(n2_pre);
+        bool shard_discard_rides = false;
         bool shard_remapped = false;  // shards: the incremental table growth also remapped the coefficients (into term[0])
         PB_CUDA(cudaEventRecord(ev[1], stream));
         // (the incremental path remaps the coefficients straight into term[0], the first Taylor order's input)
@@ -1086,7 +1087,7 @@ void Engine::run_step(pb200_diag* out) {
                 const size_t ext_bytes = (size_t(next.n) + next.halo_n) * 16 + 16;
                 if (ext_bytes > term[0].cap) sync();  // (the copy of a growing buffer is not stream-ordered)
                 term[0].ensure_keep(ext_bytes, size_t(next.n) * 16);
-                rec.discarded_weight = allreduce_host(read_back<double>(dctl()->out));
+                shard_discard_rides = true;  // (its all-reduce rides on the first Taylor order's)
             } else {
                 term[0].ensure((size_t(next.n) + next.halo_n) * 16 + 16);
                 rec.discarded_weight = remap(old.words.as<uint32_t>(), c_old, old.n, next.words.as<uint32_t>(), next.n,
@@ -1110,7 +1111,8 @@ void Engine::run_step(pb200_diag* out) {
         double ltn = 0, lcn = 0;
         if (sharded) {
             expmv_sharded(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, shard_fused,
-                          shard_fused ? &e : nullptr, shard_fused ? &n2 : nullptr);
+                          shard_fused ? &e : nullptr, shard_fused ? &n2 : nullptr,
+                          shard_discard_rides ? &rec.discarded_weight : nullptr);
         } else {
             try {
                 expmv(next, psi, cfg.dt, cfg.rtol, cfg.max_order, cfg.substeps, &order, &ltn, &lcn, true, incremental);

@@ -281,7 +281,7 @@ struct Engine {
     /// state (*exp_out, *norm2_out; a non-finite coefficient throws) and takes that state from term[0], writing c only
     void expmv_sharded(const Space& sp, double2* c, double dt, double rtol, int max_order, int substeps,
                        int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_first = false,
-                       double* exp_out = nullptr, double* norm2_out = nullptr);
+                       double* exp_out = nullptr, double* norm2_out = nullptr, double* discarded_out = nullptr);
     /// the sharded Taylor orders of sp run on the tile kernels (else: row lists)
     bool shard_tiles(const Space& sp) const { return taylor_tiles_usable(sp.max_row) && !sp.row_lists; }
 

@@ -382,15 +382,17 @@ bool Engine::grow_incremental_sharded(const Space& old, const double2* c_old, ui
     exclusive_scan(vs, uint64_t(n) + 2);
     inc_shard_head_kernel<<<1, 32, 0, stream>>>(n, vs, m, ictr);
     check_launch();
-    const IncHead fin = read_back<IncHead>(&ictr->h);
-    if (fin.overflow) local_fail = true;
     {
         // test hook: rank 0 pretends to have hit a bound on every k-th step (the other ranks must follow it)
         static const char* fe = std::getenv("PB200_SHARD_INC_FAIL_EVERY");
         if (fe != nullptr && rank == 0 && std::atoi(fe) > 0 && steps_done % uint64_t(std::atoi(fe)) == 0) local_fail = true;
     }
-    // any rank's overflow sends every rank to the full path
-    if (allreduce_host_u64(local_fail ? 1 : 0) != 0) return false;
+    // any rank's overflow sends every rank to the full path: the flags are summed on the device, the one read-back of
+    // the phase brings the verdict with the sizes
+    if (local_fail) PB_CUDA(cudaMemsetAsync(&ictr->h.overflow, 1, 4, stream));
+    comm_check(ops.allreduce_u32_dev(ops.user, &ictr->h.overflow, 1, stream), "allreduce_u32_dev(overflow)");
+    const IncHead fin = read_back<IncHead>(&ictr->h);
+    if (fin.overflow != 0) return false;
     if (uint64_t(fin.n_new) > 0x7fffffffull) throw PacesError("subspace growth: table exceeds 2^31 rows (CSR columns are int32)");
     next.words.ensure(size_t(fin.n_new) * W * 4 + 64);
     next.full.ensure(size_t(fin.n_new) + 64);
@@ -577,16 +579,22 @@ void Engine::assemble_sharded(Space& sp, const AsmHint* hint) {
     sp.max_row = width;
     sp.has_h = true;
     sp.val_valid = true;
-    sp.has_code = want_codes && read_back<uint32_t>(fail) == 0;
+    // global sizes and the code-failure verdict: one device all-reduce of three doubles, one read-back
+    shard_sizes_kernel<<<1, 32, 0, stream>>>(n, nnz, want_codes ? fail : nullptr, c->out + 4);
+    check_launch();
+    comm_check(ops.allreduce_f64_dev(ops.user, c->out + 4, 3, stream), "allreduce_f64_dev(sizes)");
+    struct Sizes {
+        double v[3];
+    };
+    const Sizes gs = read_back<Sizes>(c->out + 4);
+    sp.has_code = want_codes && gs.v[2] == 0.0;
     sp.has_move = true;
     // the tile kernels tell rows without / with halo columns apart themselves; the row-list kernels need the lists
     sp.n_interior = sp.n_boundary = 0;
     sp.row_lists = false;
     if (!tiles) classify_rows(sp);
-    uint64_t g[2] = {n, nnz};
-    comm_check(ops.allreduce_u64_host(ops.user, g, 2), "allreduce_u64_host");
-    sp.n_global = g[0];
-    sp.nnz_global = g[1];
+    sp.n_global = uint64_t(gs.v[0]);
+    sp.nnz_global = uint64_t(gs.v[1]);
     require_memory(sp.nnz_global * 2 * 16, "matrix assembly buffer");
     (void)c;
 }
@@ -769,7 +777,7 @@ uint32_t Engine::compact_kept_counted(const uint32_t* d_words, uint32_t n) {
 // ------------------------------------------------------------------------------------------------
 void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rtol, int max_order, int substeps,
                            int* order_used, double* last_term_norm, double* last_c_norm, bool fuse_first, double* exp_out,
-                           double* norm2_out) {
+                           double* norm2_out, double* discarded_out) {
     if (!(dt > 0)) throw PacesError("propagator: dt must be > 0");
     if (!(rtol > 0) || !(rtol < 1)) throw PacesError("propagator: rtol must be in (0, 1)");
     if (max_order < 1) throw PacesError("propagator: max_order must be >= 1");
@@ -796,6 +804,9 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
     double exp_sums[4] = {0, 0, 0, -1};
     PB_CUDA(cudaMemsetAsync(&c->taylor, 0, sizeof(TaylorCtl), stream));
     PB_CUDA(cudaMemsetAsync(c->tsum, 0, sizeof(c->tsum), stream));  // a part that never launches deposits nothing
+    // the remap's discarded weight (Ctl::out[0], this rank's part) rides on the fused first order's all-reduce
+    const bool ride = fuse_first && discarded_out != nullptr;
+    if (ride) PB_CUDA(cudaMemcpyAsync(c->tsum + 14, c->out, sizeof(double), cudaMemcpyDeviceToDevice, stream));
     for (int s = 0; s < substeps; ++s) {
         // (fused first order: the caller left the state in term[0]; the launch writes c_vec, it does not read it)
         if (!(fuse_first && s == 0))
@@ -850,7 +861,7 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
                 }
                 if (mode == TAYLOR_ROWS_DEFER) continue;  // its |term|^2 rides on the next order's all-reduce
                 // (the first order's <x|H|x>, |x|^2 and non-finite count ride on its all-reduce)
-                comm_check(ops.allreduce_f64_dev(ops.user, c->tsum, first ? 14 : 8, stream), "allreduce_f64_dev");
+                comm_check(ops.allreduce_f64_dev(ops.user, c->tsum, first ? (ride ? 15 : 14) : 8, stream), "allreduce_f64_dev");
                 if (mode == TAYLOR_ROWS_CATCHUP)
                     taylor_stop_pair_kernel<<<1, 32, 0, stream>>>(&c->taylor, c->tsum, order, rtol);
                 else
@@ -863,6 +874,7 @@ void Engine::expmv_sharded(const Space& sp, double2* c_vec, double dt, double rt
                 exp_sums[1] = last_ctl.tsum[9] + last_ctl.tsum[12];
                 exp_sums[2] = last_ctl.tsum[10] + last_ctl.tsum[13];
                 exp_sums[3] = 0;
+                if (ride) *discarded_out = last_ctl.tsum[14];
                 // the reference checks its input before it iterates (propagator.hpp:55-57)
                 if (exp_sums[2] != 0.0) throw PacesError("expmv: non-finite input coefficient");
             }

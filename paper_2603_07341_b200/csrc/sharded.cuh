@@ -351,6 +351,14 @@ static __global__ void pick_boundaries_kernel(const uint32_t* __restrict__ scan,
     if (threadIdx.x == 0 && extra != nullptr) out[65] = *extra;
 }
 
+/// (rows, non-zeros, code-failure flag) of this rank as doubles, for one device all-reduce at the end of the assembly.
+static __global__ void shard_sizes_kernel(uint32_t n, uint32_t nnz, const uint32_t* __restrict__ fail, double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    out[0] = double(n);
+    out[1] = double(nnz);
+    out[2] = (fail != nullptr && *fail != 0) ? 1.0 : 0.0;
+}
+
 /// send_idx[found_pos[j]] = answer[j] for found requests (order preserving).
 static __global__ void __launch_bounds__(NT) build_send_list_kernel(const uint32_t* __restrict__ answer,
                                                              const uint32_t* __restrict__ found_pos, uint32_t nr,
