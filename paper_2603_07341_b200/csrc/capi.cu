@@ -640,15 +640,22 @@ int pb200_step_io(pb200_ctx* ctx, const pb200_run_cfg* cfg, uint64_t step_index,
             // uploads first, both on the io stream; the two comparison kernels follow once the Taylor phase is enqueued
             // and wait for its end: the GPU is idle then (the coefficient download is the critical path), while beside
             // the Taylor launches they would take SM slots from the persistent tile kernels
+            // PB200_EARLY_COEFF_UPLOAD=1: both uploads beside the step (the round-2 v1 behaviour); default: only the keys
+            // travel beside the step, the coefficients go up while the result's coefficients come down (the link is full
+            // duplex and the GPU idle), so the Taylor phase shares the device with less DMA traffic
+            static const bool early_coeff = std::getenv("PB200_EARLY_COEFF_UPLOAD") != nullptr;
             auto upload = [&e, flags, coeff, words, rows, W]() {
                 PB_CUDA(cudaMemsetAsync(flags, 0, 8, e.io_stream));
-                PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
+                if (early_coeff)
+                    PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
                 PB_CUDA(cudaMemcpyAsync(e.aux_words.p, words, rows * W * 4, cudaMemcpyHostToDevice, e.io_stream));
             };
             const uint32_t* res_words = res.words.as<uint32_t>();
             const uint32_t* res_coeff = e.coeff[e.ccur].as<uint32_t>();
-            auto compare = [&e, flags, rows, W, res_words, res_coeff](cudaEvent_t after) {
+            auto compare = [&e, flags, coeff, rows, W, res_words, res_coeff](cudaEvent_t after) {
                 if (after) PB_CUDA(cudaStreamWaitEvent(e.io_stream, after, 0));
+                if (!early_coeff)
+                    PB_CUDA(cudaMemcpyAsync(e.aux_coeff.p, coeff, rows * 16, cudaMemcpyHostToDevice, e.io_stream));
                 words_differ_kernel<<<e.grid_for(rows * 4), NT, 0, e.io_stream>>>(e.aux_coeff.as<uint32_t>(), res_coeff,
                                                                                   rows * 4, flags);
                 e.check_launch();
