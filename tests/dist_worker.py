@@ -21,6 +21,17 @@ from paper_2603_07341_b200.dist import NcclComm, TorchComm, gather_state  # noqa
 from cases import CASES  # noqa: E402
 
 
+# shards of more than 65 536 rows: the coarse candidate buckets (sh > 0) and multi-tile scans of the incremental growth
+BIG_CASES = {
+    "big_c2_q2e5": dict(model=dict(kind=1, extents=(16,), eps=(0.0,), hop=(1.0,), omega=(1.0,), g=(1.0,), d_pho=16),
+                        run=dict(init="localized", site=-1, m_init=8, m=2, q_nom=200000, dt=0.05, rtol=1e-15, t_max=50.0,
+                                 seed=7), steps=9),
+    "big_c4_q1e5": dict(model=dict(kind=1, extents=(4, 4, 4), eps=(0.0,), hop=(0.55,), omega=(1.0,), g=(0.71,), d_pho=16),
+                        run=dict(init="localized", site=-1, m_init=5, m=2, q_nom=100000, dt=0.05, rtol=1e-15, t_max=50.0,
+                                 seed=7), steps=7),
+}
+
+
 def close(a, b, rtol=1e-10, atol=0.0):
     return abs(a - b) <= atol + rtol * max(abs(a), abs(b))
 
@@ -36,17 +47,23 @@ def main():
     comm = NcclComm(device=dev) if use_nccl else TorchComm(device=0)
     report = {}
     port = None
-    if rank == 0:
+    if rank == 0 and os.environ.get("PB200_WORKER_REF") != "gpu":
         from oracle import pyoracle
 
         port = pyoracle.load_port()
+    # PB200_WORKER_REF=gpu: the reference trajectory is the single-GPU path of this library (itself pinned to the oracle
+    # by the other tests) instead of the CPU oracle -- sizes the oracle would need minutes for
+    gpu_ref = os.environ.get("PB200_WORKER_REF") == "gpu"
     for name in names:
-        case = CASES[name]
+        case = BIG_CASES[name] if name in BIG_CASES else CASES[name]
         ctx = pb.Context(pb.ModelDef(**case["model"]), device=dev, comm=comm)
         run = ctx.run(**case["run"])
         ro = None
         if rank == 0:
-            ro = port.model(pyoracle.ModelDef(**case["model"])).run(**case["run"])
+            if gpu_ref:
+                ro = pb.Context(pb.ModelDef(**case["model"]), device=dev).run(**case["run"])
+            else:
+                ro = port.model(pyoracle.ModelDef(**case["model"])).run(**case["run"])
         w, c = gather_state(run)
         sizes = []
         if rank == 0:

@@ -57,6 +57,21 @@ def test_incremental_growth_falls_back_collectively():
 
 
 @pytest.mark.gpu
+def test_large_shards_match_single_gpu_path():
+    """Shards of 1e5-1e6 rows (coarse candidate buckets, multi-tile scans, hundreds of thousands of halo columns): two
+    and four ranks against the single-GPU path of the library, tables and coefficients bit for bit at every step."""
+    import json
+
+    out = _launch(2, "big_c2_q2e5", 9, 29620, env={"PB200_WORKER_REF": "gpu"})
+    rep = json.loads(out[out.index("SHARDED_OK ") + len("SHARDED_OK "):].splitlines()[0])
+    assert min(rep["big_c2_q2e5"]["shard_rows"]) > 65536, rep
+    # (while the subspace still grows by more than a quarter per step the incremental growth overflows its side list and
+    # every rank falls back for that step -- as on one GPU; the later steps must take it)
+    assert rep["big_c2_q2e5"]["adapt"]["incremental_steps"] >= 5, rep
+    _launch(4, "big_c4_q1e5", 7, 29621, env={"PB200_WORKER_REF": "gpu"})
+
+
+@pytest.mark.gpu
 def test_three_and_four_ranks_match_oracle():
     _launch(3, "ties_holstein_L5_d6,square_3x3_d5", 25, 29612)
     _launch(4, "cfg2_layout_L16_d16_small,substeps_L4_d4_m1,tb_chain_31", 20, 29613)
