@@ -368,7 +368,7 @@ def main():
         run.reset_times()
         launches0 = ctx.kernel_launches
         single = world == 1 and not args.sharded
-        adapt0 = run.adapt_stats() if single else None
+        adapt0 = run.adapt_stats()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         sampler.start()
@@ -384,7 +384,7 @@ def main():
         dev_ms = ev0.elapsed_time(ev1)
         # ---- everything the line reports about the timed window is read HERE, before any further step
         times = run.times()
-        adapt1 = run.adapt_stats() if single else None
+        adapt1 = run.adapt_stats()
         launches = ctx.kernel_launches - launches0
         rows, nnz, t_now, steps_done = run.info()
         rows_g, nnz_g = run.global_sizes()
@@ -576,7 +576,16 @@ def main():
         phases["note"] = ("grow_ms = the whole incremental adapt phase (expansion + assembly + remap fused into one "
                           "pass over the previous H_eff); expmv_ms includes <H> (first Taylor order); the separate "
                           "assemble/remap/expectation timers are empty on this path and are not reported")
-        if not single or (adapt1 and adapt1["incremental_steps"] == adapt0["incremental_steps"]):
+        inc_in_window = adapt1["incremental_steps"] - adapt0["incremental_steps"]
+        if not single:
+            phases.update({k: times[k] / args.steps for k in ("assemble_ms", "remap_ms", "expectation_ms")})
+            phases["note"] = (
+                "sharded path: grow_ms = incremental table growth over the previous H_eff (halo distances on the halo "
+                "lists, routed frontier keys) incl. the remap; assemble_ms = assembly hinted by the previous H_eff + "
+                "look-up requests / halo plan; <H> rides on the first Taylor order"
+                if inc_in_window else
+                "sharded path, full expansion: grow / assemble / remap / expectation are separate phases")
+        elif inc_in_window == 0:
             phases.update({k: times[k] / args.steps for k in ("assemble_ms", "remap_ms", "expectation_ms")})
             phases["note"] = "full expansion path: grow / assemble / remap / expectation are separate phases"
         line = {
