@@ -263,12 +263,27 @@ static __global__ void __launch_bounds__(NT) assemble_rows_hinted_sharded_kernel
         const Key<W> k = load_key<W>(table + size_t(i) * W);
         const uint32_t org = __ldg(h.origin + i);
         const bool hinted = !(org & ORIGIN_SIDE) && !__ldg(h.touched + org);
-        // the previous row lists, in generator order, the neighbours that were in the previous table (any rank): one
-        // cursor walks it beside the generator
-        uint32_t oe = 0, oend = 0;
+        // the previous row lists the neighbours that were in the previous table (any rank), each tagged with its move
+        // id.  Everything the generator will ask about it is fetched up front with INDEPENDENT loads -- the row's
+        // columns and move ids, then the new indices of its local columns -- so a row costs three exposed latencies,
+        // not one per neighbour
+        uint32_t ni[MAX_ROW];
+        unsigned long long mpack = ~0ull;  // 4-bit move ids of the previous entries (0xf: none)
         if (hinted) {
-            oe = __ldg(h.row_ptr + org);
-            oend = __ldg(h.row_ptr + org + 1);
+            const uint32_t kb = __ldg(h.row_ptr + org);
+            const uint32_t olen = min(__ldg(h.row_ptr + org + 1) - kb, uint32_t(MAX_ROW));
+            uint32_t oc[MAX_ROW];
+#pragma unroll
+            for (int u = 0; u < MAX_ROW; ++u)
+                if (uint32_t(u) < olen) {
+                    oc[u] = uint32_t(__ldg(h.col + kb + u));
+                    mpack = (mpack & ~(0xfull << (4 * u))) | ((unsigned long long)(__ldg(h.move + kb + u) & 0xf) << (4 * u));
+                }
+#pragma unroll
+            for (int u = 0; u < MAX_ROW; ++u) {
+                ni[u] = IDX_NONE;
+                if (uint32_t(u) < olen && oc[u] < h.n_old) ni[u] = __ldg(h.newidx + oc[u]);
+            }
         }
         int len = 0;
         uint32_t* tc = tmp_col + size_t(i) * width;
@@ -277,22 +292,16 @@ static __global__ void __launch_bounds__(NT) assemble_rows_hinted_sharded_kernel
         for_each_neighbor<W>(m, k, true, [&](int move, const Key<W>& kk, double amp, bool is_diag) {
             uint32_t pos = i;
             bool keep = true;
-            bool was = false;  // hinted rows: this neighbour had an entry in the previous row
-            uint32_t ocol = 0;
-            if (hinted && oe < oend && int(__ldg(h.move + oe)) == move) {
-                was = true;
-                ocol = uint32_t(__ldg(h.col + oe));
-                ++oe;
-            }
             if (!is_diag) {
                 const uint32_t dest = neighbor_owner<W>(m, move, kk, rank, P);
                 if (dest == rank) {
                     if (hinted) {
-                        keep = false;
-                        if (was) {
-                            pos = __ldg(h.newidx + ocol);
-                            keep = pos != IDX_NONE;
-                        }
+                        // the previous entry with this move id, if any (a local neighbour: its column was local)
+                        pos = IDX_NONE;
+#pragma unroll
+                        for (int u = 0; u < MAX_ROW; ++u)
+                            if (int((mpack >> (4 * u)) & 0xf) == move) pos = ni[u];
+                        keep = pos != IDX_NONE;
                     } else {
                         keep = find_row_in4<W>(table, 0, n, kk, pos);
                     }
