@@ -112,9 +112,14 @@ typedef struct pb200_comm_ops {
     void* user;
     int (*allreduce_f64_host)(void* user, double* buf, uint64_t n);          /* sum, in place */
     int (*allreduce_u64_host)(void* user, uint64_t* buf, uint64_t n);        /* sum, in place */
-    int (*alltoall_u64_host)(void* user, const uint64_t* send, uint64_t* recv); /* one value per peer */
+    /* one value per peer.  Not called any more: the per-peer counts of a routed exchange travel on the device
+     * (alltoallv_dev with one 4-byte element per peer) and come back in one read-back; the slot stays for ABI
+     * compatibility and must still be non-NULL. */
+    int (*alltoall_u64_host)(void* user, const uint64_t* send, uint64_t* recv);
     int (*allgather_host)(void* user, const void* send, uint64_t nbytes, void* recv); /* recv: world * nbytes */
-    /* buckets are contiguous and in rank order on both sides; counts are in elements of elem_bytes bytes */
+    /* buckets are contiguous and in rank order on both sides; counts are in elements of elem_bytes bytes (1 for the BFS
+     * distances of the halo rows, 4 for counts and look-up replies, 4 * words for keys, 16 for complex128 halos);
+     * the device pointers need no alignment beyond elem_bytes */
     int (*alltoallv_dev)(void* user, const void* send, const uint64_t* send_counts, void* recv,
                          const uint64_t* recv_counts, uint64_t elem_bytes, void* stream);
     int (*allreduce_f64_dev)(void* user, double* buf, uint64_t n, void* stream);   /* sum, in place */
