@@ -45,6 +45,12 @@ def test_two_ranks_full_expansion_equals_incremental_growth():
 
 
 @pytest.mark.gpu
+def test_two_ranks_incremental_growth_without_assembly_hint():
+    """PB200_NO_ASSEMBLY_HINT=1: the table grows incrementally, every row of it is assembled by key search."""
+    _launch(2, "cfg1_holstein_L4_d8,disordered_4x3_d7", 12, 29622, env={"PB200_NO_ASSEMBLY_HINT": "1"})
+
+
+@pytest.mark.gpu
 def test_incremental_growth_falls_back_collectively():
     """A buffer bound hit on ONE rank sends every rank to the full expansion for that step (forced on rank 0 every third
     step); the next step grows incrementally again from the fully assembled space.  Same trajectories."""
