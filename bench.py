@@ -416,7 +416,7 @@ def main():
 
         # ---- e2e: paces::step with a host SparseState in and out, every step (pinned host buffers)
         e2e = e2e_miss = None
-        if not args.no_e2e and single:
+        if not args.no_e2e:
             rows_now = run.info()[0]
             cap = int(rows_now * 1.25) + 1024
             hw = [torch.empty(cap * W, dtype=torch.int32).pin_memory() for _ in range(2)]
@@ -460,13 +460,32 @@ def main():
                         "d2h_bytes_per_step": d2h // k_e2e, "steps": k_e2e, "rows": n_cur}
 
             k_e2e = max(5, min(args.steps, 20))
-            e2e = measure(False, k_e2e)
-            e2e["api"] = ("pb200_step_io (paces::step on a host SparseState in pinned buffers, every byte uploaded and "
-                          "downloaded every step; the uploads are compared on the device with the resident result of "
-                          "the previous call and, when identical, the step reuses the resident H_eff)")
-            e2e_miss = measure(True, max(3, k_e2e // 2))
-            e2e_miss["api"] = ("the same call with PB200_NO_STEP_CACHE=1: nothing resident is reused, the subspace is "
-                               "rebuilt from the uploaded table every step (full expansion + assembly)")
+            if single:
+                e2e = measure(False, k_e2e)
+                e2e["api"] = ("pb200_step_io (paces::step on a host SparseState in pinned buffers, every byte uploaded "
+                              "and downloaded every step; the uploads are compared on the device with the resident "
+                              "result of the previous call and, when identical, the step reuses the resident H_eff)")
+                e2e_miss = measure(True, max(3, k_e2e // 2))
+                e2e_miss["api"] = ("the same call with PB200_NO_STEP_CACHE=1: nothing resident is reused, the subspace "
+                                   "is rebuilt from the uploaded table every step (full expansion + assembly)")
+            else:
+                # shards: every rank hands its rows of the state in and takes its rows of the result out, every step
+                # (collective call; nothing resident is reused across calls, so each step is a full expansion)
+                try:
+                    e2e = measure(True, max(3, k_e2e // 2))
+                    h2d_t = torch.tensor([e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"], e2e["rows"]],
+                                         dtype=torch.float64)
+                    if world > 1:
+                        dist.all_reduce(h2d_t)
+                        v = torch.tensor([e2e["value"]], dtype=torch.float64)
+                        dist.all_reduce(v, op=dist.ReduceOp.MIN)  # the slowest rank's clock
+                        e2e["value"] = float(v.item())
+                    e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"], e2e["rows"] = (int(x) for x in h2d_t.tolist())
+                    e2e["api"] = ("pb200_step_io on every rank with its rows of the host SparseState (pinned buffers, "
+                                  "bytes summed over the ranks); no resident state is reused on shards: upload, full "
+                                  "expansion + assembly, evolve, download")
+                except Exception as ex:  # a rank without rows cannot call the host-buffer step
+                    e2e = {"unavailable": str(ex)[:200]}
 
         # clocks: keep the same loop running for ~1 s so NVML (10 ms period) sees them under this load; the count is
         # derived from the all-reduced step time so every rank runs the same number of (collective) steps

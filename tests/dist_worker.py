@@ -86,6 +86,21 @@ def main():
                     assert close(d[k], do[k]), (name, s, k, d[k], do[k])
                 assert close(d["energy"], do["energy"], 1e-10, 1e-12), (name, s, d["energy"], do["energy"])
                 assert close(d["discarded_weight"], do["discarded_weight"], 1e-9, 1e-30), (name, s)
+        # the host-buffer step on shards (collective): every rank hands in its rows of the state and the result must be
+        # the next step of the trajectory (only when every rank has rows: the call rejects an empty state)
+        lw, lc = run.state()
+        nloc = [None] * world
+        dist.all_gather_object(nloc, len(lc))
+        if min(nloc) > 0 and not gpu_ref:
+            _, _, t_now, sd_now = run.info()
+            kw = {k: v for k, v in case["run"].items() if k not in ("init", "site")}
+            ctx.step(np.ascontiguousarray(lw), np.ascontiguousarray(lc), t_now, sd_now + 1, **kw)
+            w, c = gather_state(run)
+            if rank == 0:
+                ro.step()
+                wo, co = ro.state()
+                assert np.array_equal(w, wo), (name, "host-buffer step: table")
+                assert c.tobytes() == co.tobytes(), (name, "host-buffer step: coefficients not bit-identical")
         ob = run.observe()
         if rank == 0:
             oo = ro.observe()
