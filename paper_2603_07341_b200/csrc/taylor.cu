@@ -279,6 +279,9 @@ __global__ void __launch_bounds__(NT, 6) taylor_catchup_kernel(uint32_t n, const
 // warp releases a stage with one mbarrier arrive.  Every mode runs on the same persistent grid, so SINGLE / DEFER /
 // CATCHUP / FIRST share one reduction shape.
 // ================================================================================================
+/// PB200_TAYLOR_ONE_WAY=1: every order walks the rows upwards (A/B for the alternating sweep of the tile kernels).
+static const bool g_alternate = std::getenv("PB200_TAYLOR_ONE_WAY") == nullptr;
+
 namespace tile {
 
 #ifndef TILE_TR
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                                                                double* __restrict__ partials, TaylorCtl* ctl,
                                                                int ignore_stop, double* __restrict__ tot_out,
                                                                double* __restrict__ expect_out, int first_from_x,
-                                                               int part) {
+                                                               int part, int reverse) {
     constexpr bool HAS_C = MODE != DEFER;
     constexpr int K = mode_sums<MODE>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -549,6 +552,9 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
     uint64_t* empty = full + STAGES;
     double* red = reinterpret_cast<double*>(smem + L.bars + 2 * STAGES * 8);
     const uint32_t ntiles = (n + TR - 1) / TR;
+    // Sweep direction: consecutive orders walk the rows in OPPOSITE directions.  The vector an order gathers is the one
+    // the previous order wrote; the rows that launch wrote last are the ones still in L2, so this launch starts there.
+    auto tile_of = [&](uint32_t t) { return reverse ? ntiles - 1 - t : t; };
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -571,20 +577,20 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         // boundaries of the NEXT tile are requested one iteration ahead (two dependent global loads otherwise)
         uint32_t e0n = 0, e1n = 0;
         if (t < ntiles) {
-            e0n = __ldg(row_ptr + size_t(t) * TR);
-            e1n = __ldg(row_ptr + min(size_t(t + 1) * TR, size_t(n)));
+            e0n = __ldg(row_ptr + size_t(tile_of(t)) * TR);
+            e1n = __ldg(row_ptr + min(size_t(tile_of(t) + 1) * TR, size_t(n)));
         }
         for (uint32_t j = 0; t < ntiles; ++j, t += gridDim.x) {
             const int s = int(j % STAGES);
             const uint32_t e0 = e0n, e1 = e1n;
             const uint32_t tn = t + gridDim.x;
             if (tn < ntiles) {
-                e0n = __ldg(row_ptr + size_t(tn) * TR);
-                e1n = __ldg(row_ptr + min(size_t(tn + 1) * TR, size_t(n)));
+                e0n = __ldg(row_ptr + size_t(tile_of(tn)) * TR);
+                e1n = __ldg(row_ptr + min(size_t(tile_of(tn) + 1) * TR, size_t(n)));
             }
             if (j >= STAGES) mbar_wait(empty + s, ((j / STAGES) - 1) & 1);
             unsigned char* st = smem + size_t(s) * L.stage_bytes;
-            const uint32_t r0 = t * TR;
+            const uint32_t r0 = tile_of(t) * TR;
             const uint32_t rows = min(uint32_t(TR), n - r0);
             const uint32_t rp_bytes = ((rows + 1 + 3) & ~3u) * 4;
             const uint32_t a0 = e0 & ~AL;
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         const int32_t* col_s = reinterpret_cast<const int32_t*>(st + L.col);
         const double* val_s = reinterpret_cast<const double*>(st + L.val);
         const uint16_t* code_s = reinterpret_cast<const uint16_t*>(st + L.val);
-        const uint32_t i = t * TR + tid;
+        const uint32_t i = tile_of(t) * TR + tid;
         const bool live = i < n;
         // independent of the ring: this row's slice of c and (catch-up / first order) of the previous term
         double2 cc = make_double2(0.0, 0.0), tp = make_double2(0.0, 0.0);
@@ -703,7 +709,8 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
     taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
-        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0);
+        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0,
+        g_alternate ? (order & 1) : 0);
     return true;
 }
 
@@ -768,7 +775,8 @@ static bool launch_shard_r(int part, int sm_count, cudaStream_t stream, uint32_t
         1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>()) * SHARD_WAVES));
     taylor_tile_kernel<MODE, MAXR, CODED, true><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
-        vt_n, term_in, term_out, c, b, order, 0.0, MAXR, partials, ctl, 0, tot_out, expect_out, first_from_x, part);
+        vt_n, term_in, term_out, c, b, order, 0.0, MAXR, partials, ctl, 0, tot_out, expect_out, first_from_x, part,
+        g_alternate ? (order & 1) : 0);
     return true;
 }
 template <int MODE>
