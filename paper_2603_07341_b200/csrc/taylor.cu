@@ -279,8 +279,19 @@ __global__ void __launch_bounds__(NT, 6) taylor_catchup_kernel(uint32_t n, const
 // warp releases a stage with one mbarrier arrive.  Every mode runs on the same persistent grid, so SINGLE / DEFER /
 // CATCHUP / FIRST share one reduction shape.
 // ================================================================================================
-/// PB200_TAYLOR_ONE_WAY=1: every order walks the rows upwards (A/B for the alternating sweep of the tile kernels).
+/// Alternating sweep of the tile kernels (see taylor_tile_kernel): pays when the gathered vector fits the L2 -- C2, 53 MB:
+/// expmv -2.2 % -- and costs when it does not (3e7 rows, 480 MB: +2.2 %, a downward sweep is the slower direction
+/// for DRAM), so it is used for vectors up to the L2 size.  PB200_TAYLOR_ONE_WAY=1: never (A/B measurements).
 static const bool g_alternate = std::getenv("PB200_TAYLOR_ONE_WAY") == nullptr;
+static int sweep_reverse(uint32_t n, int order) {
+    static const size_t l2_bytes = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) != cudaSuccess)
+            cudaGetLastError();
+        return size_t(v > 0 ? v : 0);
+    }();
+    return (g_alternate && size_t(n) * 16 <= l2_bytes) ? (order & 1) : 0;
+}
 
 namespace tile {
 
@@ -710,7 +721,7 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
     taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
         vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0,
-        g_alternate ? (order & 1) : 0);
+        sweep_reverse(n, order));
     return true;
 }
 
@@ -776,7 +787,7 @@ static bool launch_shard_r(int part, int sm_count, cudaStream_t stream, uint32_t
     taylor_tile_kernel<MODE, MAXR, CODED, true><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
         vt_n, term_in, term_out, c, b, order, 0.0, MAXR, partials, ctl, 0, tot_out, expect_out, first_from_x, part,
-        g_alternate ? (order & 1) : 0);
+        sweep_reverse(n, order));
     return true;
 }
 template <int MODE>
