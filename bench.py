@@ -251,7 +251,13 @@ def reference_arm(args):
 def spawn_ranks(n):
     """`python bench.py --gpus N` without a torchrun environment: one process per GPU, rank 0's JSON line on stdout."""
     import socket
+    import time
 
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n and not os.environ.get("PB200_BENCH_SAME_DEVICE"):
+        raise SystemExit("bench.py: --gpus %d needs %d CUDA devices, this node has %d (one process per GPU)" % (n, n, have))
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -262,9 +268,20 @@ def spawn_ranks(n):
                    MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
                                       stdout=None if r == 0 else subprocess.DEVNULL))
+    # a rank that dies (before or inside a collective) takes the job down instead of leaving its peers waiting
     rc = 0
-    for p in procs:
-        rc = rc or p.wait()
+    live = list(procs)
+    while live and rc == 0:
+        time.sleep(0.2)
+        for p in list(live):
+            code = p.poll()
+            if code is not None:
+                live.remove(p)
+                rc = rc or code
+    for p in live:
+        p.kill()
+    for p in live:
+        p.wait()
     raise SystemExit(rc)
 
 
@@ -324,6 +341,9 @@ def main():
         raise SystemExit("bench.py: no CUDA device; the B200 path has no CPU fallback (use --impl reference)")
     if os.environ.get("PB200_BENCH_SAME_DEVICE"):  # test hook: several ranks on one GPU (needs the gloo transport)
         local = 0
+    if local >= torch.cuda.device_count():
+        raise SystemExit("bench.py: rank %d wants cuda:%d, this node has %d CUDA device(s) (one process per GPU)"
+                         % (rank, local, torch.cuda.device_count()))
     torch.cuda.set_device(local)
     import paper_2603_07341_b200 as pb
 
