@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <stdexcept>
+#include <string>
 
 #include "primitives.cuh"
 
@@ -551,11 +553,11 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
     constexpr bool HAS_C = MODE != DEFER;
     constexpr int K = mode_sums<MODE>();
     extern __shared__ __align__(128) unsigned char smem[];
-    if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
-    if (MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
-        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
-        return;
-    }
+    // Programmatic dependent launch (launch_r): the NEXT order's CTAs may become resident as this order's CTAs retire and
+    // run their prologue (barrier init, value table) there; they touch nothing this order writes -- the stop flags
+    // included -- before griddepcontrol.wait below, which returns once the previous grid has completed and flushed.
+    // Both instructions do nothing in a launch without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;");
     constexpr int STAGES = stages<CODED>();
     constexpr uint32_t AL = CODED ? 7u : 3u;  // the slices start at a 16-byte boundary of the narrowest array
     const Layout L = make_layout<CODED>(max_row, vt_n);
@@ -580,6 +582,12 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         for (int q = int(tid); q < vt_n; q += NTHREADS) vt_w[q] = __ldg(vtab + q);
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
+    if (MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
+        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
+        return;
+    }
 
     if (tid >= TR) {
         // ---------------- producer warp: one lane streams the tiles of this CTA into the ring ----------------
@@ -718,10 +726,26 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
     const uint32_t ntiles = (n + TR - 1) / TR;
     const uint32_t grid =
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
-    taylor_tile_kernel<MODE, MAXR, CODED><<<grid, NTHREADS, L.total, stream>>>(
-        n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
-        vt_n, term_in, term_out, c, b, order, rtol, MAXR, partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0,
-        sweep_reverse(n, order));
+    // consecutive orders as programmatic dependent launches (see the kernel's prologue); PB200_NO_PDL=1: plain launches
+    static const bool pdl = std::getenv("PB200_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const uint16_t* code_p = CODED ? codes->code : nullptr;
+    const double* diag_p = CODED ? codes->diag : nullptr;
+    const double* vtab_p = CODED ? codes->vtab : nullptr;
+    const cudaError_t err = cudaLaunchKernelEx(&cfg, taylor_tile_kernel<MODE, MAXR, CODED>, n, row_ptr, col, val, code_p,
+                                               diag_p, vtab_p, vt_n, term_in, term_out, c, b, order, rtol, int(MAXR),
+                                               partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0,
+                                               int(sweep_reverse(n, order)));
+    if (err != cudaSuccess) throw std::runtime_error(std::string("taylor_tile_kernel launch: ") + cudaGetErrorString(err));
     return true;
 }
 
