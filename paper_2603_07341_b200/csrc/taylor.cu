@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                                                                double* __restrict__ partials, TaylorCtl* ctl,
                                                                int ignore_stop, double* __restrict__ tot_out,
                                                                double* __restrict__ expect_out, int first_from_x,
-                                                               int part, int reverse) {
+                                                               int part, int reverse, int prefetch) {
     constexpr bool HAS_C = MODE != DEFER;
     constexpr int K = mode_sums<MODE>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -582,34 +582,25 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
         for (int q = int(tid); q < vt_n; q += NTHREADS) vt_w[q] = __ldg(vtab + q);
     }
     __syncthreads();
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (!ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail))) return;
-    if (MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
-        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
-        return;
-    }
 
-    if (tid >= TR) {
-        // ---------------- producer warp: one lane streams the tiles of this CTA into the ring ----------------
-        if (tid != TR) return;
-        uint32_t t = blockIdx.x;
-        // boundaries of the NEXT tile are requested one iteration ahead (two dependent global loads otherwise)
-        uint32_t e0n = 0, e1n = 0;
-        if (t < ntiles) {
-            e0n = __ldg(row_ptr + size_t(tile_of(t)) * TR);
-            e1n = __ldg(row_ptr + min(size_t(tile_of(t) + 1) * TR, size_t(n)));
-        }
-        for (uint32_t j = 0; t < ntiles; ++j, t += gridDim.x) {
-            const int s = int(j % STAGES);
+    // ---------------- producer (one lane of the last warp) streams the tiles of this CTA into the ring ----------------
+    // Its state lives here because it runs in two parts: with `prefetch` (an order whose predecessor in the stream is the
+    // previous order of the same series: the matrix is read-only there) the first STAGES tiles are requested BEFORE
+    // griddepcontrol.wait, i.e. while the previous order's last CTAs are still running; the rest after the role split.
+    uint32_t pt = blockIdx.x, pj = 0;
+    uint32_t e0n = 0, e1n = 0;  // boundaries of the NEXT tile, requested one iteration ahead (two dependent loads otherwise)
+    auto produce = [&](uint32_t jmax) {
+        for (; pt < ntiles && pj < jmax; ++pj, pt += gridDim.x) {
+            const int s = int(pj % STAGES);
             const uint32_t e0 = e0n, e1 = e1n;
-            const uint32_t tn = t + gridDim.x;
+            const uint32_t tn = pt + gridDim.x;
             if (tn < ntiles) {
                 e0n = __ldg(row_ptr + size_t(tile_of(tn)) * TR);
                 e1n = __ldg(row_ptr + min(size_t(tile_of(tn) + 1) * TR, size_t(n)));
             }
-            if (j >= STAGES) mbar_wait(empty + s, ((j / STAGES) - 1) & 1);
+            if (pj >= STAGES) mbar_wait(empty + s, ((pj / STAGES) - 1) & 1);
             unsigned char* st = smem + size_t(s) * L.stage_bytes;
-            const uint32_t r0 = tile_of(t) * TR;
+            const uint32_t r0 = tile_of(pt) * TR;
             const uint32_t rows = min(uint32_t(TR), n - r0);
             const uint32_t rp_bytes = ((rows + 1 + 3) & ~3u) * 4;
             const uint32_t a0 = e0 & ~AL;
@@ -624,6 +615,29 @@ __global__ void __launch_bounds__(NTHREADS, tile_ctas_per_sm<MAXR>()) taylor_til
                     bulk_load(st + L.val, val + a0, cnt * 8, full + s);
             }
         }
+    };
+    if (tid == TR) {
+        if (pt < ntiles) {
+            e0n = __ldg(row_ptr + size_t(tile_of(pt)) * TR);
+            e1n = __ldg(row_ptr + min(size_t(tile_of(pt) + 1) * TR, size_t(n)));
+        }
+        if (prefetch) produce(STAGES);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    bool quit = !ignore_stop && (ld_flag(&ctl->done) | ld_flag(&ctl->bail));
+    if (!quit && MODE == DEFER && ld_flag(&ctl->streak) != 0) {  // the series may stop at this order: it has to run SINGLE
+        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)&ctl->bail = order;
+        quit = true;
+    }
+    if (quit) {
+        // the shared memory must outlive the bulk copies already under way
+        if (tid == TR)
+            for (uint32_t q = 0; q < pj; ++q) mbar_wait(full + q, 0);
+        return;
+    }
+
+    if (tid >= TR) {
+        if (tid == TR) produce(0xffffffffu);
         return;
     }
 
@@ -728,6 +742,11 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
         std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sm_count) * uint32_t(tile_ctas_per_sm<MAXR>())));
     // consecutive orders as programmatic dependent launches (see the kernel's prologue); PB200_NO_PDL=1: plain launches
     static const bool pdl = std::getenv("PB200_NO_PDL") == nullptr;
+    // orders >= 2 follow the previous order of the same series in the stream: H_eff is read-only between them, so the
+    // producer MAY request its first tiles before the previous order has completed.  Measured: no gain (C2 expmv 0.614
+    // either way, C4 2.22 vs 2.23 ms; profiles/r2_experiments.md), so it is off unless PB200_PDL_PREFETCH=1.
+    static const bool pre = std::getenv("PB200_PDL_PREFETCH") != nullptr;
+    const int prefetch = pdl && pre && MODE != FIRST && order >= 2 ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NTHREADS);
@@ -744,7 +763,7 @@ static bool launch_r(int sm_count, cudaStream_t stream, uint32_t n, const uint32
     const cudaError_t err = cudaLaunchKernelEx(&cfg, taylor_tile_kernel<MODE, MAXR, CODED>, n, row_ptr, col, val, code_p,
                                                diag_p, vtab_p, vt_n, term_in, term_out, c, b, order, rtol, int(MAXR),
                                                partials, ctl, ignore_stop, tot_out, expect_out, first_from_x, 0,
-                                               int(sweep_reverse(n, order)));
+                                               int(sweep_reverse(n, order)), prefetch);
     if (err != cudaSuccess) throw std::runtime_error(std::string("taylor_tile_kernel launch: ") + cudaGetErrorString(err));
     return true;
 }
@@ -811,7 +830,7 @@ static bool launch_shard_r(int part, int sm_count, cudaStream_t stream, uint32_t
     taylor_tile_kernel<MODE, MAXR, CODED, true><<<grid, NTHREADS, L.total, stream>>>(
         n, row_ptr, col, val, CODED ? codes->code : nullptr, CODED ? codes->diag : nullptr, CODED ? codes->vtab : nullptr,
         vt_n, term_in, term_out, c, b, order, 0.0, MAXR, partials, ctl, 0, tot_out, expect_out, first_from_x, part,
-        sweep_reverse(n, order));
+        sweep_reverse(n, order), 0);
     return true;
 }
 template <int MODE>
