@@ -20,8 +20,9 @@ print("# cuobjdump -sass of the tile Taylor kernels (taylor.cu, namespace tile),
 print("# taylor_tile_kernel<MODE, MAXR, CODED, SHARD>: MODE 0 SINGLE, 1 FIRST, 2 DEFER, 3 CATCHUP; MAXR = row-length bound;")
 print("# SHARD 1 = a rank's rows of a sharded space (row filter by halo columns, sums deposited for the all-reduce);")
 print("# CODED 1 = 2-byte value codes + shared-memory table.  UBLKCP = cp.async.bulk (bulk copy global -> shared),")
+print("# PREEXIT / ACQBULK = griddepcontrol.launch_dependents / griddepcontrol.wait (programmatic dependent launch),")
 print("# SYNCS = mbarrier operations, LDG = gathers of x / c / previous term, LDS = slices + value table")
-ops = ["UBLKCP", "SYNCS", "LDG", "LDS", "STG", "DMUL", "DADD", "DFMA", "BAR"]
+ops = ["UBLKCP", "SYNCS", "PREEXIT", "ACQBULK", "LDG", "LDS", "STG", "DMUL", "DADD", "DFMA", "BAR"]
 for fn, lines in funcs.items():
     m = re.search(r"taylor_tile_kernelILi(\d)ELi(\d)ELb([01])ELb([01])E", fn)
     if not m:
